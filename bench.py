@@ -1,0 +1,317 @@
+"""Benchmark: sub-sampled Hessian-vector products/s at CIFAR-10 shape
+(BASELINE.json metric; configs[2]: 50k x 3072, C=10, 5% Hessian sample).
+
+One step = one outer iteration's sampled-Hessian work on fresh inputs:
+snx_hess_prepare on a new S_H (rows gathered from the 1.23 GB X in HBM) and a
+device CG solve (theta=1e-4, <=10 Hessian products, reference cg.py).
+value = Hessian products applied / device time.  Also reported: e2e through
+the public numpy API (host buffers, H2D/D2H in the timed region), the
+roofline of the Hessian product, a CPU baseline (the oracle port on this
+host), and time-to-tolerance of a full newton_solve.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+N, P, C = 50000, 3072, 10
+F_H, LAM, THETA, T_CG = 0.05, 1e-3, 1e-4, 10
+METRIC = "subsampled Hessian-vector products/s (CIFAR-10 shape, 5% sample)"
+UNIT = "Hv/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index, self.samples, self._stop = index, [], threading.Event()
+        self._t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                    timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": float(self.samples[0][1]) if self.samples else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def make_problem(seed=0):
+    import oracle  # synthetic data generator only (the checker's data recipe)
+
+    return oracle.synthetic_problem(N, P, C, seed=seed)
+
+
+def cpu_baseline(A, y, x, steps_budget_s=12.0, max_steps=50):
+    """The oracle port (numpy/OpenBLAS fp64) on the same step: h-prep on a fresh
+    S_H + CG with <= 10 Hessian products; bounded to ~steps_budget_s."""
+    import oracle
+
+    g = oracle.grad(A, y, C, x, LAM)
+    hv, t_total, steps = 0, 0.0, 0
+    while steps < max_steps and t_total < steps_budget_s:
+        s_h = oracle.draw_samples(1.0, F_H, False, 0, N, 1000 + steps)[1]
+        t0 = time.perf_counter()
+        Ah, yh = A[s_h], y[s_h]
+        h = oracle.hess_probs(Ah, yh, C, x)
+        count = [0]
+
+        def op(v):
+            count[0] += 1
+            return oracle.hess_apply(Ah, h, C, v, N / len(s_h), LAM)
+
+        oracle.cg(op, g, THETA, T_CG)
+        t_total += time.perf_counter() - t0
+        hv += count[0]
+        steps += 1
+    return {"value": hv / t_total, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+            "sample": f"{steps} steps (S_H gather + h-prep + CG, {hv} Hv) of the CIFAR-shape "
+                      f"workload, numpy/OpenBLAS fp64, {t_total:.1f} s"}
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    A, y = make_problem()
+    x = 0.01 * np.random.default_rng(7).standard_normal((C - 1) * P)
+    import oracle
+
+    g = oracle.grad(A, y, C, x, LAM)
+    for w in range(args.warmup):
+        s_h = oracle.draw_samples(1.0, F_H, False, 0, N, w)[1]
+        h = oracle.hess_probs(A[s_h], y[s_h], C, x)
+        oracle.hess_apply(A[s_h], h, C, g, N / len(s_h), LAM)
+    hv, t = 0, 0.0
+    for k in range(args.steps):
+        s_h = oracle.draw_samples(1.0, F_H, False, 0, N, 100 + k)[1]
+        t0 = time.perf_counter()
+        Ah, yh = A[s_h], y[s_h]
+        h = oracle.hess_probs(Ah, yh, C, x)
+        cnt = [0]
+
+        def op(v):
+            cnt[0] += 1
+            return oracle.hess_apply(Ah, h, C, v, N / len(s_h), LAM)
+
+        oracle.cg(op, g, THETA, T_CG)
+        t += time.perf_counter() - t0
+        hv += cnt[0]
+    v = hv / t
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": "cifar10-shape 50000x3072 C=10, 5% S_H",
+                                        "n": N, "p": P, "C": C, "hessian_fraction": F_H},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
+                         "sample": f"{args.steps} steps, oracle port (numpy/OpenBLAS fp64)"},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }))
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1802_09113_b200 as snx
+    from paper_1802_09113_b200 import _lib, cg as cgmod, softmax
+    from paper_1802_09113_b200.device import ptr, stream_handle
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+
+    A, y = make_problem()
+    x_host = 0.01 * np.random.default_rng(7).standard_normal((C - 1) * P)
+    ds = snx.DeviceDataset.from_numpy(A, y, C, dtype=args.dtype)
+    prob = snx.SoftmaxProblem(ds, LAM)
+    dev = torch.device("cuda", local)
+    x = torch.from_numpy(x_host).to(dev)
+    g, _ = softmax.gradient_parts(ds, x, 1.0, LAM)
+    total = args.warmup + args.steps
+    # inputs of every step (fresh S_H per step) resident before timing
+    views = [ds.take(snx.draw_samples(snx.SampleConfig(1.0, F_H), N, k)[1]) for k in range(total)]
+    m = views[0].n_rows
+    cgws = cgmod.CgWorkspace(ds.dim, T_CG, dev)
+    ops = [None] * total
+    iters = torch.zeros(total, dtype=torch.float64, device=dev)
+
+    def step(k):
+        op = softmax.HessianOperator(views[k], x, LAM, scale=N / m)
+        ops[k] = op
+        cgmod.enqueue_cg(op, g, THETA, T_CG, cgws)
+        iters[k:k + 1].copy_(cgws.slot(T_CG)[3:4])
+
+    for k in range(args.warmup):
+        step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record(st)
+        for k in range(args.warmup, total):
+            step(k)
+        e1.record(st)
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t)
+    hv_count = int(iters[args.warmup:].sum())
+    value = hv_count / (ms / 1e3)
+
+    # ---- roofline of the dominant op: one Hessian product (snx_hess_apply)
+    op = ops[-1]
+    v = g.clone()
+    out = torch.empty_like(v)
+    reps = 50
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    for _ in range(5):
+        op.apply_into(v, out)
+    torch.cuda.synchronize()
+    ev[0].record(st)
+    for _ in range(reps):
+        op.apply_into(v, out)
+    ev[1].record(st)
+    torch.cuda.synchronize()
+    hv_ms = ev[0].elapsed_time(ev[1]) / reps
+    tb = 8 if args.dtype == "f64" else 4
+    alg_bytes = m * P * tb + m * (C - 1) * tb + 2 * ds.dim * 8
+    pk, pk_kind = peaks()
+    achieved = alg_bytes / (hv_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "kernel": "snx_hess_apply (rowpass GEMM1+ComputeU, xtu GEMM2, finalize)",
+                "peak_kind": pk_kind, "ms_per_launch": hv_ms,
+                "flops_per_launch": 4 * m * P * (C - 1),
+                "note": "X_S rows re-read from L2 across CG iterations; bytes counted once"}
+
+    # ---- e2e: the public numpy API, host buffers in and out
+    g_host = g.cpu().numpy()
+    cfg = snx.CgConfig(THETA, T_CG)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    e2e_hv = 0
+    e2e_steps = max(3, min(args.steps, 20))
+    for k in range(e2e_steps):
+        orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, F_H), 500 + k)
+        rep = snx.cg_solve(orc.hessian_operator(x_host), g_host, cfg)
+        e2e_hv += rep.iterations
+    e2e_s = time.perf_counter() - t0
+    e2e = {"value": e2e_hv / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": 2 * ds.dim * 8 + m * 8,
+           "d2h_bytes_per_step": ds.dim * 8 + 8 * 8}
+
+    # ---- time-to-tolerance of one full Newton solve (device resident)
+    solve = None
+    if not args.skip_solve:
+        from paper_1802_09113_b200.device import dot
+
+        gz = softmax.gradient_parts(ds, torch.zeros_like(x), 1.0, LAM)[0]
+        g0 = math.sqrt(float(dot(gz, gz)))
+        ncfg = snx.make_variant("subsampled-100", snx.NewtonConfig(
+            epsilon=1e-6 * g0, max_outer_iters=100))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr = snx.newton_solve(prob, ncfg, x0=torch.zeros_like(x))
+        torch.cuda.synchronize()
+        solve = {"time_to_tol_s": time.perf_counter() - t0, "outer_iters": tr.iterations,
+                 "reason": tr.reason, "final_objective": tr.final_objective,
+                 "cg_iters": [r.cg_iters for r in tr.records[1:]],
+                 "epsilon": 1e-6 * g0}
+
+    cpu = cpu_baseline(A, y, x_host) if (rank == 0 and world == 1 and not args.skip_cpu) \
+        else None
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": args.dtype, "data": "synthetic",
+            "config": {"workload": "cifar10-shape 50000x3072 C=10, 5% S_H (m=2500)",
+                       "n": N, "p": P, "C": C, "hessian_fraction": F_H, "lam": LAM,
+                       "theta": THETA, "cg_max_iters": T_CG, "parallelism": f"rows/{world}",
+                       "l2": "inputs > L2: 1.23 GB X in HBM, fresh S_H gathered every step"},
+            "hv_applied": hv_count, "gpu_launches": args.steps * (3 + 5 * T_CG),
+            "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
+            "cpu_baseline": cpu, "newton_solve": solve,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-solve", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

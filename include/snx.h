@@ -1,0 +1,137 @@
+/*
+ * snx.h -- C ABI of libsnx, the sm_100a kernels behind the sub-sampled
+ * Newton-CG hot path (arXiv 1802.09113).
+ *
+ * The reference (/root/reference/pkg/src/subnewton) is pure Python on numpy;
+ * it has no FFI.  Its plugin seam is Python callables:
+ *   objective_fn(x), oracle.gradient(x), oracle.hessian_operator(x)(v),
+ *   cg_solve(apply_H, g, cfg), line_search(f, f0, slope, cfg).
+ * Each entry point below replaces the arithmetic of one of those callables;
+ * the Python package paper_1802_09113_b200 binds them with ctypes and keeps
+ * the reference's names, argument meaning and exceptions.
+ *
+ * Conventions
+ *   - All pointers are DEVICE pointers unless stated; the library never
+ *     allocates persistent memory (workspace is passed in, sized by
+ *     snx_workspace_bytes).  `stream` is a cudaStream_t (NULL = legacy).
+ *   - dtype: SNX_F64 (X stored fp64, fp64 math: 1e-10 parity path) or
+ *     SNX_F32 (X stored fp32, fp32 products, fp64 reductions: 1e-4 path).
+ *   - X is row-major with leading dimension ldx (elements).  p is the true
+ *     feature count; kernels stream P = round_up(p, 4) columns, so ldx >= P,
+ *     ldx % 4 == 0 and columns p..P-1 must be zero (snx_pack_rows does this).
+ *   - Weight-shaped vectors (x, v, gradients, Hv, CG vectors) are fp64 and
+ *     flat class-major, d = K*p, w[c*p + j] for weighted class c < K = C-1:
+ *     exactly the reference layout x.reshape((p, C-1), order="F")
+ *     (softmax.py:62-74).
+ *   - rows: optional int64 row indices (a sorted sample S, sampling.py:38-45);
+ *     NULL means rows 0..nrows-1.  labels are int32 in [0, C).
+ *   - Return 0 on success; non-zero => snx_last_error() has the message.
+ *   - Every reduction runs in a fixed order: results are bit-identical run
+ *     to run (the reference's reruns are, tests/test_newton.py:102-114).
+ */
+#ifndef SNX_H
+#define SNX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SNX_ABI_VERSION 1
+#define SNX_F64 0
+#define SNX_F32 1
+#define SNX_DOT_BLOCKS 256 /* fixed partial count of every dot product */
+#define SNX_CG_SLOT 8      /* doubles per CG state slot */
+
+int snx_abi_version(void);
+const char *snx_last_error(void);
+
+/* Bytes of workspace the calls below need for nrows rows of p features, K
+ * weighted classes (any of the row-pass calls).  The workspace must be
+ * zero-filled once when allocated; calls leave its counters at zero. */
+size_t snx_workspace_bytes(int dtype, int64_t nrows, int32_t p, int32_t K);
+
+/* softmax.py:125-141 (data_objective/objective) + softmax.py:239-247
+ * (predict/accuracy), evaluated at w_eff = w + alpha*dir (dir may be NULL;
+ * the line-search trial x + a*p of newton.py:92 without materialising it).
+ *   out[0] = sum_i (M_i + log alpha_i - lin_i)   (data loss)
+ *   out[1] = ||w_eff||^2                          (for lam/2 ||x||^2)
+ *   correct_out[0] (nullable) = #rows with argmax prob == label. */
+int snx_objective(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                  int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
+                  const double *w, const double *dir, double alpha, double *out,
+                  int64_t *correct_out, void *ws, size_t ws_bytes, void *stream);
+
+/* softmax.py:144-169 (data_gradient/gradient), sampling.py:84-87:
+ *   G_out = scale * vec(X_rows^T (E/alpha - onehot)) + lam * w
+ * plus out[0..1] as snx_objective (the loss comes for free). */
+int snx_objective_grad(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                       int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
+                       const double *w, double scale, double lam, double *out,
+                       double *G_out, void *ws, size_t ws_bytes, void *stream);
+
+/* softmax.py:181-195 (HessianOperator.__init__): H_out[r*K + c] =
+ * h(a_rows[r], x_c) = E_rc / alpha_r, stored in the X dtype. */
+int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                     int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
+                     const double *w, void *H_out, void *ws, size_t ws_bytes,
+                     void *stream);
+
+/* softmax.py:197-210 (HessianOperator.apply), scale = n/|S_H| (sampling.py:82):
+ *   Hv_out = scale * vec(X_S^T (V.W - W.rowsum(V.W))) + lam * v,  V = X_S Q(v)
+ * dots (nullable, SNX_DOT_BLOCKS*2 doubles): per-block partials of v.Hv and v.v
+ * (the CG curvature test, cg.py:78).  skip (nullable): if *skip != 0 the
+ * call is a no-op (device-side early exit of a captured CG loop). */
+int snx_hess_apply(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                   int64_t nrows, int32_t p, int32_t K, const void *H,
+                   const double *v, double scale, double lam, double *Hv_out,
+                   double *dots, const double *skip, void *ws, size_t ws_bytes,
+                   void *stream);
+
+/* Fixed-order dot product: out[0] = x . y (np.dot / np.linalg.norm**2).
+ * out must hold 1 + SNX_DOT_BLOCKS doubles (out[1..] = block partials). */
+int snx_dot(const double *x, const double *y, int64_t d, double *out, void *stream);
+
+/* SNX_DOT_BLOCKS fixed-order block partials of x . y into part (the layout
+ * snx_cg_update expects for its dots argument: [s.Hs partials | s.s partials]). */
+int snx_dot_partials(const double *x, const double *y, int64_t d, double *part, void *stream);
+
+/* x_out = x + alpha * p, rounded as numpy's `x + alpha * p` (no FMA):
+ * newton.py:97 and the trial points of newton.py:92. */
+int snx_axpy(const double *x, const double *p, double alpha, int64_t d, double *x_out,
+             void *stream);
+
+/* out = a*x + b*y with numpy rounding of `a * x + b * y` (two products, one
+ * add, no FMA); the vector updates of Steihaug-CG (trust region). */
+int snx_axpby(double a, const double *x, double b, const double *y, int64_t d, double *out,
+              void *stream);
+
+/* Device CG (cg.py:51-98).  state: (max_iters+2)*SNX_CG_SLOT + SNX_DOT_BLOCKS
+ * doubles (the tail is reduction scratch); slot t
+ * holds the scalars entering iteration t: [rs, best_norm, done, iters,
+ * converged, threshold, err, curvature].  Vectors r, s, p, p_best have d
+ * entries.  snx_cg_init sets r = s = -g, p = 0, p_best = -g and slot 0; a
+ * zero g finishes immediately (cg.py:61-62). */
+int snx_cg_init(const double *g, int64_t d, double theta, int32_t max_iters,
+                double *r, double *s, double *p, double *p_best, double *state,
+                void *stream);
+
+/* One CG iteration t after Hs = H s was written with its dot partials
+ * (snx_hess_apply(..., dots, skip = &state slot t done flag)). */
+int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
+                  const double *dots, double *r, double *s, double *p, double *p_best,
+                  double *state, void *stream);
+
+/* Address of the "done" field of slot t (pass as snx_hess_apply's skip). */
+const double *snx_cg_done_flag(const double *state, int32_t t);
+
+/* Copy+convert host-layout helpers (device to device). */
+int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
+                  int64_t ldd, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SNX_H */

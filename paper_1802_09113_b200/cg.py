@@ -1,0 +1,127 @@
+"""Conjugate gradient for H p = -g with best-iterate tracking (reference cg.py).
+
+The CG state (r, s, p, p_best and the scalars rs, ||r_best||, threshold,
+iteration count, flags) lives on the device.  One iteration is
+
+    snx_hess_apply(s -> Hs, + s.Hs / s.s partials)   [skipped once done]
+    snx_cg_update(t)  = curvature test, alpha, p/r update, best copy, stop
+                        test and new direction (cg.py:77-96)
+
+so the whole solve is enqueued without a host round trip; the host reads the
+final slot once.  Every decision (curvature <= 1e-32 s.s, r_norm <= best,
+r_norm <= theta ||g||) is the reference's, taken on device in fp64.
+
+Foreign operators (any callable v -> H v, e.g. the reference's own
+HessianOperator or a test's CountingOperator, tests/test_cg.py:10-20) are
+supported through the same device state: s is handed to the callable as
+numpy and H s uploaded back.
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import cuda_device, ptr, stream_handle, vec_in, vec_out
+from .errors import CurvatureError, DataError
+
+CURVATURE_EPS = 1e-32  # cg.py:16
+
+
+@dataclass(frozen=True)
+class CgConfig:
+    """theta: relative residual tolerance; max_iters: operator applications."""
+
+    theta: float = 1e-4
+    max_iters: int = 10
+
+    def __post_init__(self):
+        if not 0.0 < self.theta < 1.0:
+            raise DataError(f"theta must be in (0, 1), got {self.theta}")
+        if self.max_iters < 1:
+            raise DataError(f"max_iters must be >= 1, got {self.max_iters}")
+
+
+@dataclass
+class CgReport:
+    """solution = best iterate by residual norm (or -g when nothing improved)."""
+
+    solution: object
+    residual_norm: float
+    iterations: int
+    converged: bool
+
+
+class CgWorkspace:
+    """Device buffers of one CG solve of dimension d with at most T iterations."""
+
+    def __init__(self, d, T, device):
+        f64 = dict(dtype=torch.float64, device=device)
+        self.d, self.T = d, T
+        self.vecs = torch.empty((5, d), **f64)
+        self.r, self.s, self.p, self.pb, self.Hs = self.vecs
+        self.state = torch.zeros((T + 2) * _lib.CG_SLOT + _lib.DOT_BLOCKS, **f64)
+        self.dots = torch.empty(2 * _lib.DOT_BLOCKS, **f64)
+
+    def slot(self, t):
+        return self.state[t * _lib.CG_SLOT:(t + 1) * _lib.CG_SLOT]
+
+    def done_ptr(self, t):
+        return _lib.done_flag(ptr(self.state), t)
+
+
+def enqueue_cg(op, g, theta, T, ws):
+    """Enqueue init + T iterations with a device operator (op.apply_into)."""
+    d = ws.d
+    _lib.call("snx_cg_init", ptr(g), d, float(theta), T, ptr(ws.r), ptr(ws.s), ptr(ws.p),
+              ptr(ws.pb), ptr(ws.state), stream_handle())
+    for t in range(T):
+        op.apply_into(ws.s, ws.Hs, dots=ws.dots, skip=ws.done_ptr(t))
+        _lib.call("snx_cg_update", t, T, d, ptr(ws.Hs), ptr(ws.dots), ptr(ws.r), ptr(ws.s),
+                  ptr(ws.p), ptr(ws.pb), ptr(ws.state), stream_handle())
+
+
+def _foreign_loop(apply_H, T, ws):
+    d = ws.d
+    last = 0
+    for t in range(T):
+        if float(ws.slot(t)[2]) != 0.0:  # done: the operator is host code anyway
+            return t
+        hs = apply_H(ws.s.cpu().numpy())
+        hs = np.asarray(hs, dtype=np.float64)
+        ws.Hs.copy_(torch.from_numpy(np.ascontiguousarray(hs)))
+        _lib.call("snx_dot_partials", ptr(ws.s), ptr(ws.Hs), d, ptr(ws.dots), stream_handle())
+        _lib.call("snx_dot_partials", ptr(ws.s), ptr(ws.s), d,
+                  ptr(ws.dots) + 8 * _lib.DOT_BLOCKS, stream_handle())
+        _lib.call("snx_cg_update", t, T, d, ptr(ws.Hs), ptr(ws.dots), ptr(ws.r), ptr(ws.s),
+                  ptr(ws.p), ptr(ws.pb), ptr(ws.state), stream_handle())
+        last = t + 1
+    return last
+
+
+def report_from(ws, t_final, as_torch):
+    rs, best, done, iters, conv, thr, err, curv = ws.slot(t_final).tolist()
+    if err != 0.0:
+        raise CurvatureError(
+            f"non-positive curvature s^T H s = {curv:.3e} at CG iteration {int(iters)}; "
+            "operator is not positive definite")
+    sol = ws.pb.clone()
+    if int(iters) == 0 and conv != 0.0:
+        sol.zero_()  # cg.py:61-62 returns zeros for g == 0
+    return CgReport(vec_out(sol, as_torch), best, int(iters), bool(conv))
+
+
+def cg_solve(apply_H, g, cfg):
+    """Approximately solve H p = -g to ||H p + g|| <= theta ||g|| (cg.py:51-98)."""
+    gd, as_t = vec_in(g, np.asarray(g).shape[0] if not isinstance(g, torch.Tensor)
+                      else g.numel(), "gradient")
+    ws = CgWorkspace(gd.numel(), cfg.max_iters, cuda_device())
+    if getattr(apply_H, "_snx_device", False):
+        enqueue_cg(apply_H, gd, cfg.theta, cfg.max_iters, ws)
+        t_final = cfg.max_iters
+    else:
+        _lib.call("snx_cg_init", ptr(gd), ws.d, float(cfg.theta), cfg.max_iters, ptr(ws.r),
+                  ptr(ws.s), ptr(ws.p), ptr(ws.pb), ptr(ws.state), stream_handle())
+        t_final = _foreign_loop(apply_H, cfg.max_iters, ws)
+    return report_from(ws, t_final, as_t)

@@ -1,0 +1,352 @@
+// d-vector kernels: weight preparation, dot products, numpy-rounded axpy and
+// the device-resident CG iteration of cg.py:51-98.  All of them run on a fixed
+// grid of SNX_DOT_BLOCKS blocks so every reduction has one summation order.
+#include <stdarg.h>
+#include <stdio.h>
+
+#include "snx_common.cuh"
+#include "snx_internal.h"
+
+namespace snx {
+
+static thread_local char g_err[512] = "";
+
+void set_error(const char *fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int check_launch(const char *what) {
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error("snx: %s failed: %s", what, cudaGetErrorString(e));
+    return 1;
+  }
+  return 0;
+}
+
+// Wt[c*P + j] = T(w + alpha*dir)[c*p + j] (zero in the pad columns j >= p);
+// block partials of ||w + alpha*dir||^2; the last block writes the total to
+// wsq_out (if given).
+template <typename T>
+__global__ void __launch_bounds__(kDotThreads)
+    prep_weights_kernel(const double *__restrict__ w, const double *__restrict__ dir,
+                        double alpha, int K, int p, int P, T *__restrict__ Wt, double *part,
+                        unsigned *counter, double *wsq_out) {
+  __shared__ double sh[kDotThreads / 32];
+  __shared__ bool last;
+  double acc = 0.0;
+  const int64_t total = (int64_t)K * P;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < total;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    const int64_t c = i / P;
+    const int j = (int)(i - c * P);
+    double v = 0.0;
+    if (j < p) {
+      const int64_t f = c * p + j;
+      v = dir ? np_axpy(w[f], alpha, dir[f]) : w[f];
+      acc += v * v;
+    }
+    if (Wt) Wt[i] = (T)v;
+  }
+  if (wsq_out == nullptr) return;
+  const double b = block_sum<kDotThreads>(acc, sh);
+  if (threadIdx.x == 0) {
+    part[blockIdx.x] = b;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last) {
+    __threadfence();
+    if (threadIdx.x < 32) {
+      double t = 0.0;
+      const volatile double *vp = part;
+#pragma unroll
+      for (int i = 0; i < kDotBlocks / 32; ++i) t += vp[threadIdx.x + 32 * i];
+      t = warp_allsum(t);
+      if (threadIdx.x == 0) {
+        *wsq_out = t;
+        *counter = 0u;
+      }
+    }
+  }
+}
+
+int launch_prep_weights(int dtype, const double *w, const double *dir, double alpha, int K,
+                        int p, int P, void *Wt, double *part, unsigned *counter,
+                        double *wsq_out, cudaStream_t st) {
+  if (dtype == SNX_F64)
+    prep_weights_kernel<double><<<kDotBlocks, kDotThreads, 0, st>>>(
+        w, dir, alpha, K, p, P, static_cast<double *>(Wt), part, counter, wsq_out);
+  else
+    prep_weights_kernel<float><<<kDotBlocks, kDotThreads, 0, st>>>(
+        w, dir, alpha, K, p, P, static_cast<float *>(Wt), part, counter, wsq_out);
+  return check_launch("prep_weights");
+}
+
+__global__ void __launch_bounds__(kDotThreads)
+    dot_part_kernel(const double *__restrict__ x, const double *__restrict__ y, int64_t d,
+                    double *part) {
+  __shared__ double sh[kDotThreads / 32];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads)
+    acc += x[i] * y[i];
+  const double b = block_sum<kDotThreads>(acc, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = b;
+}
+
+__global__ void dot_final_kernel(const double *part, double *out) {
+  const double t = warp_sum_partials(part);
+  if (threadIdx.x == 0) *out = t;
+}
+
+__global__ void __launch_bounds__(kDotThreads)
+    axpy_kernel(const double *__restrict__ x, const double *__restrict__ p, double alpha,
+                int64_t d, double *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads)
+    out[i] = np_axpy(x[i], alpha, p[i]);
+}
+
+__global__ void __launch_bounds__(kDotThreads)
+    axpby_kernel(double a, const double *__restrict__ x, double b, const double *__restrict__ y,
+                 int64_t d, double *__restrict__ out) {
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads)
+    out[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
+}
+
+// ------------------------------------------------------------------ CG (cg.py)
+// slot layout (SNX_CG_SLOT doubles)
+enum { kRs = 0, kBest = 1, kDone = 2, kIters = 3, kConv = 4, kThr = 5, kErr = 6, kCurv = 7 };
+
+__device__ __forceinline__ double *slot(double *state, int t) { return state + t * SNX_CG_SLOT; }
+
+// scratch after the slots: [0, B) g.g / r.r partials
+__device__ __forceinline__ double *scratch(double *state, int max_iters) {
+  return state + (max_iters + 2) * SNX_CG_SLOT;
+}
+
+__global__ void __launch_bounds__(kDotThreads)
+    cg_init_kernel(const double *__restrict__ g, int64_t d, int max_iters, double *r,
+                   double *s, double *p, double *pb, double *state) {
+  __shared__ double sh[kDotThreads / 32];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    const double gi = g[i];
+    r[i] = -gi;  // cg.py:65-69: r = -g, s = r, p = 0, p_best = s
+    s[i] = -gi;
+    p[i] = 0.0;
+    pb[i] = -gi;
+    acc += gi * gi;
+  }
+  const double b = block_sum<kDotThreads>(acc, sh);
+  if (threadIdx.x == 0) scratch(state, max_iters)[blockIdx.x] = b;
+  // zero every slot's flags (block 0)
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < (max_iters + 2) * SNX_CG_SLOT; i += kDotThreads)
+      state[i] = 0.0;
+}
+
+__global__ void cg_init_final_kernel(double theta, int max_iters, double *state) {
+  const double gg = warp_sum_partials(scratch(state, max_iters));
+  if (threadIdx.x == 0) {
+    double *s0 = slot(state, 0);
+    const double gn = sqrt(gg);  // np.linalg.norm = sqrt(dot)
+    s0[kRs] = gg;                // (-g).(-g) == g.g bitwise
+    s0[kBest] = gn;
+    s0[kThr] = theta * gn;
+    s0[kIters] = 0.0;
+    s0[kConv] = gn == 0.0 ? 1.0 : 0.0;
+    s0[kDone] = gn == 0.0 ? 1.0 : 0.0;  // cg.py:61-62
+  }
+}
+
+// Iteration t, part 1 (cg.py:77-86): curvature test, alpha, p += a s, r -= a Hs.
+__global__ void __launch_bounds__(kDotThreads)
+    cg_step1_kernel(int t, int max_iters, int64_t d, const double *__restrict__ Hs,
+                    const double *__restrict__ dots, double *r, const double *s, double *p,
+                    double *state) {
+  const double *st = slot(state, t);
+  if (st[kDone] != 0.0) return;
+  __shared__ double sh[kDotThreads / 32];
+  __shared__ double s_alpha;
+  __shared__ bool s_bad;
+  if (threadIdx.x < 32) {
+    const double curv = warp_sum_partials(dots);            // s.Hs
+    const double ss = warp_sum_partials(dots + kDotBlocks);  // s.s
+    if (threadIdx.x == 0) {
+      s_bad = curv <= 1e-32 * ss;  // cg.py:16, :79
+      s_alpha = st[kRs] / curv;
+      if (s_bad && blockIdx.x == 0) {
+        slot(state, t + 1)[kErr] = 1.0;
+        slot(state, t + 1)[kCurv] = curv;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_bad) return;
+  const double alpha = s_alpha;
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    p[i] = np_axpy(p[i], alpha, s[i]);
+    const double ri = np_axmy(r[i], alpha, Hs[i]);
+    r[i] = ri;
+    acc += ri * ri;
+  }
+  const double b = block_sum<kDotThreads>(acc, sh);
+  if (threadIdx.x == 0) scratch(state, max_iters)[blockIdx.x] = b;
+}
+
+// Iteration t, part 2 (cg.py:87-96): best-iterate copy, stop test, new direction.
+__global__ void __launch_bounds__(kDotThreads)
+    cg_step2_kernel(int t, int max_iters, int64_t d, const double *__restrict__ r, double *s,
+                    const double *__restrict__ p, double *pb, double *state) {
+  const double *st = slot(state, t);
+  double *nx = slot(state, t + 1);
+  if (st[kDone] != 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x < SNX_CG_SLOT) nx[threadIdx.x] = st[threadIdx.x];
+    return;
+  }
+  if (nx[kErr] != 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      nx[kRs] = st[kRs];
+      nx[kBest] = st[kBest];
+      nx[kThr] = st[kThr];
+      nx[kConv] = 0.0;
+      nx[kIters] = t + 1;
+      nx[kDone] = 1.0;
+    }
+    return;
+  }
+  __shared__ double s_rr;
+  if (threadIdx.x < 32) {
+    const double rr = warp_sum_partials(scratch(state, max_iters));
+    if (threadIdx.x == 0) s_rr = rr;
+  }
+  __syncthreads();
+  const double rr = s_rr;
+  const double rn = sqrt(rr);
+  const bool best = rn <= st[kBest];
+  const bool conv = rn <= st[kThr];
+  const double beta = rr / st[kRs];
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    if (best) pb[i] = p[i];
+    if (!conv) s[i] = np_axpy(r[i], beta, s[i]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    nx[kRs] = conv ? st[kRs] : rr;
+    nx[kBest] = best ? rn : st[kBest];
+    nx[kThr] = st[kThr];
+    nx[kConv] = conv ? 1.0 : 0.0;
+    nx[kIters] = t + 1;
+    nx[kDone] = (conv || t + 1 >= max_iters) ? 1.0 : 0.0;
+  }
+}
+
+template <typename T>
+__global__ void pack_rows_kernel(const double *__restrict__ src, int64_t nrows, int p,
+                                 T *__restrict__ dst, int64_t ldd) {
+  const int64_t total = nrows * ldd;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / ldd;
+    const int64_t j = i - r * ldd;
+    dst[i] = j < p ? (T)src[r * p + j] : T(0);
+  }
+}
+
+}  // namespace snx
+
+using namespace snx;
+
+extern "C" {
+
+int snx_abi_version(void) { return SNX_ABI_VERSION; }
+
+const char *snx_last_error(void) { return g_err; }
+
+int snx_dot(const double *x, const double *y, int64_t d, double *out, void *stream) {
+  // out holds 1 + SNX_DOT_BLOCKS doubles: the partials go to out[1..]
+  cudaStream_t st = (cudaStream_t)stream;
+  dot_part_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(x, y, d, out + 1);
+  if (check_launch("dot")) return 1;
+  dot_final_kernel<<<1, 32, 0, st>>>(out + 1, out);
+  return check_launch("dot_final");
+}
+
+int snx_dot_partials(const double *x, const double *y, int64_t d, double *part, void *stream) {
+  dot_part_kernel<<<kDotBlocks, kDotThreads, 0, (cudaStream_t)stream>>>(x, y, d, part);
+  return check_launch("dot_partials");
+}
+
+int snx_axpy(const double *x, const double *p, double alpha, int64_t d, double *x_out,
+             void *stream) {
+  axpy_kernel<<<kDotBlocks, kDotThreads, 0, (cudaStream_t)stream>>>(x, p, alpha, d, x_out);
+  return check_launch("axpy");
+}
+
+int snx_axpby(double a, const double *x, double b, const double *y, int64_t d, double *out,
+              void *stream) {
+  axpby_kernel<<<kDotBlocks, kDotThreads, 0, (cudaStream_t)stream>>>(a, x, b, y, d, out);
+  return check_launch("axpby");
+}
+
+int snx_cg_init(const double *g, int64_t d, double theta, int32_t max_iters, double *r,
+                double *s, double *p, double *p_best, double *state, void *stream) {
+  if (max_iters < 1) {
+    set_error("snx_cg_init: max_iters must be >= 1");
+    return 1;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cg_init_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(g, d, max_iters, r, s, p, p_best, state);
+  if (check_launch("cg_init")) return 1;
+  cg_init_final_kernel<<<1, 32, 0, st>>>(theta, max_iters, state);
+  return check_launch("cg_init_final");
+}
+
+int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
+                  const double *dots, double *r, double *s, double *p, double *p_best,
+                  double *state, void *stream) {
+  if (t < 0 || t >= max_iters) {
+    set_error("snx_cg_update: iteration %d outside [0, %d)", t, max_iters);
+    return 1;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cg_step1_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(t, max_iters, d, Hs, dots, r, s, p,
+                                                      state);
+  if (check_launch("cg_step1")) return 1;
+  cg_step2_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(t, max_iters, d, r, s, p, p_best, state);
+  return check_launch("cg_step2");
+}
+
+const double *snx_cg_done_flag(const double *state, int32_t t) {
+  return state + (size_t)t * SNX_CG_SLOT + kDone;
+}
+
+int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
+                  int64_t ldd, void *stream) {
+  if (ldd < p) {
+    set_error("snx_pack_rows: ldd < p");
+    return 1;
+  }
+  if (nrows == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int blocks = 148 * 8;
+  if (dtype == SNX_F64)
+    pack_rows_kernel<double><<<blocks, 256, 0, st>>>(src, nrows, p, static_cast<double *>(dst),
+                                                     ldd);
+  else
+    pack_rows_kernel<float><<<blocks, 256, 0, st>>>(src, nrows, p, static_cast<float *>(dst),
+                                                    ldd);
+  return check_launch("pack_rows");
+}
+
+}  // extern "C"

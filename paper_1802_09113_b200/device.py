@@ -1,0 +1,223 @@
+"""HBM-resident datasets, row views and d-vector plumbing.
+
+A `DeviceDataset` is the B200 counterpart of the reference's LabeledDataset
+(dataset.py:150-190): the feature matrix lives in HBM, row-major with a
+16-byte aligned leading dimension, in the compute dtype ("f64": the 1e-10
+parity path, "f32": the 1e-4 path); labels are int32.  `take(indices)` is the
+row gather of dataset.py:90-97 -- it does not copy rows, it returns a view
+holding the (sorted) indices, which the kernels gather through (the fused
+gather-GEMM of the north star).  The identity selection returns the dataset
+itself, as the reference does, so full-sample runs use the unsampled path.
+
+torch owns the device memory; all arithmetic is done by libsnx kernels.
+"""
+
+import weakref
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DataError, DimensionError
+
+DTYPES = {"f64": (_lib.F64, torch.float64), "f32": (_lib.F32, torch.float32)}
+
+
+def cuda_device():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1802_09113_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def ptr(t):
+    return None if t is None else t.data_ptr()
+
+
+def round_up(x, a):
+    return (x + a - 1) // a * a
+
+
+class DeviceDataset:
+    """Features (n x p, padded to ld) + int32 labels in HBM."""
+
+    def __init__(self, X, labels, n_classes, n_features, dtype="f64"):
+        if dtype not in DTYPES:
+            raise ValueError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
+        if n_classes < 2:
+            raise DataError(f"need at least 2 classes, got {n_classes}")
+        if n_classes - 1 > 16:
+            raise DataError(f"C = {n_classes} classes: this build supports C <= 17")
+        self.X = X
+        self.labels = labels
+        self.n_classes = int(n_classes)
+        self.n_features = int(n_features)
+        self.dtype = dtype
+        self.code = DTYPES[dtype][0]
+        self.ld = int(X.shape[1])
+        self._ws = None
+        self.rows = None  # a dataset is its own identity view
+
+    # ------------------------------------------------------------ construction
+    @classmethod
+    def from_numpy(cls, features, labels, n_classes, dtype="f64"):
+        dev = cuda_device()
+        A = np.ascontiguousarray(features, dtype=np.float64)
+        if A.ndim != 2:
+            raise DimensionError(f"feature matrix must be 2-D, got shape {A.shape}")
+        y = np.asarray(labels, dtype=np.int64)
+        n, p = A.shape
+        if len(y) != n:
+            raise DimensionError(f"{len(y)} labels for {n} rows")
+        if n_classes < 2:
+            raise DataError(f"need at least 2 classes, got {n_classes}")
+        if len(y) and (y.min() < 0 or y.max() >= n_classes):
+            raise DataError(f"labels must lie in [0, {n_classes})")
+        code, tdtype = DTYPES.get(dtype, (None, None))
+        if code is None:
+            raise ValueError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
+        ld = max(4, round_up(p, 4))
+        X = torch.empty((n, ld), dtype=tdtype, device=dev)
+        if n:
+            if code == _lib.F64 and ld == p:
+                X.copy_(torch.from_numpy(A))
+            else:
+                stage = torch.from_numpy(A).to(dev)
+                _lib.call("snx_pack_rows", code, ptr(stage), n, p, ptr(X), ld, stream_handle())
+                del stage
+        lab = torch.from_numpy(y.astype(np.int32)).to(dev)
+        return cls(X, lab, n_classes, p, dtype)
+
+    @classmethod
+    def from_dataset(cls, ds, dtype="f64"):
+        """From the reference's LabeledDataset (duck-typed: features.toarray(), labels,
+        n_classes) or anything with the same fields."""
+        feats = ds.features
+        A = feats.toarray() if hasattr(feats, "toarray") else np.asarray(feats)
+        return cls.from_numpy(A, ds.labels, ds.n_classes, dtype=dtype)
+
+    # ------------------------------------------------------------ shape
+    @property
+    def n_rows(self):
+        return int(self.X.shape[0])
+
+    @property
+    def K(self):
+        return self.n_classes - 1
+
+    @property
+    def dim(self):
+        return self.K * self.n_features
+
+    @property
+    def base(self):
+        return self
+
+    # ------------------------------------------------------------ views
+    def take(self, indices):
+        """Row gather (dataset.py:90-97, 180-185); identity returns self."""
+        idx = np.asarray(indices, dtype=np.int64)
+        n = self.n_rows
+        if len(idx) == n and np.array_equal(idx, np.arange(n)):
+            return self
+        if len(idx) and (idx.min() < 0 or idx.max() >= n):
+            raise DimensionError("row index out of range")
+        return DeviceView(self, torch.from_numpy(idx).to(self.X.device), len(idx))
+
+    def slice_rows(self, i0, i1):
+        return self.take(np.arange(i0, i1))
+
+    # ------------------------------------------------------------ workspace
+    def workspace(self, nrows):
+        need = _lib.workspace_bytes(self.code, nrows, self.n_features, self.K)
+        if self._ws is None or self._ws.numel() < need:
+            floor = _lib.workspace_bytes(self.code, self.n_rows, self.n_features, self.K)
+            self._ws = torch.zeros(max(need, floor), dtype=torch.uint8, device=self.X.device)
+        return self._ws
+
+
+class DeviceView:
+    """Rows `rows` (sorted int64 device indices) of a DeviceDataset."""
+
+    def __init__(self, base, rows, n_rows):
+        self.base = base
+        self.rows = rows
+        self._n = int(n_rows)
+
+    n_features = property(lambda self: self.base.n_features)
+    n_classes = property(lambda self: self.base.n_classes)
+    K = property(lambda self: self.base.K)
+    dim = property(lambda self: self.base.dim)
+    dtype = property(lambda self: self.base.dtype)
+    code = property(lambda self: self.base.code)
+    X = property(lambda self: self.base.X)
+    ld = property(lambda self: self.base.ld)
+    labels = property(lambda self: self.base.labels)
+
+    @property
+    def n_rows(self):
+        return self._n
+
+    def workspace(self, nrows):
+        return self.base.workspace(nrows)
+
+
+# Reference-dataset objects are uploaded once and cached (keyed by identity).
+_CACHE = {}
+
+
+def as_device(ds, dtype="f64"):
+    if isinstance(ds, (DeviceDataset, DeviceView)):
+        return ds
+    key = (id(ds), dtype)
+    hit = _CACHE.get(key)
+    if hit is not None and hit[0]() is ds:
+        return hit[1]
+    dev = DeviceDataset.from_dataset(ds, dtype=dtype)
+    try:
+        ref = weakref.ref(ds, lambda _r, k=key: _CACHE.pop(k, None))
+    except TypeError:  # not weak-referenceable: keep a strong reference
+        ref = (lambda obj: (lambda: obj))(ds)
+    _CACHE[key] = (ref, dev)
+    return dev
+
+
+def vec_in(x, d, what="weight vector"):
+    """User vector -> (contiguous fp64 CUDA tensor of length d, caller_used_torch)."""
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 1 or x.numel() != d:
+            raise DimensionError(f"expected {what} of length {d}, got {tuple(x.shape)}")
+        return x.to(device=cuda_device(), dtype=torch.float64).contiguous(), True
+    a = np.asarray(x, dtype=np.float64)
+    if a.shape != (d,):
+        raise DimensionError(f"expected {what} of length {d}, got {a.shape}")
+    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda_device()), False
+
+
+def vec_out(t, as_torch):
+    return t if as_torch else t.cpu().numpy()
+
+
+def dot(x, y):
+    """Fixed-order device dot product (np.dot); returns a 0-d device tensor view."""
+    out = torch.empty(1 + _lib.DOT_BLOCKS, dtype=torch.float64, device=x.device)
+    _lib.call("snx_dot", ptr(x), ptr(y), x.numel(), ptr(out), stream_handle())
+    return out[0]
+
+
+def axpy(x, alpha, p, out=None):
+    """x + alpha * p with numpy rounding (newton.py:97)."""
+    out = torch.empty_like(x) if out is None else out
+    _lib.call("snx_axpy", ptr(x), ptr(p), float(alpha), x.numel(), ptr(out), stream_handle())
+    return out
+
+
+def axpby(a, x, b, y, out=None):
+    out = torch.empty_like(x) if out is None else out
+    _lib.call("snx_axpby", float(a), ptr(x), float(b), ptr(y), x.numel(), ptr(out),
+              stream_handle())
+    return out

@@ -1,0 +1,183 @@
+"""Inexact sub-sampled Newton-CG with Armijo line search (reference newton.py).
+
+`minimize` is the generic loop and plugin seam (newton.py:60-112): any
+objective_fn / oracle_factory pair works; vectors are kept on the device and
+handed to foreign callables as numpy.  `newton_solve` (newton.py:115-140) is
+the device-resident specialisation used for speed: x, g, p and the CG state
+never leave HBM; the host only reads the scalars the reference branches on
+(||g|| < eps, the Armijo test) and the trace values.
+
+One deliberate fusion, output-identical to the reference: each line-search
+trial F(x + a p) is a single pass that also counts correct predictions.  The
+reference recomputes F at the accepted point (newton.py:98) -- that value is
+bit-identical to the accepted trial (the trial point and the new iterate are
+both formed by the same numpy-rounded x + a*p, snx_objective's `dir` path and
+snx_axpy), so the trial's value and accuracy are reused instead of a third
+full-data pass.
+"""
+
+import math
+import time
+from dataclasses import dataclass, field, replace
+
+import numpy as np
+import torch
+
+from . import softmax
+from .cg import CgConfig, CgWorkspace, cg_solve, enqueue_cg, report_from
+from .device import as_device, axpy, cuda_device, dot, vec_in, vec_out
+from .errors import DataError, LineSearchError
+from .linesearch import LineSearchConfig, line_search
+from .sampling import SampleConfig, SubsampledOracle
+from .trace import RunRecord, SolveTrace
+
+VARIANT_FRACTIONS = {
+    "full": (1.0, 1.0),
+    "subsampled-100": (1.0, 0.05),
+    "subsampled-20": (0.2, 0.05),
+}
+
+
+@dataclass(frozen=True)
+class NewtonConfig:
+    epsilon: float = 1e-8
+    max_outer_iters: int = 100
+    cg: CgConfig = field(default_factory=CgConfig)
+    ls: LineSearchConfig = field(default_factory=LineSearchConfig)
+    samples: SampleConfig = field(default_factory=SampleConfig)
+
+    def __post_init__(self):
+        if self.epsilon <= 0:
+            raise DataError(f"epsilon must be > 0, got {self.epsilon}")
+
+
+def make_variant(name, base=NewtonConfig()):
+    """NewtonConfig with the named variant's sample fractions (newton.py:46-57)."""
+    if name not in VARIANT_FRACTIONS:
+        raise ValueError(
+            f"unknown variant {name!r}; expected one of {sorted(VARIANT_FRACTIONS)}")
+    f_g, f_h = VARIANT_FRACTIONS[name]
+    return replace(base, samples=replace(base.samples, gradient_fraction=f_g,
+                                         hessian_fraction=f_h))
+
+
+def _host(v):
+    return v.cpu().numpy()
+
+
+def minimize(objective_fn, oracle_factory, x0, cfg, metrics=None, solver_name="newton"):
+    """Generic inexact Newton-CG loop (newton.py:60-112).
+
+    oracle_factory(k) -> object with .gradient(x) and .hessian_operator(x);
+    objective_fn(x) -> full objective; metrics(x) -> (train_acc, test_acc).
+    Callables flagged `_snx_device` receive device tensors, others numpy.
+    """
+    n0 = x0.numel() if isinstance(x0, torch.Tensor) else len(np.asarray(x0))
+    x, as_t = vec_in(x0, n0, "initial point")
+    x = x.clone()
+    on_dev = lambda fn: getattr(fn, "_snx_device", False)  # noqa: E731
+    f_dev = on_dev(objective_fn)
+
+    def F(v):
+        return float(objective_fn(v if f_dev else _host(v)))
+
+    def M(v):
+        if metrics is None:
+            return math.nan, math.nan
+        return metrics(v if on_dev(metrics) else _host(v))
+
+    t0 = time.perf_counter()
+    f_cur = F(x)
+    tr, te = M(x)
+    records = [RunRecord(solver_name, 0, 0.0, f_cur, tr, te, 0.0, 0)]
+    reason = "max-iters"
+    for k in range(cfg.max_outer_iters):
+        oracle = oracle_factory(k)
+        xin = x if on_dev(oracle) else _host(x)
+        g, _ = vec_in(oracle.gradient(xin), n0, "gradient")
+        if math.sqrt(float(dot(g, g))) < cfg.epsilon:
+            reason = "gradient-converged"
+            break
+        report = cg_solve(oracle.hessian_operator(xin), g, cfg.cg)
+        p = report.solution
+        slope = float(dot(p, g))
+        try:
+            alpha, _ = line_search(lambda a: F(axpy(x, a, p)), f_cur, slope, cfg.ls)
+        except LineSearchError:
+            reason = "line-search-failure"
+            break
+        x = axpy(x, alpha, p)
+        f_cur = F(x)
+        tr, te = M(x)
+        records.append(RunRecord(solver_name, k + 1, time.perf_counter() - t0, f_cur, tr, te,
+                                 alpha, report.iterations))
+    return SolveTrace(records, vec_out(x, as_t), reason)
+
+
+class _Trial:
+    """F(x + a p) and the correct count at that point, one fused device pass."""
+
+    def __init__(self, view, lam, x, p):
+        self.view, self.lam, self.x, self.p = view, lam, x, p
+        self.seen = {}
+
+    def __call__(self, a):
+        out, corr = softmax.objective_parts(self.view, self.x, self.p, a, want_correct=True)
+        loss, wsq = out.tolist()
+        f = loss + 0.5 * self.lam * wsq
+        self.seen[a] = (f, int(corr))
+        return f
+
+
+def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
+    """Sub-sampled Newton-CG on a SoftmaxProblem, device resident (newton.py:115-140).
+
+    x0 defaults to zeros.  Rows log the full objective, train accuracy and,
+    with a test set, test accuracy.  x0 may be numpy (x_final is numpy) or a
+    CUDA tensor (x_final stays on the device).
+    """
+    ds = as_device(prob.dataset)
+    if ds.n_rows == 0:
+        raise DataError("cannot solve on an empty dataset")
+    n, d = ds.n_rows, ds.dim
+    if x0 is None:
+        x0 = np.zeros(d)
+    x, as_t = vec_in(x0, d, "initial point")
+    x = x.clone()
+    test = as_device(test_set) if test_set is not None else None
+    dev_prob = softmax.SoftmaxProblem(ds, prob.lam)
+    lam = prob.lam
+    cgws = CgWorkspace(d, cfg.cg.max_iters, cuda_device())
+
+    def test_acc(w):
+        return (float(softmax.correct_count(test, w)) / test.n_rows) if test is not None \
+            else math.nan
+
+    t0 = time.perf_counter()
+    out, corr = softmax.objective_parts(ds, x, want_correct=True)
+    loss, wsq = out.tolist()
+    f_cur = loss + 0.5 * lam * wsq
+    records = [RunRecord(solver_name, 0, 0.0, f_cur, int(corr) / n, test_acc(x), 0.0, 0)]
+    reason = "max-iters"
+    for k in range(cfg.max_outer_iters):
+        oracle = SubsampledOracle(dev_prob, cfg.samples, k)
+        g, _ = oracle.gradient_device(x)
+        if math.sqrt(float(dot(g, g))) < cfg.epsilon:
+            reason = "gradient-converged"
+            break
+        hess = oracle.hessian_operator(x)
+        enqueue_cg(hess, g, cfg.cg.theta, cfg.cg.max_iters, cgws)
+        report = report_from(cgws, cfg.cg.max_iters, True)
+        p = report.solution
+        slope = float(dot(p, g))
+        trial = _Trial(ds, lam, x, p)
+        try:
+            alpha, _ = line_search(trial, f_cur, slope, cfg.ls)
+        except LineSearchError:
+            reason = "line-search-failure"
+            break
+        x = axpy(x, alpha, p)
+        f_cur, ncorr = trial.seen[alpha]
+        records.append(RunRecord(solver_name, k + 1, time.perf_counter() - t0, f_cur,
+                                 ncorr / n, test_acc(x), alpha, report.iterations))
+    return SolveTrace(records, vec_out(x, as_t), reason)

@@ -1,0 +1,197 @@
+"""L2-regularised softmax cross-entropy on the GPU: objective, gradient and the
+matrix-free sub-sampled Hessian operator.
+
+Same names, argument meaning, layouts and exceptions as the reference's
+softmax.py (file:line cited per function); the arithmetic runs in libsnx:
+
+  objective / data_objective   -> snx_objective        (softmax.py:125-141)
+  gradient  / data_gradient    -> snx_objective_grad   (softmax.py:144-169)
+  HessianOperator.__init__     -> snx_hess_prepare     (softmax.py:181-195)
+  HessianOperator.apply        -> snx_hess_apply       (softmax.py:197-212)
+  accuracy                     -> snx_objective(correct_out)  (softmax.py:243-247)
+
+Vectors may be numpy arrays (results come back as numpy, the reference's
+contract) or CUDA torch tensors (results stay on the device).
+"""
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .device import DeviceDataset, DeviceView, as_device, ptr, stream_handle, vec_in, vec_out
+from .errors import DataError, DimensionError
+
+BLOCK_ROWS = 8192  # accepted for API parity (softmax.py:25); kernels tile rows themselves
+
+
+@dataclass(frozen=True)
+class SoftmaxProblem:
+    """A labeled dataset together with the regularisation coefficient (softmax.py:28-41)."""
+
+    dataset: object
+    lam: float
+
+    def __post_init__(self):
+        if self.lam < 0:
+            raise DataError(f"regularization coefficient must be >= 0, got {self.lam}")
+
+    @property
+    def dim(self):
+        return (self.dataset.n_classes - 1) * self.dataset.n_features
+
+
+def zero_weights(p, n_classes):
+    return np.zeros((n_classes - 1) * p, dtype=np.float64)
+
+
+def weights_as_matrix(x, p, n_classes):
+    """softmax.py:62-70: flat class-major x viewed as the p-by-(C-1) matrix."""
+    x = np.asarray(x, dtype=np.float64)
+    if x.shape != ((n_classes - 1) * p,):
+        raise DimensionError(
+            f"weight vector must have length {(n_classes - 1) * p}, got {x.shape}")
+    return x.reshape((p, n_classes - 1), order="F")
+
+
+def matrix_as_weights(X):
+    return np.asarray(X, dtype=np.float64).ravel(order="F")
+
+
+def _view(ds):
+    return as_device(ds)
+
+
+def _args(view):
+    """Common leading ABI arguments for a dataset or a row view."""
+    return (view.code, ptr(view.X), view.ld, ptr(view.rows), view.n_rows, view.n_features,
+            view.K)
+
+
+def _ws(view):
+    ws = view.workspace(view.n_rows)
+    return ptr(ws), ws.numel()
+
+
+def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
+    """Device [data loss, ||w_eff||^2] (+ correct count) at w_eff = w + alpha*direction."""
+    out = torch.empty(2, dtype=torch.float64, device=w.device)
+    corr = torch.empty(1, dtype=torch.int64, device=w.device) if want_correct else None
+    _lib.call("snx_objective", *_args(view), ptr(view.labels), ptr(w), ptr(direction),
+              float(alpha), ptr(out), ptr(corr), *_ws(view), stream_handle())
+    return out, corr
+
+
+def gradient_parts(view, w, scale, lam):
+    """Device (G = scale * data_gradient + lam * w, [data loss, ||w||^2])."""
+    out = torch.empty(2, dtype=torch.float64, device=w.device)
+    G = torch.empty_like(w)
+    _lib.call("snx_objective_grad", *_args(view), ptr(view.labels), ptr(w), float(scale),
+              float(lam), ptr(out), ptr(G), *_ws(view), stream_handle())
+    return G, out
+
+
+def data_objective(ds, x):
+    """softmax.py:125-135: sum_i (maxPart_i + logPart_i - linearPart_i)."""
+    view = _view(ds)
+    w, _ = vec_in(x, view.dim)
+    out, _ = objective_parts(view, w)
+    return float(out[0])
+
+
+def objective(prob, x):
+    """softmax.py:138-141: data loss + (lam/2) ||x||^2."""
+    view = _view(prob.dataset)
+    w, _ = vec_in(x, view.dim, "weight vector")
+    loss, wsq = objective_parts(view, w)[0].tolist()
+    return loss + 0.5 * prob.lam * wsq
+
+
+def data_gradient(ds, x):
+    """softmax.py:144-163: vec(A^T (E/alpha - onehot))."""
+    view = _view(ds)
+    w, as_t = vec_in(x, view.dim)
+    G, _ = gradient_parts(view, w, 1.0, 0.0)
+    return vec_out(G, as_t)
+
+
+def gradient(prob, x):
+    """softmax.py:166-169: data gradient + lam x."""
+    view = _view(prob.dataset)
+    w, as_t = vec_in(x, view.dim)
+    G, _ = gradient_parts(view, w, 1.0, prob.lam)
+    return vec_out(G, as_t)
+
+
+class HessianOperator:
+    """v -> scale * H_data(x) v + lam * v over the rows of `ds` (softmax.py:172-212).
+
+    The per-row softmax probabilities h(a_i, x_c) are computed once at
+    construction (snx_hess_prepare) and kept in HBM; each `apply` costs one
+    fused pass of two feature products (snx_hess_apply).
+    """
+
+    _snx_device = True
+
+    def __init__(self, ds, x, lam, scale=1.0, block_rows=BLOCK_ROWS):
+        view = _view(ds)
+        w, _ = vec_in(x, view.dim)
+        self.view = view
+        self.ds = ds
+        self.lam = float(lam)
+        self.scale = float(scale)
+        self.block_rows = block_rows
+        self.p, self.C = view.n_features, view.n_classes
+        self.dim = view.dim
+        tdtype = view.X.dtype
+        self._h = torch.empty((max(view.n_rows, 1), view.K), dtype=tdtype, device=w.device)
+        _lib.call("snx_hess_prepare", *_args(view), ptr(view.labels), ptr(w), ptr(self._h),
+                  *_ws(view), stream_handle())
+
+    def apply_into(self, v, out, dots=None, skip=None):
+        """Device-only apply: out = H v; optional CG dot partials and skip flag."""
+        _lib.call("snx_hess_apply", *_args(self.view), ptr(self._h), ptr(v), self.scale,
+                  self.lam, ptr(out), ptr(dots), skip, *_ws(self.view), stream_handle())
+        return out
+
+    def apply(self, v):
+        if isinstance(v, torch.Tensor) or np.asarray(v).shape == (self.dim,):
+            vv, as_t = vec_in(v, self.dim, "vector")
+        else:
+            raise DimensionError(
+                f"expected vector of length {self.dim}, got {np.asarray(v).shape}")
+        out = torch.empty_like(vv)
+        self.apply_into(vv, out)
+        return vec_out(out, as_t)
+
+    __call__ = apply
+
+
+def hess_vec(prob, x, v):
+    """softmax.py:215-221: one-shot operator + apply."""
+    return HessianOperator(prob.dataset, x, prob.lam).apply(v)
+
+
+def correct_count(ds, x):
+    """Device count of rows whose most probable class equals the label."""
+    view = _view(ds)
+    w, _ = vec_in(x, view.dim)
+    _, corr = objective_parts(view, w, want_correct=True)
+    return corr
+
+
+def accuracy(ds, x):
+    """softmax.py:243-247: fraction of rows predicted correctly (ties -> lowest class)."""
+    view = _view(ds)
+    if view.n_rows == 0:
+        raise DataError("accuracy is undefined on an empty dataset")
+    return float(correct_count(view, x)) / view.n_rows
+
+
+__all__ = [
+    "BLOCK_ROWS", "SoftmaxProblem", "zero_weights", "weights_as_matrix", "matrix_as_weights",
+    "data_objective", "objective", "data_gradient", "gradient", "HessianOperator", "hess_vec",
+    "accuracy", "correct_count", "objective_parts", "gradient_parts", "DeviceDataset",
+    "DeviceView",
+]
