@@ -23,8 +23,8 @@
  *     flat class-major, d = K*p, w[c*p + j] for weighted class c < K = C-1:
  *     exactly the reference layout x.reshape((p, C-1), order="F")
  *     (softmax.py:62-74).
- *   - rows: optional int64 row indices (a sorted sample S, sampling.py:38-45);
- *     NULL means rows 0..nrows-1.  labels are int32 in [0, C).
+ *   - rows: int64 row indices of a sorted sample S (sampling.py:38-45);
+ *     labels are int32 in [0, C).  X pointers must be 16-byte aligned.
  *   - Return 0 on success; non-zero => snx_last_error() has the message.
  *   - Every reduction runs in a fixed order: results are bit-identical run
  *     to run (the reference's reruns are, tests/test_newton.py:102-114).
@@ -53,42 +53,50 @@ const char *snx_last_error(void);
  * zero-filled once when allocated; calls leave its counters at zero. */
 size_t snx_workspace_bytes(int dtype, int64_t nrows, int32_t p, int32_t K);
 
+/* Row gather (the reference's dataset.take, dataset.py:90-97, 180-185):
+ * X_out[r][0:ld_out] = X[rows[r]][0:ld_out]; labels_out[r] = labels[rows[r]]
+ * (labels/labels_out nullable).  Materialises a sample S once so every later
+ * pass streams contiguous rows through TMA tiles. */
+int snx_gather_rows(int dtype, const void *X, int64_t ldx, const int32_t *labels,
+                    const int64_t *rows, int64_t nrows, void *X_out, int64_t ld_out,
+                    int32_t *labels_out, void *stream);
+
 /* softmax.py:125-141 (data_objective/objective) + softmax.py:239-247
- * (predict/accuracy), evaluated at w_eff = w + alpha*dir (dir may be NULL;
- * the line-search trial x + a*p of newton.py:92 without materialising it).
+ * (predict/accuracy) over rows 0..nrows-1 of X, evaluated at
+ * w_eff = w + alpha*dir (dir may be NULL; the line-search trial x + a*p of
+ * newton.py:92 without materialising it).
  *   out[0] = sum_i (M_i + log alpha_i - lin_i)   (data loss)
  *   out[1] = ||w_eff||^2                          (for lam/2 ||x||^2)
  *   correct_out[0] (nullable) = #rows with argmax prob == label. */
-int snx_objective(int dtype, const void *X, int64_t ldx, const int64_t *rows,
-                  int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
-                  const double *w, const double *dir, double alpha, double *out,
-                  int64_t *correct_out, void *ws, size_t ws_bytes, void *stream);
+int snx_objective(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
+                  const int32_t *labels, const double *w, const double *dir, double alpha,
+                  double *out, int64_t *correct_out, void *ws, size_t ws_bytes, void *stream);
 
 /* softmax.py:144-169 (data_gradient/gradient), sampling.py:84-87:
- *   G_out = scale * vec(X_rows^T (E/alpha - onehot)) + lam * w
+ *   G_out = scale * vec(X^T (E/alpha - onehot)) + lam * w
  * plus out[0..1] as snx_objective (the loss comes for free). */
-int snx_objective_grad(int dtype, const void *X, int64_t ldx, const int64_t *rows,
-                       int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
-                       const double *w, double scale, double lam, double *out,
-                       double *G_out, void *ws, size_t ws_bytes, void *stream);
+int snx_objective_grad(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                       int32_t K, const int32_t *labels, const double *w, double scale,
+                       double lam, double *out, double *G_out, void *ws, size_t ws_bytes,
+                       void *stream);
 
-/* softmax.py:181-195 (HessianOperator.__init__): H_out[r*K + c] =
- * h(a_rows[r], x_c) = E_rc / alpha_r, stored in the X dtype. */
-int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
-                     int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
-                     const double *w, void *H_out, void *ws, size_t ws_bytes,
-                     void *stream);
+/* softmax.py:181-195 (HessianOperator.__init__) on the sample rows S_H:
+ * when rows != NULL the sample is first gathered into Xs_out (ld_out), else
+ * X itself is the sample (the f = 1 identity, dataset.py:94-96).
+ *   H_out[r*K + c] = h(a_r, x_c) = E_rc / alpha_r, stored in the X dtype. */
+int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+                     int32_t p, int32_t K, const double *w, void *Xs_out, int64_t ld_out,
+                     void *H_out, void *ws, size_t ws_bytes, void *stream);
 
-/* softmax.py:197-210 (HessianOperator.apply), scale = n/|S_H| (sampling.py:82):
- *   Hv_out = scale * vec(X_S^T (V.W - W.rowsum(V.W))) + lam * v,  V = X_S Q(v)
- * dots (nullable, SNX_DOT_BLOCKS*2 doubles): per-block partials of v.Hv and v.v
- * (the CG curvature test, cg.py:78).  skip (nullable): if *skip != 0 the
+/* softmax.py:197-210 (HessianOperator.apply), scale = n/|S_H| (sampling.py:82),
+ * on the contiguous sample Xs prepared above:
+ *   Hv_out = scale * vec(Xs^T (V.W - W.rowsum(V.W))) + lam * v,  V = Xs Q(v)
+ * dots (nullable, 2*SNX_DOT_BLOCKS doubles): fixed-count partials of v.Hv and
+ * v.v (the CG curvature test, cg.py:78).  skip (nullable): if *skip != 0 the
  * call is a no-op (device-side early exit of a captured CG loop). */
-int snx_hess_apply(int dtype, const void *X, int64_t ldx, const int64_t *rows,
-                   int64_t nrows, int32_t p, int32_t K, const void *H,
-                   const double *v, double scale, double lam, double *Hv_out,
-                   double *dots, const double *skip, void *ws, size_t ws_bytes,
-                   void *stream);
+int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
+                   const void *H, const double *v, double scale, double lam, double *Hv_out,
+                   double *dots, const double *skip, void *ws, size_t ws_bytes, void *stream);
 
 /* Fixed-order dot product: out[0] = x . y (np.dot / np.linalg.norm**2).
  * out must hold 1 + SNX_DOT_BLOCKS doubles (out[1..] = block partials). */

@@ -24,13 +24,15 @@ SIGNATURES = {
     "snx_abi_version": (_c_int, []),
     "snx_last_error": (ctypes.c_char_p, []),
     "snx_workspace_bytes": (_c_size, [_c_int, _c_i64, _c_i32, _c_i32]),
-    "snx_objective": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
-                               _c_p, _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
-    "snx_objective_grad": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p,
-                                    _c_p, _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_gather_rows": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_p, _c_i64, _c_p, _c_i64, _c_p,
+                                 _c_p]),
+    "snx_objective": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p,
+                               _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_objective_grad": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                    _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_hess_prepare": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p,
-                                  _c_p, _c_p, _c_p, _c_size, _c_p]),
-    "snx_hess_apply": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                  _c_p, _c_i64, _c_p, _c_p, _c_size, _c_p]),
+    "snx_hess_apply": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                 _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_dot": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "snx_dot_partials": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),

@@ -18,24 +18,32 @@ inline size_t dtype_bytes(int dtype) { return dtype == SNX_F64 ? 8 : 4; }
 
 // Row-pass launch geometry (shared by workspace sizing and the launchers).
 struct Geometry {
-  int rows_per_warp;
-  int warps;
-  int64_t rowpass_blocks;  // blocks of the GEMM1+epilogue kernel
-  int xtu_tiles;           // column tiles of the GEMM2 kernel
-  int64_t splits;          // row splits of the GEMM2 kernel
-  int64_t rows_per_split;
+  int grid1, grid2;    // persistent CTAs (<= one per SM, <= items)
+  // GEMM1 (logits): items = row_blocks x nchunks, stream-K over `grid` CTAs
+  int chunk;           // columns per chunk (512 B)
+  int nchunks;
+  int64_t row_blocks;  // 64-row blocks
+  int64_t g1_items;
+  int g1_maxseg;       // CTA segments per row block (upper bound)
+  // GEMM2 (X^T U): items = col_tiles x rchunks, stream-K over `grid` CTAs
+  int tcol;            // columns per tile (1 KB)
+  int col_tiles;
+  int rchunks;         // 32-row chunks
+  int64_t g2_items;
+  int g2_maxseg;
 };
-Geometry geometry(int dtype, int64_t nrows, int32_t P);
+Geometry geometry(int dtype, int64_t nrows, int32_t P, int32_t K);
 
 // Workspace carve-up (byte offsets), all 256-B aligned.
 struct Workspace {
   size_t weights;     // K*P of T: weights converted to the X dtype
-  size_t rowbuf;      // nrows*K of T: R / W / U per row
-  size_t partial;     // splits*K*P of T: GEMM2 partials
-  size_t loss_part;   // rowpass_blocks doubles
-  size_t corr_part;   // rowpass_blocks uint64
-  size_t dot_part;    // 4*kDotBlocks doubles (w.w, v.Hv, v.v)
-  size_t counters;    // 16 uint32 (zero at rest; kernels restore zero)
+  size_t rowbuf;      // nrows*K of T: R / U per row (+ slack)
+  size_t zp;          // nslices*nrows*K doubles: GEMM1 slice partials
+  size_t gp;          // rsplits*K*P doubles: GEMM2 split partials
+  size_t loss_part;   // row_blocks doubles
+  size_t corr_part;   // row_blocks uint64
+  size_t dot_part;    // 4*kDotBlocks doubles (w.w partials)
+  size_t counters;    // uint32 scheduler words + arrival counters (zero at rest)
   size_t total;
 };
 Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K);

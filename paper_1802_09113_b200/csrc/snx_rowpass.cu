@@ -1,39 +1,299 @@
 // Row-pass kernels: the two feature products of every softmax quantity.
 //
-//   GEMM1 + row epilogue  (rowpass_kernel): z_r = X[row_r] . W  (K logits per
-//       row, softmax.py:91 / :206) followed by the per-row softmax algebra of
-//       softmax.py:85-99 (objective, accuracy), :157-161 (gradient residual),
-//       :189-195 (Hessian probabilities) or :206-208 (ComputeU).
-//   GEMM2 (xtu_kernel + finalize_kernel): out = scale * X_rows^T U + lam * base
-//       (softmax.py:162 / :209-210) with a split over rows and a fixed-order
-//       reduction of the split partials (no float atomics => reruns are
-//       bit-identical).
+//   GEMM1 + row epilogue (gemm1_kernel): z_r = X[r] . W (K logits per row,
+//     softmax.py:91 / :206) followed by the per-row softmax algebra of
+//     softmax.py:85-99 (objective, accuracy), :157-161 (gradient residual),
+//     :189-195 (Hessian probabilities) or :206-208 (ComputeU).
+//   GEMM2 (gemm2_kernel): out = scale * X^T U + lam * base
+//     (softmax.py:162 / :209-210), plus the CG dot partials of out.
 //
-// v1 layout: X row-major (ldx), rows optionally gathered through an index
-// array (the sample S_H / S_g, no materialised X_S copy).  GEMM1 maps lanes to
-// features with 16-byte vector loads (coalesced row streams) and one warp to
-// RW rows; GEMM2 maps threads to feature columns and streams rows.
+// Both kernels are persistent and warp-specialised (sm_100a):
+//   * one producer warp streams tiles into a ring of shared-memory stages with
+//     2-D tensor-map TMA (cp.async.bulk.tensor, 8-32 KB boxes; out-of-range
+//     rows/columns arrive zero-filled) completing on mbarriers; eight consumer
+//     warps do the fp64/fp32 FMAs from shared memory.  Rows are contiguous: a
+//     sample S_H is materialised once per outer iteration (snx_gather_rows /
+//     snx_hess_prepare), then every Hessian product streams it as tiles;
+//   * work units are handed out dynamically (one atomic ticket per unit) so
+//     all SMs stay busy to the end;
+//   * GEMM1 unit = (64-row block, feature slice).  X boxes are 64 rows x 128 B
+//     with the 128-B swizzle, so lanes can own rows (2 each) without bank
+//     conflicts while the weights are smem broadcasts; warps own 64-B column
+//     strips.  The 8 warp partials are reduced in smem, the slice partial goes
+//     to L2, and the last slice to arrive for a row block (arrival counter)
+//     sums the slices in fixed order and runs the epilogue;
+//   * GEMM2 unit = (feature tile, row split).  Lanes own 2 x 16 B of
+//     consecutive columns, U rows are smem broadcasts, warps split rows; the
+//     last row split to arrive for a tile sums the split partials in fixed
+//     order and writes scale*X^T U + lam*base and the tile's dot partials.
+// Every reduction has a fixed order and there are no float atomics: results
+// are bit-identical run to run.
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "snx_common.cuh"
 #include "snx_internal.h"
+#include "snx_pipe.cuh"
 
 namespace snx {
 
 enum Mode { kObjective = 0, kGradient = 1, kHessPrep = 2, kHessApply = 3 };
 
-struct RowArgs {
-  const void *X;
-  int64_t ldx;
-  const int64_t *rows;
+constexpr int kWarps = 8;                    // consumer warps
+constexpr int kConsumers = kWarps * 32;      // consumer threads
+constexpr int kThreads = kConsumers + 32;    // + one producer warp
+constexpr int kRB = 96;                      // rows per GEMM1 item (3 per lane)
+constexpr int kEpiThreads = 4 * kRB;         // epilogue: 4 threads per row
+constexpr int kG2Rows = 32;                  // rows per GEMM2 item
+constexpr int kMaxTiles = kDotBlocks;
+constexpr size_t kSmemBudget = 220 * 1024;
+constexpr int64_t kMaxRowBlocks = 1 << 17;   // 12.5M rows per call
+constexpr int kCounterWords = 16 + kMaxTiles + kMaxRowBlocks;
+
+__host__ __device__ constexpr size_t cround(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// GEMM1 shape: an item is (96-row block) x (512 B of columns).  X arrives as
+// four 96-row x 128-B boxes with the 128-B swizzle; warp w owns the 64-B strip
+// (w & 1) of box (w >> 1); lanes own rows lane, lane+32, lane+64 (they share
+// the swizzle phase lane & 7), so the weights are smem broadcasts.
+template <typename T, int K> struct G1Shape {
+  static constexpr int V = 16 / (int)sizeof(T);
+  static constexpr int BOXC = 128 / (int)sizeof(T);
+  static constexpr int WC = 64 / (int)sizeof(T);
+  static constexpr int CHUNK = kWarps * WC;
+  static constexpr int NB = CHUNK / BOXC;
+  static constexpr size_t BOX = (size_t)kRB * 128;
+  static constexpr size_t WBYTES = (size_t)K * CHUNK * sizeof(T);
+  static constexpr size_t STAGE = cround(NB * BOX + WBYTES, 1024);
+  static constexpr size_t RED = (size_t)(kWarps / 2) * kRB * K * 8;
+  static constexpr int S = (3 * STAGE + RED + 256 <= kSmemBudget) ? 3 : 2;
+  static constexpr size_t SMEM = S * STAGE + RED + 2 * S * 8 + 64;
+};
+
+// GEMM2 shape: an item is (1-KB column tile) x (32 rows); lanes own 2 x 16 B of
+// consecutive columns; U rows are padded to a 16-B multiple (KP) so each row
+// is a few 128-bit smem broadcasts.
+template <typename T, int K> struct G2Shape {
+  static constexpr int V = 16 / (int)sizeof(T);
+  static constexpr int LC = 2 * V;
+  static constexpr int TCOL = 32 * LC;
+  static constexpr int KP = (int)(cround(K * sizeof(T), 16) / sizeof(T));
+  static constexpr size_t XB = (size_t)kG2Rows * TCOL * sizeof(T);
+  static constexpr size_t UB = (size_t)kG2Rows * KP * sizeof(T);
+  static constexpr size_t STAGE = cround(XB + UB, 128);
+  static constexpr size_t RED = (size_t)(kWarps / 2) * K * TCOL * 8;
+  static constexpr int S = (4 * STAGE + RED + 256 <= kSmemBudget)   ? 4
+                           : (3 * STAGE + RED + 256 <= kSmemBudget) ? 3
+                                                                    : 2;
+  static constexpr size_t SMEM = S * STAGE + RED + 2 * S * 8 + 64;
+};
+
+inline int u_stride(int dtype, int K) {  // padded U row stride (elements)
+  const int tb = dtype == SNX_F64 ? 8 : 4;
+  return (int)(cround((size_t)K * tb, 16) / tb);
+}
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ void lds(const double *p, double (&o)[2]) {
+  const double2 v = *reinterpret_cast<const double2 *>(p);
+  o[0] = v.x;
+  o[1] = v.y;
+}
+__device__ __forceinline__ void lds(const float *p, float (&o)[4]) {
+  const float4 v = *reinterpret_cast<const float4 *>(p);
+  o[0] = v.x;
+  o[1] = v.y;
+  o[2] = v.z;
+  o[3] = v.w;
+}
+
+// fixed-order u64 sum over the block; valid in thread 0
+template <int NT>
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v,
+                                                            unsigned long long *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < NT / 32; ++i) t += sh[i];
+  }
+  __syncthreads();
+  return t;
+}
+
+// Stream-K split of `items` over `G` CTAs: CTA c owns [T*c/G, T*(c+1)/G).
+__host__ __device__ __forceinline__ int64_t sk_begin(int64_t T, int G, int c) {
+  return T * c / G;
+}
+__host__ __device__ __forceinline__ int sk_owner(int64_t T, int G, int64_t i) {
+  return (int)(((i + 1) * G - 1) / T);
+}
+
+// ---------------------------------------------------------------- GEMM1
+struct G1Args {
+  CUtensorMap xmap;  // X: [nrows][P] boxes of 96 rows x 128 B, 128-B swizzle
+  CUtensorMap wmap;  // W: [K][P] boxes of K rows x CHUNK columns
   int64_t nrows;
-  int P;
+  int nchunks;     // CHUNK-column chunks per row (ceil(P / CHUNK))
+  int maxseg;      // max CTA segments per row block
+  int64_t items;   // row_blocks * nchunks, split evenly over the CTAs
+  double *zp;      // [row_blocks][maxseg][kRB][K] segment partial logits
+  const double *skip;
+};
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constant__ G1Args a) {
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  using Sh = G1Shape<T, K>;
+  constexpr int V = Sh::V, S = Sh::S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double *red = reinterpret_cast<double *>(smem + S * Sh::STAGE);  // [4][kRB][K]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * Sh::STAGE + Sh::RED);
+  uint64_t *empty = full + S;
+
+  if (tid == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
+  if (i0 == i1) return;  // more CTAs than items (the host never launches that)
+  const int64_t rb0 = i0 / a.nchunks;
+  const int ch0 = (int)(i0 - rb0 * a.nchunks);
+
+  if (warp == kWarps) {
+    // ------------------------------------------------ producer warp (TMA)
+    if (lane == 0) {
+      tma_prefetch_desc(&a.xmap);
+      tma_prefetch_desc(&a.wmap);
+      constexpr unsigned kTx = (unsigned)(Sh::NB * Sh::BOX + Sh::WBYTES);
+      int64_t rb = rb0;
+      int ch = ch0;
+      for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
+        const int s = (int)(it % S);
+        mbar_wait(&empty[s], (unsigned)((it / S) & 1) ^ 1u);
+        mbar_arrive_expect_tx(&full[s], kTx);
+        unsigned char *st = smem + s * Sh::STAGE;
+        const int col = ch * Sh::CHUNK, row = (int)(rb * kRB);
+#pragma unroll
+        for (int b = 0; b < Sh::NB; ++b)
+          tma_load_2d(st + b * Sh::BOX, &a.xmap, col + b * Sh::BOXC, row, &full[s]);
+        tma_load_2d(st + Sh::NB * Sh::BOX, &a.wmap, col, 0, &full[s]);
+        if (++ch == a.nchunks) {
+          ch = 0;
+          ++rb;
+        }
+      }
+    }
+    return;
+  }
+
+  // -------------------------------------------------- consumer warps
+  const int box = warp >> 1;
+  const int c0 = (warp & 1) * 4;  // first 16-B chunk of this warp's strip
+  const int sw = lane & 7;        // swizzle phase of rows lane, lane+32, lane+64
+  T acc0[K], acc1[K], acc2[K];
+#pragma unroll
+  for (int c = 0; c < K; ++c) acc0[c] = acc1[c] = acc2[c] = T(0);
+  int64_t rb = rb0;
+  int ch = ch0;
+  for (int64_t i = i0, it = 0; i <= i1; ++i) {
+    if (i == i1 || (ch == 0 && i > i0)) {
+      // flush the segment partial of the row block just finished: warp pairs
+      // (w, w+4) in smem, then the 4 pair sums in order
+      const int64_t frb = (i == i1 && ch != 0) ? rb : rb - 1;
+      double *mine = red + (size_t)(warp & 3) * kRB * K;
+      if (warp >= 4) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          mine[lane * K + c] = (double)acc0[c];
+          mine[(lane + 32) * K + c] = (double)acc1[c];
+          mine[(lane + 64) * K + c] = (double)acc2[c];
+        }
+      }
+      consumer_sync(kConsumers);
+      if (warp < 4) {
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          mine[lane * K + c] = (double)acc0[c] + mine[lane * K + c];
+          mine[(lane + 32) * K + c] = (double)acc1[c] + mine[(lane + 32) * K + c];
+          mine[(lane + 64) * K + c] = (double)acc2[c] + mine[(lane + 64) * K + c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) acc0[c] = acc1[c] = acc2[c] = T(0);
+      consumer_sync(kConsumers);
+      const int seg = cta - sk_owner(a.items, G, frb * a.nchunks);
+      double *zb = a.zp + (frb * a.maxseg + seg) * (int64_t)kRB * K;
+      const int valid = (int)min((int64_t)kRB, a.nrows - frb * kRB) * K;
+      for (int t = tid; t < valid; t += kConsumers) {
+        const double z = ((red[t] + red[kRB * K + t]) + red[2 * kRB * K + t]) +
+                         red[3 * kRB * K + t];
+        zb[t] = z;
+      }
+      consumer_sync(kConsumers);  // red free again
+    }
+    if (i == i1) break;
+    const int s = (int)(it % S);
+    mbar_wait(&full[s], (unsigned)((it / S) & 1));
+    const unsigned char *st = smem + s * Sh::STAGE;
+    const unsigned char *xa = st + box * Sh::BOX + lane * 128;
+    const T *wp = reinterpret_cast<const T *>(st + Sh::NB * Sh::BOX) + warp * Sh::WC;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int off = ((c0 + q) ^ sw) * 16;
+      T v0[V], v1[V], v2[V];
+      lds(reinterpret_cast<const T *>(xa + off), v0);
+      lds(reinterpret_cast<const T *>(xa + 32 * 128 + off), v1);
+      lds(reinterpret_cast<const T *>(xa + 64 * 128 + off), v2);
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+        T w[V];
+        lds(wp + c * Sh::CHUNK + q * V, w);  // warp-uniform address: broadcast
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          acc0[c] = fma(v0[v], w[v], acc0[c]);
+          acc1[c] = fma(v1[v], w[v], acc1[c]);
+          acc2[c] = fma(v2[v], w[v], acc2[c]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    ++it;
+    if (++ch == a.nchunks) {
+      ch = 0;
+      ++rb;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- epilogue
+struct E1Args {
+  int64_t nrows;
+  int nchunks;
+  int maxseg;
+  int grid;        // CTAs of the GEMM1 launch
+  int64_t items;
+  int ustride;     // row stride of rowout (K for h, padded KP for R / U)
+  const double *zp;
   const int32_t *labels;
-  const void *W;      // K*P weights (X dtype), class-major
-  const void *H;      // kHessApply: nrows*K probabilities (X dtype)
-  void *rowout;       // nrows*K: R (gradient), h (prep), U (apply)
-  double *loss_part;  // per-block partial losses
+  const void *H;   // kHessApply: nrows*K probabilities
+  void *rowout;    // R (gradient), h (prep), U (apply)
+  double *loss_part;   // [blocks]
   unsigned long long *corr_part;
   unsigned *counter;
   double *loss_out;
@@ -41,67 +301,51 @@ struct RowArgs {
   const double *skip;
 };
 
-constexpr int kWarps = 8;
-
-template <typename T, int K, int MODE, int RW>
-__global__ void __launch_bounds__(kWarps * 32) rowpass_kernel(RowArgs a) {
+// Row epilogue: block b owns rows [96b, 96b+96); 4 threads per row sum the
+// CTA segment partials (fixed order), part 0 runs the softmax algebra.
+template <typename T, int K, int MODE>
+__global__ void __launch_bounds__(kEpiThreads) g1_epilogue_kernel(const E1Args a) {
   if (a.skip != nullptr && *a.skip != 0.0) return;
-  constexpr int V = Vec<T>::N;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t r0 = ((int64_t)blockIdx.x * kWarps + warp) * RW;
-  const T *__restrict__ X = static_cast<const T *>(a.X);
-  const T *__restrict__ W = static_cast<const T *>(a.W);
-
-  const T *xr[RW];
-#pragma unroll
-  for (int q = 0; q < RW; ++q) {
-    int64_t r = r0 + q;
-    if (r >= a.nrows) r = a.nrows - 1;  // clamp; results of padding rows are dropped
-    const int64_t g = a.rows ? a.rows[r] : r;
-    xr[q] = X + g * a.ldx;
-  }
-
-  T acc[RW][K];
-#pragma unroll
-  for (int q = 0; q < RW; ++q)
-#pragma unroll
-    for (int c = 0; c < K; ++c) acc[q][c] = T(0);
-
-  for (int j = lane * V; j < a.P; j += 32 * V) {
-    T w[K][V];
-#pragma unroll
-    for (int c = 0; c < K; ++c) ldv(W + (size_t)c * a.P + j, w[c]);
-#pragma unroll
-    for (int q = 0; q < RW; ++q) {
-      T x[V];
-      ldv(xr[q] + j, x);
-#pragma unroll
-      for (int c = 0; c < K; ++c)
-#pragma unroll
-        for (int v = 0; v < V; ++v) acc[q][c] = fma(x[v], w[c][v], acc[q][c]);
-    }
-  }
-#pragma unroll
-  for (int q = 0; q < RW; ++q)
-#pragma unroll
-    for (int c = 0; c < K; ++c) acc[q][c] = warp_allsum(acc[q][c]);
-
-  // lane q < RW runs the epilogue of row r0+q in fp64
+  __shared__ double shd[kEpiThreads / 32];
+  __shared__ unsigned long long shu[kEpiThreads / 32];
+  __shared__ bool last;
+  const int tid = threadIdx.x;
+  const int lr = tid >> 2, part = tid & 3;
+  const int64_t rb = blockIdx.x;
+  const int64_t r = rb * kRB + lr;
+  const bool valid = r < a.nrows;
   double z[K];
 #pragma unroll
-  for (int c = 0; c < K; ++c) z[c] = (double)acc[0][c];
+  for (int c = 0; c < K; ++c) z[c] = 0.0;
+  if (valid) {
+    // segments of this row block = the CTAs that covered its chunks, in order
+    const int c_lo = sk_owner(a.items, a.grid, rb * a.nchunks);
+    const int nseg = sk_owner(a.items, a.grid, (rb + 1) * a.nchunks - 1) - c_lo + 1;
+    const double *zb = a.zp + (rb * a.maxseg * kRB + lr) * K;
+    int sg = part;
+    for (; sg + 4 < nseg; sg += 8) {  // two segments' loads in flight
+      double v0[K], v1[K];
 #pragma unroll
-  for (int q = 1; q < RW; ++q)
-    if (lane == q) {
+      for (int c = 0; c < K; ++c) {
+        v0[c] = __ldcg(zb + (int64_t)sg * kRB * K + c);
+        v1[c] = __ldcg(zb + (int64_t)(sg + 4) * kRB * K + c);
+      }
 #pragma unroll
-      for (int c = 0; c < K; ++c) z[c] = (double)acc[q][c];
+      for (int c = 0; c < K; ++c) z[c] = (z[c] + v0[c]) + v1[c];
     }
-  const int64_t r = r0 + lane;
-  const bool mine = lane < RW && r < a.nrows;
+    for (; sg < nseg; sg += 4) {
+#pragma unroll
+      for (int c = 0; c < K; ++c) z[c] += __ldcg(zb + (int64_t)sg * kRB * K + c);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < K; ++c) {  // (p0+p1)+(p2+p3), identical on the 4 lanes
+    z[c] += __shfl_xor_sync(0xffffffffu, z[c], 1);
+    z[c] += __shfl_xor_sync(0xffffffffu, z[c], 2);
+  }
   double loss = 0.0;
   unsigned long long corr = 0;
-  if (mine) {
-    const int64_t g = a.rows ? a.rows[r] : r;
+  if (valid && part == 0) {
     if (MODE == kHessApply) {
       // softmax.py:206-208: VW = V*W; U = VW - W*rowsum(VW)
       const T *h = static_cast<const T *>(a.H) + r * K;
@@ -112,7 +356,7 @@ __global__ void __launch_bounds__(kWarps * 32) rowpass_kernel(RowArgs a) {
         vw[c] = z[c] * hw[c];
         s += vw[c];
       }
-      T *u = static_cast<T *>(a.rowout) + r * K;
+      T *u = static_cast<T *>(a.rowout) + r * a.ustride;
 #pragma unroll
       for (int c = 0; c < K; ++c) u[c] = (T)(vw[c] - hw[c] * s);
     } else {
@@ -120,27 +364,26 @@ __global__ void __launch_bounds__(kWarps * 32) rowpass_kernel(RowArgs a) {
       double M = 0.0;
 #pragma unroll
       for (int c = 0; c < K; ++c) M = (z[c] > M || isnan(z[c])) ? z[c] : M;  // NaN propagates
-      double E[K], alpha = exp(-M);
-      double se = 0.0;
+      double E[K], se = 0.0;
 #pragma unroll
       for (int c = 0; c < K; ++c) {
         E[c] = exp(z[c] - M);
         se += E[c];
       }
-      alpha += se;
+      const double alpha = exp(-M) + se;
       if (MODE == kHessPrep) {
-        T *h = static_cast<T *>(a.rowout) + r * K;
+        T *h = static_cast<T *>(a.rowout) + r * a.ustride;
 #pragma unroll
         for (int c = 0; c < K; ++c) h[c] = (T)(E[c] / alpha);
       } else {
-        const int y = a.labels[g];
+        const int y = a.labels[r];
         double lin = 0.0;
 #pragma unroll
         for (int c = 0; c < K; ++c)
           if (c == y) lin = z[c];
         loss = (M + log(alpha)) - lin;  // softmax.py:134
         if (MODE == kGradient) {
-          T *R = static_cast<T *>(a.rowout) + r * K;
+          T *R = static_cast<T *>(a.rowout) + r * a.ustride;
 #pragma unroll
           for (int c = 0; c < K; ++c) R[c] = (T)(E[c] / alpha - (c == y ? 1.0 : 0.0));
         } else if (a.corr_out != nullptr) {
@@ -162,131 +405,204 @@ __global__ void __launch_bounds__(kWarps * 32) rowpass_kernel(RowArgs a) {
       }
     }
   }
-  if (MODE == kObjective || MODE == kGradient) {
-    // fixed-order per-block sums, then the last block reduces the partials
-    __shared__ double sl[kWarps];
-    __shared__ unsigned long long sc[kWarps];
-    __shared__ bool last;
-    double wl = 0.0;
-    unsigned long long wc = 0;
-#pragma unroll
-    for (int q = 0; q < RW; ++q) {
-      wl += __shfl_sync(0xffffffffu, loss, q);
-      wc += __shfl_sync(0xffffffffu, corr, q);
-    }
-    if (lane == 0) {
-      sl[warp] = wl;
-      sc[warp] = wc;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double bl = 0.0;
-      unsigned long long bc = 0;
-#pragma unroll
-      for (int i = 0; i < kWarps; ++i) {
-        bl += sl[i];
-        bc += sc[i];
-      }
-      a.loss_part[blockIdx.x] = bl;
-      a.corr_part[blockIdx.x] = bc;
-      __threadfence();
-      last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
-    }
-    __syncthreads();
-    if (last) {
-      __threadfence();
-      __shared__ double sh[kWarps];
-      double t = 0.0;
-      unsigned long long tc = 0;
-      for (int i = threadIdx.x; i < (int)gridDim.x; i += kWarps * 32) {
-        t += ((volatile double *)a.loss_part)[i];
-        tc += ((volatile unsigned long long *)a.corr_part)[i];
-      }
-      const double tot = block_sum<kWarps * 32>(t, sh);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
-      __shared__ unsigned long long shc[kWarps];
-      if (lane == 0) shc[warp] = tc;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        unsigned long long ct = 0;
-        for (int i = 0; i < kWarps; ++i) ct += shc[i];
-        a.loss_out[0] = tot;
-        if (a.corr_out) a.corr_out[0] = (long long)ct;
-        *a.counter = 0u;  // leave the counter at rest
-      }
-    }
+  if (MODE != kObjective && MODE != kGradient) return;
+  const double bl = block_sum<kEpiThreads>(loss, shd);
+  const unsigned long long bc = block_sum_u64<kEpiThreads>(corr, shu);
+  if (tid == 0) {
+    a.loss_part[rb] = bl;
+    a.corr_part[rb] = bc;
+    __threadfence();  // release (cumulative over the barrier above)
+    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
+    if (last) __threadfence();  // acquire
+  }
+  __syncthreads();
+  if (!last) return;
+  double t = 0.0;
+  unsigned long long tc = 0;
+  for (int64_t i = tid; i < (int64_t)gridDim.x; i += kEpiThreads) {
+    t += __ldcg(a.loss_part + i);
+    tc += __ldcg(a.corr_part + i);
+  }
+  const double tot = block_sum<kEpiThreads>(t, shd);
+  const unsigned long long ct = block_sum_u64<kEpiThreads>(tc, shu);
+  if (tid == 0) {
+    a.loss_out[0] = tot;
+    if (a.corr_out) a.corr_out[0] = (long long)ct;
+    *a.counter = 0u;  // rest state for the next launch
   }
 }
 
-// GEMM2 partials: partial[s][c][j] = sum_{r in split s} X[row_r][j] * U[r][c]
+// ---------------------------------------------------------------- GEMM2
+struct G2Args {
+  CUtensorMap xmap;  // X: [nrows][P] boxes of 32 rows x TCOL columns
+  int64_t nrows;
+  int rchunks;     // 32-row chunks (ceil(nrows / 32))
+  int maxseg;      // max CTA segments per column tile
+  int64_t items;   // col_tiles * rchunks, split evenly over the CTAs
+  const void *U;   // nrows rows of KP (padded) elements, X dtype
+  double *gp;      // [col_tiles][maxseg][K][TCOL] segment partials
+  const double *skip;
+};
+
 template <typename T, int K>
-__global__ void __launch_bounds__(128) xtu_kernel(const T *__restrict__ X, int64_t ldx,
-                                                  const int64_t *__restrict__ rows,
-                                                  int64_t nrows, int P,
-                                                  const T *__restrict__ U, int64_t rps,
-                                                  T *__restrict__ partial,
-                                                  const double *skip) {
-  if (skip != nullptr && *skip != 0.0) return;
-  constexpr int V = Vec<T>::N, CH = 64;
-  __shared__ T su[CH * K];
-  __shared__ int64_t sr[CH];
-  const int j = (blockIdx.x * 128 + threadIdx.x) * V;
-  const bool active = j < P;
-  const int64_t rb = (int64_t)blockIdx.y * rps;
-  const int64_t re = min(rb + rps, nrows);
-  T acc[V][K];
+__global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constant__ G2Args a) {
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  using Sh = G2Shape<T, K>;
+  constexpr int V = Sh::V, LC = Sh::LC, TCOL = Sh::TCOL, KP = Sh::KP, S = Sh::S;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double *red = reinterpret_cast<double *>(smem + S * Sh::STAGE);  // [4][K][TCOL]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * Sh::STAGE + Sh::RED);
+  uint64_t *empty = full + S;
+
+  if (tid == 0) {
 #pragma unroll
-  for (int v = 0; v < V; ++v)
-#pragma unroll
-    for (int c = 0; c < K; ++c) acc[v][c] = T(0);
-  for (int64_t c0 = rb; c0 < re; c0 += CH) {
-    const int nch = (int)min((int64_t)CH, re - c0);
-    __syncthreads();
-    for (int t = threadIdx.x; t < nch * K; t += 128) su[t] = U[c0 * K + t];
-    for (int t = threadIdx.x; t < nch; t += 128) sr[t] = rows ? rows[c0 + t] : c0 + t;
-    __syncthreads();
-    if (active) {
-#pragma unroll 4
-      for (int r = 0; r < nch; ++r) {
-        T x[V];
-        ldv(X + sr[r] * ldx + j, x);
-#pragma unroll
-        for (int c = 0; c < K; ++c) {
-          const T u = su[r * K + c];
-#pragma unroll
-          for (int v = 0; v < V; ++v) acc[v][c] = fma(x[v], u, acc[v][c]);
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
+  if (i0 == i1) return;
+  const int tile0 = (int)(i0 / a.rchunks);
+  const int rc0 = (int)(i0 - (int64_t)tile0 * a.rchunks);
+
+  if (warp == kWarps) {
+    // ------------------------------------------------ producer warp (TMA)
+    if (lane == 0) {
+      tma_prefetch_desc(&a.xmap);
+      const T *U = static_cast<const T *>(a.U);
+      int tile = tile0, rc = rc0;
+      for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
+        const int64_t c0 = (int64_t)rc * kG2Rows;
+        const int nr = (int)min((int64_t)kG2Rows, a.nrows - c0);
+        const int s = (int)(it % S);
+        mbar_wait(&empty[s], (unsigned)((it / S) & 1) ^ 1u);
+        const unsigned ub = (unsigned)(nr * KP * sizeof(T));
+        mbar_arrive_expect_tx(&full[s], (unsigned)Sh::XB + ub);
+        unsigned char *st = smem + s * Sh::STAGE;
+        tma_load_2d(st, &a.xmap, tile * TCOL, (int)c0, &full[s]);
+        bulk_g2s(st + Sh::XB, U + c0 * KP, ub, &full[s]);
+        if (++rc == a.rchunks) {
+          rc = 0;
+          ++tile;
         }
       }
     }
+    return;
   }
-  if (active) {
+
+  // -------------------------------------------------- consumer warps
+  T acc[LC][K];
 #pragma unroll
-    for (int c = 0; c < K; ++c)
+  for (int v = 0; v < LC; ++v)
 #pragma unroll
-      for (int v = 0; v < V; ++v)
-        partial[((int64_t)blockIdx.y * K + c) * P + j + v] = acc[v][c];
+    for (int c = 0; c < K; ++c) acc[v][c] = T(0);
+  int tile = tile0, rc = rc0;
+  for (int64_t i = i0, it = 0; i <= i1; ++i) {
+    if (i == i1 || (rc == 0 && i > i0)) {
+      // flush the segment partial of the tile just finished: warp pairs
+      // (w, w+4), then the 4 pair sums in order
+      const int ftile = (i == i1 && rc != 0) ? tile : tile - 1;
+      double *mine = red + (size_t)(warp & 3) * K * TCOL + lane * LC;
+      if (warp >= 4) {
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+#pragma unroll
+          for (int v = 0; v < LC; ++v) mine[c * TCOL + v] = (double)acc[v][c];
+      }
+      consumer_sync(kConsumers);
+      if (warp < 4) {
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+#pragma unroll
+          for (int v = 0; v < LC; ++v)
+            mine[c * TCOL + v] = (double)acc[v][c] + mine[c * TCOL + v];
+      }
+#pragma unroll
+      for (int v = 0; v < LC; ++v)
+#pragma unroll
+        for (int c = 0; c < K; ++c) acc[v][c] = T(0);
+      consumer_sync(kConsumers);
+      const int seg = cta - sk_owner(a.items, G, (int64_t)ftile * a.rchunks);
+      double *gb = a.gp + ((int64_t)ftile * a.maxseg + seg) * K * TCOL;
+      for (int t = tid; t < K * TCOL; t += kConsumers)
+        gb[t] = ((red[t] + red[K * TCOL + t]) + red[2 * K * TCOL + t]) + red[3 * K * TCOL + t];
+      consumer_sync(kConsumers);  // red free again
+    }
+    if (i == i1) break;
+    const int s = (int)(it % S);
+    mbar_wait(&full[s], (unsigned)((it / S) & 1));
+    const int nr = (int)min((int64_t)kG2Rows, a.nrows - (int64_t)rc * kG2Rows);
+    const T *xs = reinterpret_cast<const T *>(smem + s * Sh::STAGE);
+    const T *us = reinterpret_cast<const T *>(smem + s * Sh::STAGE + Sh::XB);
+    for (int r = warp; r < nr; r += kWarps) {
+      T x0[V], x1[V];
+      lds(xs + r * TCOL + lane * LC, x0);
+      lds(xs + r * TCOL + lane * LC + V, x1);
+      T u[KP];
+#pragma unroll
+      for (int k = 0; k < KP; k += V) {  // 128-bit broadcasts of the U row
+        T t4[V];
+        lds(us + r * KP + k, t4);
+#pragma unroll
+        for (int v = 0; v < V; ++v) u[k + v] = t4[v];
+      }
+#pragma unroll
+      for (int c = 0; c < K; ++c) {
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+          acc[v][c] = fma(x0[v], u[c], acc[v][c]);
+          acc[V + v][c] = fma(x1[v], u[c], acc[V + v][c]);
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    ++it;
+    if (++rc == a.rchunks) {
+      rc = 0;
+      ++tile;
+    }
   }
 }
 
-// out[c*p + j] = scale * sum_s partial[s][c*P + j] + lam * base[c*p + j]
-// (numpy rounding: two products, one add), optional per-block partials of
+// out[c*p + j] = scale * sum_seg gp[tile][seg][c][j % TCOL] + lam * base[c*p + j]
+// with the segments (CTAs that covered the tile) summed in CTA order (numpy
+// rounding: two products, one add), plus kDotBlocks fixed-order partials of
 // base.out and base.base (the CG curvature test).
-template <typename T>
 __global__ void __launch_bounds__(kDotThreads)
-    finalize_kernel(const T *__restrict__ partial, int64_t splits, int K, int p, int P,
-                    double scale, double lam, const double *__restrict__ base,
-                    double *__restrict__ out, double *dots, const double *skip) {
+    finalize_kernel(const double *__restrict__ gp, int64_t items, int grid, int rchunks,
+                    int maxseg, int tcol, int K, int p, double scale, double lam,
+                    const double *__restrict__ base, double *__restrict__ out, double *dots,
+                    const double *skip) {
   if (skip != nullptr && *skip != 0.0) return;
   __shared__ double sh[kDotThreads / 32];
   double bo = 0.0, bb = 0.0;
-  const int64_t d = (int64_t)K * p, stride = (int64_t)K * P;
+  const int64_t d = (int64_t)K * p;
   for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
        i += (int64_t)kDotBlocks * kDotThreads) {
-    const int64_t c = i / p;
-    const int64_t pi = c * P + (i - c * p);
+    const int c = (int)(i / p);
+    const int j = (int)(i - (int64_t)c * p);
+    const int tile = j / tcol;
+    const int c_lo = sk_owner(items, grid, (int64_t)tile * rchunks);
+    const int nseg = sk_owner(items, grid, (int64_t)(tile + 1) * rchunks - 1) - c_lo + 1;
+    const double *g = gp + ((int64_t)tile * maxseg * K + c) * tcol + (j - tile * tcol);
+    const int64_t sstride = (int64_t)K * tcol;
     double s = 0.0;
-    for (int64_t k = 0; k < splits; ++k) s += (double)partial[k * stride + pi];
+    int sg = 0;
+    for (; sg + 4 <= nseg; sg += 4) {  // independent loads first, fixed-order sum
+      double v[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) v[k] = __ldcg(g + (sg + k) * sstride);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) s += v[k];
+    }
+    for (; sg < nseg; ++sg) s += __ldcg(g + sg * sstride);
     const double b = base[i];
     const double o = __dadd_rn(__dmul_rn(scale, s), __dmul_rn(lam, b));
     out[i] = o;
@@ -303,29 +619,133 @@ __global__ void __launch_bounds__(kDotThreads)
   }
 }
 
+// out = lam * base (the empty dataset: every data term vanishes), with the
+// dot partials the CG expects.
+__global__ void __launch_bounds__(kDotThreads)
+    lam_only_kernel(int K, int p, double lam, const double *__restrict__ base,
+                    double *__restrict__ out, double *dots, const double *skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  __shared__ double sh[kDotThreads / 32];
+  double bo = 0.0, bb = 0.0;
+  const int64_t d = (int64_t)K * p;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    const double b = base[i];
+    const double o = __dadd_rn(0.0, __dmul_rn(lam, b));
+    out[i] = o;
+    bo += b * o;
+    bb += b * b;
+  }
+  if (dots != nullptr) {
+    const double so = block_sum<kDotThreads>(bo, sh);
+    const double sb = block_sum<kDotThreads>(bb, sh);
+    if (threadIdx.x == 0) {
+      dots[blockIdx.x] = so;
+      dots[kDotBlocks + blockIdx.x] = sb;
+    }
+  }
+}
+
+// Row gather (dataset.py:90-97 `take`): dst[r][0:ldd] = X[rows[r]][0:ldd],
+// labels_out[r] = labels[rows[r]]; one warp per row, 16-B vectors.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    gather_rows_kernel(const T *__restrict__ X, int64_t ldx, const int32_t *__restrict__ labels,
+                       const int64_t *__restrict__ rows, int64_t nrows, T *__restrict__ dst,
+                       int64_t ldd, int32_t *__restrict__ labels_out) {
+  constexpr int V = Vec<T>::N;
+  const int lane = threadIdx.x & 31;
+  const int64_t nvec = ldd / V;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < nrows;
+       r += (int64_t)gridDim.x * 8) {
+    const int64_t g = rows[r];
+    const uint4 *src = reinterpret_cast<const uint4 *>(X + g * ldx);
+    uint4 *out = reinterpret_cast<uint4 *>(dst + r * ldd);
+    for (int64_t q = lane; q < nvec; q += 32) out[q] = __ldg(src + q);
+    if (lane == 0 && labels_out != nullptr) labels_out[r] = labels[g];
+  }
+}
+
 // ---------------------------------------------------------------- host side
-Geometry geometry(int dtype, int64_t nrows, int32_t P) {
+static int g_sms = 0;
+
+static int sm_count() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        g_sms <= 0)
+      g_sms = 148;
+  }
+  return g_sms;
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static int make_map(CUtensorMap *m, int dtype, const void *base, uint64_t cols, uint64_t rows,
+                    uint64_t ld, uint32_t box_cols, uint32_t box_rows, bool swizzle) {
+  if (g_encode == nullptr) {
+    void *fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        fn == nullptr) {
+      set_error("snx: cuTensorMapEncodeTiled unavailable (driver too old?)");
+      return 1;
+    }
+    g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }
+  const size_t tb = dtype_bytes(dtype);
+  const cuuint64_t dims[2] = {cols, rows > 0 ? rows : 1};
+  const cuuint64_t strides[1] = {ld * tb};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(
+      m, dtype == SNX_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+      const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("snx: cuTensorMapEncodeTiled failed (%d) for %llux%llu ld=%llu box %ux%u", (int)r,
+              (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)ld,
+              box_rows, box_cols);
+    return 1;
+  }
+  return 0;
+}
+
+static int sk_maxseg(int64_t items, int grid, int per_group) {
+  const int64_t per = items / grid > 0 ? items / grid : 1;
+  return (int)((per_group + per - 1) / per + 1);
+}
+
+Geometry geometry(int dtype, int64_t nrows, int32_t P, int32_t K) {
+  (void)K;
   Geometry g{};
-  g.rows_per_warp = 4;
-  g.warps = kWarps;
-  const int64_t per_block = (int64_t)g.rows_per_warp * g.warps;
-  g.rowpass_blocks = nrows > 0 ? (nrows + per_block - 1) / per_block : 0;
-  const int V = dtype == SNX_F64 ? 2 : 4;
-  g.xtu_tiles = (P + 128 * V - 1) / (128 * V);
-  if (g.xtu_tiles < 1) g.xtu_tiles = 1;
-  int64_t s = (4 * 148 + g.xtu_tiles - 1) / g.xtu_tiles;
-  const int64_t by_rows = (nrows + 31) / 32;
-  if (s > by_rows) s = by_rows;
-  if (s > 128) s = 128;
-  if (s < 1) s = 1;
-  g.rows_per_split = nrows > 0 ? (nrows + s - 1) / s : 1;
-  g.splits = nrows > 0 ? (nrows + g.rows_per_split - 1) / g.rows_per_split : 1;
+  const int sms = sm_count();
+  const size_t tb = dtype_bytes(dtype);
+  // GEMM1: (96-row block x 512-B column chunk) items, stream-K over the CTAs
+  g.chunk = (int)(512 / tb);
+  g.nchunks = (P + g.chunk - 1) / g.chunk;
+  g.row_blocks = nrows > 0 ? (nrows + kRB - 1) / kRB : 0;
+  g.g1_items = g.row_blocks * g.nchunks;
+  // never more CTAs than items: every CTA between a group's first and last
+  // owner then holds a segment of it
+  g.grid1 = (int)(g.g1_items < sms ? (g.g1_items > 0 ? g.g1_items : 1) : sms);
+  g.g1_maxseg = sk_maxseg(g.g1_items, g.grid1, g.nchunks);
+  // GEMM2: (1-KB column tile x 32-row chunk) items, stream-K over the CTAs
+  g.tcol = (int)(1024 / tb);
+  g.col_tiles = (P + g.tcol - 1) / g.tcol;
+  g.rchunks = nrows > 0 ? (int)((nrows + kG2Rows - 1) / kG2Rows) : 0;
+  g.g2_items = (int64_t)g.col_tiles * g.rchunks;
+  g.grid2 = (int)(g.g2_items < sms ? (g.g2_items > 0 ? g.g2_items : 1) : sms);
+  g.g2_maxseg = sk_maxseg(g.g2_items, g.grid2, g.rchunks);
   return g;
 }
 
 Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K) {
   const int32_t P = padded(p);
-  const Geometry g = geometry(dtype, nrows, P);
+  const Geometry g = geometry(dtype, nrows, P, K);
   const size_t tb = dtype_bytes(dtype);
   Workspace w{};
   size_t off = 0;
@@ -334,35 +754,59 @@ Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K) {
     off = round_up(off + bytes, 256);
     return o;
   };
+  const int64_t nr = nrows > 0 ? nrows : 1;
+  // The counters sit at offset 0 with a size independent of nrows, so one
+  // zero-filled workspace serves calls of every row count (they stay zero at
+  // rest).
+  w.counters = take((size_t)kCounterWords * 4);
   w.weights = take((size_t)K * P * tb);
-  w.rowbuf = take((size_t)(nrows > 0 ? nrows : 1) * K * tb);
-  w.partial = take((size_t)g.splits * K * P * tb);
-  w.loss_part = take((size_t)(g.rowpass_blocks + 1) * 8);
-  w.corr_part = take((size_t)(g.rowpass_blocks + 1) * 8);
+  w.rowbuf = take((size_t)nr * u_stride(dtype, K) * tb);  // R / U rows, 16-B padded
+  w.zp = take((size_t)(g.row_blocks > 0 ? g.row_blocks : 1) * g.g1_maxseg * kRB * K * 8);
+  w.gp = take((size_t)g.col_tiles * g.g2_maxseg * K * g.tcol * 8);
+  w.loss_part = take((size_t)(g.row_blocks + 1) * 8);
+  w.corr_part = take((size_t)(g.row_blocks + 1) * 8);
   w.dot_part = take((size_t)4 * kDotBlocks * 8);
-  w.counters = take(16 * 4);
   w.total = off;
   return w;
 }
 
-template <typename T, int K>
-static void launch_rowpass(int mode, const RowArgs &a, int64_t blocks, cudaStream_t st) {
-  const dim3 grid((unsigned)blocks), block(kWarps * 32);
-  switch (mode) {
-    case kObjective: rowpass_kernel<T, K, kObjective, 4><<<grid, block, 0, st>>>(a); break;
-    case kGradient: rowpass_kernel<T, K, kGradient, 4><<<grid, block, 0, st>>>(a); break;
-    case kHessPrep: rowpass_kernel<T, K, kHessPrep, 4><<<grid, block, 0, st>>>(a); break;
-    default: rowpass_kernel<T, K, kHessApply, 4><<<grid, block, 0, st>>>(a); break;
+template <typename KernelT, typename ArgT>
+static int launch_persistent(KernelT kernel, int grid, size_t smem, size_t *configured,
+                             cudaStream_t st, const ArgT &args, const char *what) {
+  if (smem > *configured) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+      return check_launch(what);
+    *configured = smem;
   }
+  kernel<<<grid, kThreads, smem, st>>>(args);  // persistent: one CTA per SM
+  return check_launch(what);
 }
 
 template <typename T, int K>
-static void launch_xtu(const RowArgs &a, const Geometry &g, const void *U, void *partial,
-                       const double *skip, cudaStream_t st) {
-  const dim3 grid((unsigned)g.xtu_tiles, (unsigned)g.splits), block(128);
-  xtu_kernel<T, K><<<grid, block, 0, st>>>(static_cast<const T *>(a.X), a.ldx, a.rows,
-                                           a.nrows, a.P, static_cast<const T *>(U),
-                                           g.rows_per_split, static_cast<T *>(partial), skip);
+static int launch_gemm1(const G1Args &a, int grid, cudaStream_t st) {
+  static size_t configured = 0;
+  return launch_persistent(gemm1_kernel<T, K>, grid, G1Shape<T, K>::SMEM, &configured, st, a,
+                           "gemm1");
+}
+
+template <typename T, int K>
+static int launch_gemm2(const G2Args &a, int grid, cudaStream_t st) {
+  static size_t configured = 0;
+  return launch_persistent(gemm2_kernel<T, K>, grid, G2Shape<T, K>::SMEM, &configured, st, a,
+                           "gemm2");
+}
+
+template <typename T, int K>
+static int launch_epilogue(int mode, const E1Args &e, int64_t blocks, cudaStream_t st) {
+  const dim3 grid((unsigned)blocks), block(kEpiThreads);
+  switch (mode) {
+    case kObjective: g1_epilogue_kernel<T, K, kObjective><<<grid, block, 0, st>>>(e); break;
+    case kGradient: g1_epilogue_kernel<T, K, kGradient><<<grid, block, 0, st>>>(e); break;
+    case kHessPrep: g1_epilogue_kernel<T, K, kHessPrep><<<grid, block, 0, st>>>(e); break;
+    default: g1_epilogue_kernel<T, K, kHessApply><<<grid, block, 0, st>>>(e); break;
+  }
+  return check_launch("epilogue");
 }
 
 #define SNX_K_SWITCH(K, CALL)                         \
@@ -405,8 +849,18 @@ static int validate(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_
     set_error("snx: negative row count");
     return 1;
   }
-  if (nrows > 0 && X == nullptr) {
-    set_error("snx: X is NULL");
+  if (nrows > 0 && (X == nullptr || (reinterpret_cast<uintptr_t>(X) & 15) != 0)) {
+    set_error("snx: X must be a non-NULL 16-byte aligned device pointer");
+    return 1;
+  }
+  const Geometry g = geometry(dtype, nrows, padded(p), K);
+  if (g.row_blocks > kMaxRowBlocks || nrows > (int64_t)0x7fffffff) {
+    set_error("snx: %lld rows exceed one call's limit (%lld); shard the rows", (long long)nrows,
+              (long long)(kMaxRowBlocks * kRB));
+    return 1;
+  }
+  if (g.col_tiles > kMaxTiles) {
+    set_error("snx: p=%d too wide for this build (max %d column tiles)", p, kMaxTiles);
     return 1;
   }
   const Workspace w = workspace_layout(dtype, nrows, p, K);
@@ -417,16 +871,16 @@ static int validate(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_
   return 0;
 }
 
-// Common driver of the four row-pass entry points.
-static int rowpass(int mode, int dtype, const void *X, int64_t ldx, const int64_t *rows,
-                   int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
-                   const double *w, const double *dir, double alpha, const void *H,
-                   void *rowout, double scale, double lam, const double *base, double *out,
-                   long long *corr_out, double *vec_out, double *dots, const double *skip,
-                   void *ws, size_t ws_bytes, cudaStream_t st) {
+// Common driver of the row-pass entry points (rows contiguous).
+static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                   int32_t K, const int32_t *labels, const double *w, const double *dir,
+                   double alpha, const void *H, void *rowout, double scale, double lam,
+                   const double *base, double *out, long long *corr_out, double *vec_out,
+                   double *dots, const double *skip, void *ws, size_t ws_bytes,
+                   cudaStream_t st) {
   if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
   const int32_t P = padded(p);
-  const Geometry g = geometry(dtype, nrows, P);
+  const Geometry g = geometry(dtype, nrows, P, K);
   const Workspace lay = workspace_layout(dtype, nrows, p, K);
   char *wsb = static_cast<char *>(ws);
   unsigned *counters = reinterpret_cast<unsigned *>(wsb + lay.counters);
@@ -439,7 +893,7 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, const int64_
   const bool convert = dtype == SNX_F32 || dir != nullptr || P != p;
   if (convert || need_wsq) {
     void *dst = convert ? (void *)(wsb + lay.weights) : nullptr;
-    if (launch_prep_weights(dtype, w, dir, alpha, K, p, P, dst, dotp, counters + 1,
+    if (launch_prep_weights(dtype, w, dir, alpha, K, p, P, dst, dotp, counters + 15,
                             need_wsq ? out + 1 : nullptr, st))
       return 1;
     if (dst) Wt = dst;
@@ -452,63 +906,102 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, const int64_
       if (corr_out && cudaMemsetAsync(corr_out, 0, sizeof(long long), st) != cudaSuccess)
         return check_launch("memset");
     }
-    if (mode == kHessPrep) return 0;
     if (mode == kGradient || mode == kHessApply) {
-      // out = lam * base (scale * 0 + lam * base)
-      cudaMemsetAsync(wsb + lay.partial, 0, (size_t)K * P * dtype_bytes(dtype), st);
-      if (dtype == SNX_F64)
-        finalize_kernel<double><<<kDotBlocks, kDotThreads, 0, st>>>(
-            reinterpret_cast<const double *>(wsb + lay.partial), 1, K, p, P, scale, lam,
-            base, vec_out, dots, skip);
-      else
-        finalize_kernel<float><<<kDotBlocks, kDotThreads, 0, st>>>(
-            reinterpret_cast<const float *>(wsb + lay.partial), 1, K, p, P, scale, lam,
-            base, vec_out, dots, skip);
-      return check_launch("finalize");
+      lam_only_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(K, p, lam, base, vec_out, dots, skip);
+      return check_launch("lam_only");
     }
-    return check_launch("objective(empty)");
+    return 0;
   }
 
-  RowArgs a{};
-  a.X = X;
-  a.ldx = ldx;
-  a.rows = rows;
+  const size_t tb = dtype_bytes(dtype);
+  void *rowbuf = rowout ? rowout : (void *)(wsb + lay.rowbuf);
+  double *zp = reinterpret_cast<double *>(wsb + lay.zp);
+  G1Args a{};
+  if (make_map(&a.xmap, dtype, X, P, nrows, ldx, (uint32_t)(128 / tb), kRB, true)) return 1;
+  if (make_map(&a.wmap, dtype, Wt, P, K, P, (uint32_t)(512 / tb), K, false)) return 1;
   a.nrows = nrows;
-  a.P = P;
-  a.labels = labels;
-  a.W = Wt;
-  a.H = H;
-  a.rowout = rowout ? rowout : (void *)(wsb + lay.rowbuf);
-  a.loss_part = reinterpret_cast<double *>(wsb + lay.loss_part);
-  a.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
-  a.counter = counters;
-  a.loss_out = out;
-  a.corr_out = corr_out;
+  a.nchunks = g.nchunks;
+  a.maxseg = g.g1_maxseg;
+  a.items = g.g1_items;
+  a.zp = zp;
   a.skip = skip;
+  E1Args e{};
+  e.nrows = nrows;
+  e.nchunks = g.nchunks;
+  e.maxseg = g.g1_maxseg;
+  e.grid = g.grid1;
+  e.items = g.g1_items;
+  e.ustride = mode == kHessPrep ? K : u_stride(dtype, K);
+  e.zp = zp;
+  e.labels = labels;
+  e.H = H;
+  e.rowout = rowbuf;
+  e.loss_part = reinterpret_cast<double *>(wsb + lay.loss_part);
+  e.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
+  e.counter = counters + 2;
+  e.loss_out = out;
+  e.corr_out = corr_out;
+  e.skip = skip;
+  int rc = 1;
   if (dtype == SNX_F64) {
-    SNX_K_SWITCH(K, (launch_rowpass<double, KK>(mode, a, g.rowpass_blocks, st)));
+    SNX_K_SWITCH(K, (rc = launch_gemm1<double, KK>(a, g.grid1, st)));
+    if (rc) return rc;
+    SNX_K_SWITCH(K, (rc = launch_epilogue<double, KK>(mode, e, g.row_blocks, st)));
   } else {
-    SNX_K_SWITCH(K, (launch_rowpass<float, KK>(mode, a, g.rowpass_blocks, st)));
+    SNX_K_SWITCH(K, (rc = launch_gemm1<float, KK>(a, g.grid1, st)));
+    if (rc) return rc;
+    SNX_K_SWITCH(K, (rc = launch_epilogue<float, KK>(mode, e, g.row_blocks, st)));
   }
-  if (check_launch("rowpass")) return 1;
-  if (mode == kGradient || mode == kHessApply) {
-    void *partial = wsb + lay.partial;
-    if (dtype == SNX_F64) {
-      SNX_K_SWITCH(K, (launch_xtu<double, KK>(a, g, a.rowout, partial, skip, st)));
-      if (check_launch("xtu")) return 1;
-      finalize_kernel<double><<<kDotBlocks, kDotThreads, 0, st>>>(
-          static_cast<const double *>(partial), g.splits, K, p, P, scale, lam, base, vec_out,
-          dots, skip);
-    } else {
-      SNX_K_SWITCH(K, (launch_xtu<float, KK>(a, g, a.rowout, partial, skip, st)));
-      if (check_launch("xtu")) return 1;
-      finalize_kernel<float><<<kDotBlocks, kDotThreads, 0, st>>>(
-          static_cast<const float *>(partial), g.splits, K, p, P, scale, lam, base, vec_out,
-          dots, skip);
-    }
-    if (check_launch("finalize")) return 1;
+  if (rc) return rc;
+  if (mode != kGradient && mode != kHessApply) return 0;
+
+  G2Args b{};
+  if (make_map(&b.xmap, dtype, X, P, nrows, ldx, (uint32_t)g.tcol, kG2Rows, false)) return 1;
+  b.nrows = nrows;
+  b.rchunks = g.rchunks;
+  b.maxseg = g.g2_maxseg;
+  b.items = g.g2_items;
+  b.U = rowbuf;
+  b.gp = reinterpret_cast<double *>(wsb + lay.gp);
+  b.skip = skip;
+  if (dtype == SNX_F64) {
+    SNX_K_SWITCH(K, (rc = launch_gemm2<double, KK>(b, g.grid2, st)));
+  } else {
+    SNX_K_SWITCH(K, (rc = launch_gemm2<float, KK>(b, g.grid2, st)));
   }
-  return 0;
+  if (rc) return rc;
+  finalize_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(b.gp, g.g2_items, g.grid2, g.rchunks,
+                                                      g.g2_maxseg, g.tcol, K, p, scale, lam,
+                                                      base, vec_out, dots, skip);
+  return check_launch("finalize");
+}
+
+static int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels,
+                  const int64_t *rows, int64_t nrows, void *dst, int64_t ldd,
+                  int32_t *labels_out, cudaStream_t st) {
+  if (nrows == 0) return 0;
+  if (X == nullptr || rows == nullptr || dst == nullptr || ldd > ldx || ldd % 4 != 0 ||
+      ldx % 4 != 0) {
+    set_error("snx_gather_rows: bad arguments (NULL pointer or ld_out > ldx / not %% 4)");
+    return 1;
+  }
+  if (labels_out != nullptr && labels == nullptr) {
+    set_error("snx_gather_rows: labels_out without labels");
+    return 1;
+  }
+  const int64_t blocks64 = (nrows + 7) / 8;
+  const int blocks = (int)(blocks64 < 8 * sm_count() ? blocks64 : 8 * sm_count());
+  if (dtype == SNX_F64)
+    gather_rows_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double *>(X), ldx,
+                                                        labels, rows, nrows,
+                                                        static_cast<double *>(dst), ldd,
+                                                        labels_out);
+  else
+    gather_rows_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float *>(X), ldx,
+                                                       labels, rows, nrows,
+                                                       static_cast<float *>(dst), ldd,
+                                                       labels_out);
+  return check_launch("gather_rows");
 }
 
 }  // namespace snx
@@ -521,55 +1014,71 @@ size_t snx_workspace_bytes(int dtype, int64_t nrows, int32_t p, int32_t K) {
   return workspace_layout(dtype, nrows, p, K).total;
 }
 
-int snx_objective(int dtype, const void *X, int64_t ldx, const int64_t *rows, int64_t nrows,
-                  int32_t p, int32_t K, const int32_t *labels, const double *w,
-                  const double *dir, double alpha, double *out, int64_t *correct_out,
-                  void *ws, size_t ws_bytes, void *stream) {
+int snx_gather_rows(int dtype, const void *X, int64_t ldx, const int32_t *labels,
+                    const int64_t *rows, int64_t nrows, void *X_out, int64_t ld_out,
+                    int32_t *labels_out, void *stream) {
+  if (dtype != SNX_F64 && dtype != SNX_F32) {
+    set_error("snx_gather_rows: unknown dtype %d", dtype);
+    return 1;
+  }
+  return gather(dtype, X, ldx, labels, rows, nrows, X_out, ld_out, labels_out,
+                (cudaStream_t)stream);
+}
+
+int snx_objective(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
+                  const int32_t *labels, const double *w, const double *dir, double alpha,
+                  double *out, int64_t *correct_out, void *ws, size_t ws_bytes, void *stream) {
   if (out == nullptr || w == nullptr || (nrows > 0 && labels == nullptr)) {
     set_error("snx_objective: NULL out/w/labels");
     return 1;
   }
-  return rowpass(kObjective, dtype, X, ldx, rows, nrows, p, K, labels, w, dir, alpha, nullptr,
+  return rowpass(kObjective, dtype, X, ldx, nrows, p, K, labels, w, dir, alpha, nullptr,
                  nullptr, 1.0, 0.0, nullptr, out, reinterpret_cast<long long *>(correct_out),
                  nullptr, nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
-int snx_objective_grad(int dtype, const void *X, int64_t ldx, const int64_t *rows,
-                       int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
-                       const double *w, double scale, double lam, double *out, double *G_out,
-                       void *ws, size_t ws_bytes, void *stream) {
+int snx_objective_grad(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                       int32_t K, const int32_t *labels, const double *w, double scale,
+                       double lam, double *out, double *G_out, void *ws, size_t ws_bytes,
+                       void *stream) {
   if (out == nullptr || w == nullptr || G_out == nullptr || (nrows > 0 && labels == nullptr)) {
     set_error("snx_objective_grad: NULL out/w/G_out/labels");
     return 1;
   }
-  return rowpass(kGradient, dtype, X, ldx, rows, nrows, p, K, labels, w, nullptr, 0.0, nullptr,
+  return rowpass(kGradient, dtype, X, ldx, nrows, p, K, labels, w, nullptr, 0.0, nullptr,
                  nullptr, scale, lam, w, out, nullptr, G_out, nullptr, nullptr, ws, ws_bytes,
                  (cudaStream_t)stream);
 }
 
-int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
-                     int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
-                     const double *w, void *H_out, void *ws, size_t ws_bytes, void *stream) {
-  (void)labels;  // h does not depend on the labels (softmax.py:189-195)
+int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+                     int32_t p, int32_t K, const double *w, void *Xs_out, int64_t ld_out,
+                     void *H_out, void *ws, size_t ws_bytes, void *stream) {
   if (w == nullptr || (nrows > 0 && H_out == nullptr)) {
     set_error("snx_hess_prepare: NULL w/H_out");
     return 1;
   }
-  return rowpass(kHessPrep, dtype, X, ldx, rows, nrows, p, K, nullptr, w, nullptr, 0.0,
-                 nullptr, H_out, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr,
-                 nullptr, ws, ws_bytes, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const void *Xs = X;
+  int64_t lds = ldx;
+  if (rows != nullptr) {  // materialise X_S = X[rows] (dataset.py:90-97)
+    if (gather(dtype, X, ldx, nullptr, rows, nrows, Xs_out, ld_out, nullptr, st)) return 1;
+    Xs = Xs_out;
+    lds = ld_out;
+  }
+  return rowpass(kHessPrep, dtype, Xs, lds, nrows, p, K, nullptr, w, nullptr, 0.0, nullptr,
+                 H_out, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ws,
+                 ws_bytes, st);
 }
 
-int snx_hess_apply(int dtype, const void *X, int64_t ldx, const int64_t *rows, int64_t nrows,
-                   int32_t p, int32_t K, const void *H, const double *v, double scale,
-                   double lam, double *Hv_out, double *dots, const double *skip, void *ws,
-                   size_t ws_bytes, void *stream) {
+int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
+                   const void *H, const double *v, double scale, double lam, double *Hv_out,
+                   double *dots, const double *skip, void *ws, size_t ws_bytes, void *stream) {
   if (v == nullptr || Hv_out == nullptr || (nrows > 0 && H == nullptr)) {
     set_error("snx_hess_apply: NULL v/Hv_out/H");
     return 1;
   }
-  return rowpass(kHessApply, dtype, X, ldx, rows, nrows, p, K, nullptr, v, nullptr, 0.0, H,
-                 nullptr, scale, lam, v, nullptr, nullptr, Hv_out, dots, skip, ws, ws_bytes,
+  return rowpass(kHessApply, dtype, Xs, ldx, nrows, p, K, nullptr, v, nullptr, 0.0, H, nullptr,
+                 scale, lam, v, nullptr, nullptr, Hv_out, dots, skip, ws, ws_bytes,
                  (cudaStream_t)stream);
 }
 

@@ -117,6 +117,9 @@ class DeviceDataset:
     def base(self):
         return self
 
+    def materialized(self):
+        return self
+
     # ------------------------------------------------------------ views
     def take(self, indices):
         """Row gather (dataset.py:90-97, 180-185); identity returns self."""
@@ -133,6 +136,9 @@ class DeviceDataset:
 
     # ------------------------------------------------------------ workspace
     def workspace(self, nrows):
+        owner = getattr(self, "_ws_owner", None)
+        if owner is not None:  # a materialised view shares its parent's workspace
+            return owner.workspace(nrows)
         need = _lib.workspace_bytes(self.code, nrows, self.n_features, self.K)
         if self._ws is None or self._ws.numel() < need:
             floor = _lib.workspace_bytes(self.code, self.n_rows, self.n_features, self.K)
@@ -141,12 +147,29 @@ class DeviceDataset:
 
 
 class DeviceView:
-    """Rows `rows` (sorted int64 device indices) of a DeviceDataset."""
+    """Rows `rows` (sorted int64 device indices) of a DeviceDataset.
+
+    Kernels stream contiguous rows (TMA tiles), so a view used by a full pass
+    is materialised once (snx_gather_rows) and cached; the Hessian operator
+    gathers its sample itself (snx_hess_prepare)."""
 
     def __init__(self, base, rows, n_rows):
         self.base = base
         self.rows = rows
         self._n = int(n_rows)
+        self._dense = None
+
+    def materialized(self):
+        if self._dense is None:
+            b = self.base
+            X = torch.empty((self._n, b.ld), dtype=b.X.dtype, device=b.X.device)
+            lab = torch.empty(self._n, dtype=torch.int32, device=b.X.device)
+            _lib.call("snx_gather_rows", b.code, ptr(b.X), b.ld, ptr(b.labels), ptr(self.rows),
+                      self._n, ptr(X), b.ld, ptr(lab), stream_handle())
+            self._dense = DeviceDataset(X, lab, b.n_classes, b.n_features, b.dtype)
+            self._dense._ws = b._ws
+            self._dense._ws_owner = b
+        return self._dense
 
     n_features = property(lambda self: self.base.n_features)
     n_classes = property(lambda self: self.base.n_classes)

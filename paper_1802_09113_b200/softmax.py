@@ -63,10 +63,9 @@ def _view(ds):
     return as_device(ds)
 
 
-def _args(view):
-    """Common leading ABI arguments for a dataset or a row view."""
-    return (view.code, ptr(view.X), view.ld, ptr(view.rows), view.n_rows, view.n_features,
-            view.K)
+def _args(ds):
+    """Common leading ABI arguments for a contiguous (materialised) dataset."""
+    return (ds.code, ptr(ds.X), ds.ld, ds.n_rows, ds.n_features, ds.K)
 
 
 def _ws(view):
@@ -76,6 +75,7 @@ def _ws(view):
 
 def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
     """Device [data loss, ||w_eff||^2] (+ correct count) at w_eff = w + alpha*direction."""
+    view = view.materialized()
     out = torch.empty(2, dtype=torch.float64, device=w.device)
     corr = torch.empty(1, dtype=torch.int64, device=w.device) if want_correct else None
     _lib.call("snx_objective", *_args(view), ptr(view.labels), ptr(w), ptr(direction),
@@ -85,6 +85,7 @@ def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
 
 def gradient_parts(view, w, scale, lam):
     """Device (G = scale * data_gradient + lam * w, [data loss, ||w||^2])."""
+    view = view.materialized()
     out = torch.empty(2, dtype=torch.float64, device=w.device)
     G = torch.empty_like(w)
     _lib.call("snx_objective_grad", *_args(view), ptr(view.labels), ptr(w), float(scale),
@@ -145,14 +146,23 @@ class HessianOperator:
         self.p, self.C = view.n_features, view.n_classes
         self.dim = view.dim
         tdtype = view.X.dtype
-        self._h = torch.empty((max(view.n_rows, 1), view.K), dtype=tdtype, device=w.device)
-        _lib.call("snx_hess_prepare", *_args(view), ptr(view.labels), ptr(w), ptr(self._h),
+        m = view.n_rows
+        self._h = torch.empty((max(m, 1), view.K), dtype=tdtype, device=w.device)
+        base = view.base
+        if view.rows is not None:  # gather the sample once (dataset.py:90-97)
+            self._xs = torch.empty((max(m, 1), base.ld), dtype=tdtype, device=w.device)
+        else:
+            self._xs = base.X
+        _lib.call("snx_hess_prepare", base.code, ptr(base.X), base.ld, ptr(view.rows), m,
+                  view.n_features, view.K, ptr(w), ptr(self._xs), base.ld, ptr(self._h),
                   *_ws(view), stream_handle())
 
     def apply_into(self, v, out, dots=None, skip=None):
         """Device-only apply: out = H v; optional CG dot partials and skip flag."""
-        _lib.call("snx_hess_apply", *_args(self.view), ptr(self._h), ptr(v), self.scale,
-                  self.lam, ptr(out), ptr(dots), skip, *_ws(self.view), stream_handle())
+        base = self.view.base
+        _lib.call("snx_hess_apply", base.code, ptr(self._xs), base.ld, self.view.n_rows,
+                  self.p, self.view.K, ptr(self._h), ptr(v), self.scale, self.lam, ptr(out),
+                  ptr(dots), skip, *_ws(self.view), stream_handle())
         return out
 
     def apply(self, v):

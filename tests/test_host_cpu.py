@@ -52,11 +52,11 @@ def test_abi_version_and_workspace(lib):
 
 def test_abi_errors_without_device(lib):
     # argument validation fails before any launch
-    rc = lib.snx_objective(7, None, 4, None, 0, 4, 3, None, None, None, 0.0, None, None,
-                           None, 0, None)
+    rc = lib.snx_objective(7, None, 4, 0, 4, 3, None, None, None, 0.0, None, None, None, 0,
+                           None)
     assert rc != 0
-    rc = lib.snx_hess_apply(0, None, 4, None, 10, 4, 40, ctypes.c_void_p(8), ctypes.c_void_p(8), 1.0, 0.0,
-                            ctypes.c_void_p(8), None, None, None, 0, None)
+    rc = lib.snx_hess_apply(0, None, 4, 10, 4, 40, ctypes.c_void_p(8), ctypes.c_void_p(8), 1.0,
+                            0.0, ctypes.c_void_p(8), None, None, None, 0, None)
     assert rc != 0 and b"K = C-1" in lib.snx_last_error()
 
 
