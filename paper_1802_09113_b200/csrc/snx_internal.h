@@ -49,6 +49,15 @@ struct Workspace {
 Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K);
 inline int32_t padded(int32_t p) { return (p + 3) / 4 * 4; }
 
+// Ask for the maximum shared-memory carveout once per kernel: every libsnx
+// kernel then runs in the same L1/smem configuration as the persistent TMA
+// kernels, so consecutive launches never pay an SM reconfiguration.
+void prefer_max_smem(const void *kernel);
+template <typename F>
+inline void carveout(F *kernel) {
+  prefer_max_smem(reinterpret_cast<const void *>(kernel));
+}
+
 // vector kernels (snx_vec.cu)
 int launch_prep_weights(int dtype, const double *w, const double *dir, double alpha, int K,
                         int p, int P, void *Wt, double *wsq_partials, unsigned *counter,

@@ -779,6 +779,7 @@ static int launch_persistent(KernelT kernel, int grid, size_t smem, size_t *conf
       return check_launch(what);
     *configured = smem;
   }
+  carveout(kernel);
   kernel<<<grid, kThreads, smem, st>>>(args);  // persistent: one CTA per SM
   return check_launch(what);
 }
@@ -991,16 +992,17 @@ static int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels,
   }
   const int64_t blocks64 = (nrows + 7) / 8;
   const int blocks = (int)(blocks64 < 8 * sm_count() ? blocks64 : 8 * sm_count());
-  if (dtype == SNX_F64)
+  if (dtype == SNX_F64) {
     gather_rows_kernel<double><<<blocks, 256, 0, st>>>(static_cast<const double *>(X), ldx,
                                                         labels, rows, nrows,
                                                         static_cast<double *>(dst), ldd,
                                                         labels_out);
-  else
+  } else {
     gather_rows_kernel<float><<<blocks, 256, 0, st>>>(static_cast<const float *>(X), ldx,
                                                        labels, rows, nrows,
                                                        static_cast<float *>(dst), ldd,
                                                        labels_out);
+  }
   return check_launch("gather_rows");
 }
 

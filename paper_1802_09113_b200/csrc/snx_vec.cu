@@ -18,6 +18,17 @@ void set_error(const char *fmt, ...) {
   va_end(ap);
 }
 
+void prefer_max_smem(const void *kernel) {
+  static const void *seen[256];
+  static int nseen = 0;
+  for (int i = 0; i < nseen; ++i)
+    if (seen[i] == kernel) return;
+  cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       cudaSharedmemCarveoutMaxShared);
+  cudaGetLastError();  // the preference is advisory
+  if (nseen < 256) seen[nseen++] = kernel;
+}
+
 int check_launch(const char *what) {
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
@@ -78,12 +89,13 @@ __global__ void __launch_bounds__(kDotThreads)
 int launch_prep_weights(int dtype, const double *w, const double *dir, double alpha, int K,
                         int p, int P, void *Wt, double *part, unsigned *counter,
                         double *wsq_out, cudaStream_t st) {
-  if (dtype == SNX_F64)
+  if (dtype == SNX_F64) {
     prep_weights_kernel<double><<<kDotBlocks, kDotThreads, 0, st>>>(
         w, dir, alpha, K, p, P, static_cast<double *>(Wt), part, counter, wsq_out);
-  else
+  } else {
     prep_weights_kernel<float><<<kDotBlocks, kDotThreads, 0, st>>>(
         w, dir, alpha, K, p, P, static_cast<float *>(Wt), part, counter, wsq_out);
+  }
   return check_launch("prep_weights");
 }
 
@@ -340,12 +352,13 @@ int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *
   if (nrows == 0) return 0;
   cudaStream_t st = (cudaStream_t)stream;
   const int blocks = 148 * 8;
-  if (dtype == SNX_F64)
+  if (dtype == SNX_F64) {
     pack_rows_kernel<double><<<blocks, 256, 0, st>>>(src, nrows, p, static_cast<double *>(dst),
                                                      ldd);
-  else
+  } else {
     pack_rows_kernel<float><<<blocks, 256, 0, st>>>(src, nrows, p, static_cast<float *>(dst),
                                                     ldd);
+  }
   return check_launch("pack_rows");
 }
 

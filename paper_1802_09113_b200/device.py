@@ -60,6 +60,7 @@ class DeviceDataset:
         self.code = DTYPES[dtype][0]
         self.ld = int(X.shape[1])
         self._ws = None
+        self._hess = {}   # m -> HessBuffers (sample buffers shared by operators)
         self.rows = None  # a dataset is its own identity view
 
     # ------------------------------------------------------------ construction
@@ -134,6 +135,14 @@ class DeviceDataset:
     def slice_rows(self, i0, i1):
         return self.take(np.arange(i0, i1))
 
+    def hess_buffers(self, m, gathered):
+        """Persistent sample buffers (X_S, h) for Hessian operators of m rows."""
+        key = (m, gathered)
+        hb = self._hess.get(key)
+        if hb is None:
+            hb = self._hess[key] = HessBuffers(self, m, gathered)
+        return hb
+
     # ------------------------------------------------------------ workspace
     def workspace(self, nrows):
         owner = getattr(self, "_ws_owner", None)
@@ -144,6 +153,24 @@ class DeviceDataset:
             floor = _lib.workspace_bytes(self.code, self.n_rows, self.n_features, self.K)
             self._ws = torch.zeros(max(need, floor), dtype=torch.uint8, device=self.X.device)
         return self._ws
+
+
+class HessBuffers:
+    """HBM buffers of one sampled Hessian (X_S rows and h probabilities).
+
+    Operators of the same dataset and sample size share them, so every outer
+    iteration reuses the same addresses and the captured CUDA graph of the CG
+    loop (cg.CgGraph) stays valid.  `owner` is the operator whose sample is
+    currently materialised; any other operator re-prepares before use."""
+
+    def __init__(self, base, m, gathered):
+        dev = base.X.device
+        mm = max(m, 1)
+        self.xs = torch.empty((mm, base.ld), dtype=base.X.dtype, device=dev) if gathered \
+            else base.X
+        self.h = torch.empty((mm, base.K), dtype=base.X.dtype, device=dev)
+        self.owner = None
+        self.graphs = {}
 
 
 class DeviceView:

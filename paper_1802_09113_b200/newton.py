@@ -24,7 +24,7 @@ import numpy as np
 import torch
 
 from . import softmax
-from .cg import CgConfig, CgWorkspace, cg_solve, enqueue_cg, report_from
+from .cg import CgConfig, cg_graph_for, cg_solve, report_from
 from .device import as_device, axpy, cuda_device, dot, vec_in, vec_out
 from .errors import DataError, LineSearchError
 from .linesearch import LineSearchConfig, line_search
@@ -147,7 +147,6 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     test = as_device(test_set) if test_set is not None else None
     dev_prob = softmax.SoftmaxProblem(ds, prob.lam)
     lam = prob.lam
-    cgws = CgWorkspace(d, cfg.cg.max_iters, cuda_device())
 
     def test_acc(w):
         return (float(softmax.correct_count(test, w)) / test.n_rows) if test is not None \
@@ -166,7 +165,7 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
             reason = "gradient-converged"
             break
         hess = oracle.hessian_operator(x)
-        enqueue_cg(hess, g, cfg.cg.theta, cfg.cg.max_iters, cgws)
+        cgws = cg_graph_for(hess, cfg.cg.max_iters, cfg.cg.theta).run(g)
         report = report_from(cgws, cfg.cg.max_iters, True)
         p = report.solution
         slope = float(dot(p, g))

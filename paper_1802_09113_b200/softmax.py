@@ -145,24 +145,32 @@ class HessianOperator:
         self.block_rows = block_rows
         self.p, self.C = view.n_features, view.n_classes
         self.dim = view.dim
-        tdtype = view.X.dtype
-        m = view.n_rows
-        self._h = torch.empty((max(m, 1), view.K), dtype=tdtype, device=w.device)
-        base = view.base
-        if view.rows is not None:  # gather the sample once (dataset.py:90-97)
-            self._xs = torch.empty((max(m, 1), base.ld), dtype=tdtype, device=w.device)
-        else:
-            self._xs = base.X
-        _lib.call("snx_hess_prepare", base.code, ptr(base.X), base.ld, ptr(view.rows), m,
-                  view.n_features, view.K, ptr(w), ptr(self._xs), base.ld, ptr(self._h),
-                  *_ws(view), stream_handle())
+        self._w = w.clone()
+        self._bufs = view.base.hess_buffers(view.n_rows, view.rows is not None)
+        self._prepare()
+
+    def _prepare(self):
+        """Materialise this operator's sample and probabilities in the shared buffers."""
+        view, base, hb = self.view, self.view.base, self._bufs
+        _lib.call("snx_hess_prepare", base.code, ptr(base.X), base.ld, ptr(view.rows),
+                  view.n_rows, view.n_features, view.K, ptr(self._w), ptr(hb.xs), base.ld,
+                  ptr(hb.h), *_ws(view), stream_handle())
+        hb.owner = self
+
+    @property
+    def _h(self):
+        if self._bufs.owner is not self:
+            self._prepare()
+        return self._bufs.h
 
     def apply_into(self, v, out, dots=None, skip=None):
         """Device-only apply: out = H v; optional CG dot partials and skip flag."""
-        base = self.view.base
-        _lib.call("snx_hess_apply", base.code, ptr(self._xs), base.ld, self.view.n_rows,
-                  self.p, self.view.K, ptr(self._h), ptr(v), self.scale, self.lam, ptr(out),
-                  ptr(dots), skip, *_ws(self.view), stream_handle())
+        if self._bufs.owner is not self:
+            self._prepare()
+        base, hb = self.view.base, self._bufs
+        _lib.call("snx_hess_apply", base.code, ptr(hb.xs), base.ld, self.view.n_rows, self.p,
+                  self.view.K, ptr(hb.h), ptr(v), self.scale, self.lam, ptr(out), ptr(dots),
+                  skip, *_ws(self.view), stream_handle())
         return out
 
     def apply(self, v):

@@ -43,3 +43,20 @@ for _ in range(5):
 e1.record(st)
 torch.cuda.synchronize()
 print(f"{dtype} full objective+acc {e0.elapsed_time(e1) / 5 * 1e3:.1f} us")
+from paper_1802_09113_b200 import cg as cgmod  # noqa: E402
+for _ in range(3):
+    ws = cgmod.cg_graph_for(op, 10, 1e-4).run(g)
+torch.cuda.synchronize()
+e0.record(st)
+for _ in range(10):
+    ws = cgmod.cg_graph_for(op, 10, 1e-4).run(g)
+e1.record(st)
+torch.cuda.synchronize()
+print(f"{dtype} cg_solve (10 Hv) {e0.elapsed_time(e1) / 10 * 1e3:.1f} us, iters {ws.slot(10)[3].item()}")
+e0.record(st)
+for k in range(5):
+    o2 = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, 0.05), 100 + k)
+    o2.hessian_operator(x)
+e1.record(st)
+torch.cuda.synchronize()
+print(f"{dtype} oracle+hess_prepare {e0.elapsed_time(e1) / 5 * 1e3:.1f} us (incl. host draw)")
