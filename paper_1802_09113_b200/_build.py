@@ -60,5 +60,14 @@ def build(force=False, verbose=False):
     return LIBPATH
 
 
+def build_timeline(out):
+    """Debug variant with per-CTA globaltimer stamps (tools/timeline.py)."""
+    cmd = [_nvcc(), *ARCH, *FLAGS, "-DSNX_TIMELINE", "-I", INCLUDE, *sources(), "-o", out]
+    proc = subprocess.run(cmd, capture_output=True, text=True)
+    if proc.returncode != 0:
+        raise RuntimeError(proc.stderr)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force=True, verbose=True))

@@ -57,11 +57,12 @@ def load():
     global _lib
     if _lib is not None:
         return _lib
-    if not os.path.exists(LIBPATH):
+    path = os.environ.get("SNX_LIB", LIBPATH)  # debug builds (tools/timeline.py)
+    if not os.path.exists(path):
         raise ImportError(
             f"libsnx CUDA extension not built ({LIBPATH} missing): run "
             "`python -c 'import __graft_entry__ as g; g.build()'` -- there is no CPU fallback")
-    lib = ctypes.CDLL(LIBPATH)
+    lib = ctypes.CDLL(path)
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(lib, name)
         fn.restype = res

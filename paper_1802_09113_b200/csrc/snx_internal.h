@@ -64,3 +64,27 @@ int launch_prep_weights(int dtype, const double *w, const double *dir, double al
                         double *wsq_out, cudaStream_t st);
 
 }  // namespace snx
+
+namespace snx {
+
+// PDL is opt-in (SNX_PDL=1); see pdl_enabled() in snx_vec.cu.
+bool pdl_enabled();
+
+// Launch with programmatic stream serialization (PDL); see snx_pipe.cuh.
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
+}  // namespace snx

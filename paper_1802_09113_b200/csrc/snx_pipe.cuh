@@ -58,6 +58,16 @@ __device__ __forceinline__ void consumer_sync(unsigned n) {
 
 __device__ __forceinline__ double ldcg(const double *p) { return __ldcg(p); }
 
+// gpu-scope atomic add with acquire-release semantics: publishes this CTA's
+// prior global writes (ordered before it by a CTA barrier) and, for the last
+// arriver, makes the other CTAs' writes visible -- one instruction instead of
+// fence + atomic + fence.
+__device__ __forceinline__ unsigned atomic_add_acq_rel(unsigned *p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 }  // namespace snx
 
 namespace snx {
@@ -76,5 +86,19 @@ __device__ __forceinline__ void tma_load_2d(void *dst, const void *tmap, int c0,
 __device__ __forceinline__ void tma_prefetch_desc(const void *tmap) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(tmap) : "memory");
 }
+
+}  // namespace snx
+
+namespace snx {
+
+// Programmatic dependent launch (PDL): every libsnx kernel lets its stream
+// successor launch as soon as all of its CTAs are resident (trigger at entry
+// is deadlock-free: the successor only launches once every CTA of this grid
+// has started), and waits for its predecessor's completion + memory before
+// touching any global data the predecessor may write or read.
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 
 }  // namespace snx

@@ -46,7 +46,6 @@ constexpr int kWarps = 8;                    // consumer warps
 constexpr int kConsumers = kWarps * 32;      // consumer threads
 constexpr int kThreads = kConsumers + 32;    // + one producer warp
 constexpr int kRB = 96;                      // rows per GEMM1 item (3 per lane)
-constexpr int kEpiThreads = 4 * kRB;         // epilogue: 4 threads per row
 constexpr int kG2Rows = 32;                  // rows per GEMM2 item
 constexpr int kMaxTiles = kDotBlocks;
 constexpr size_t kSmemBudget = 220 * 1024;
@@ -54,6 +53,22 @@ constexpr int64_t kMaxRowBlocks = 1 << 17;   // 12.5M rows per call
 constexpr int kCounterWords = 16 + kMaxTiles + kMaxRowBlocks;
 
 __host__ __device__ constexpr size_t cround(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+// Optional per-CTA timeline (compile with -DSNX_TIMELINE; tools/timeline.py):
+// globaltimer stamps at kernel entry, first data ready, last item done, exit.
+#ifdef SNX_TIMELINE
+__device__ unsigned long long g_timeline[3][160][4];
+#define SNX_TL(slot, ev)                                                   \
+  do {                                                                     \
+    unsigned long long t_;                                                 \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+    if (blockIdx.x < 160) g_timeline[slot][blockIdx.x][ev] = t_;          \
+  } while (0)
+#else
+#define SNX_TL(slot, ev) \
+  do {                   \
+  } while (0)
+#endif
 
 // GEMM1 shape: an item is (96-row block) x (512 B of columns).  X arrives as
 // four 96-row x 128-B boxes with the 128-B swizzle; warp w owns the 64-B strip
@@ -127,6 +142,36 @@ __device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v
   return t;
 }
 
+// fixed-order sums over the 256 consumer threads (named barrier 1; the
+// producer warp never joins); valid in consumer thread 0
+__device__ __forceinline__ double consumer_sum(double v, double *sh) {
+  v = warp_allsum(v);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  consumer_sync(kConsumers);
+  double t = 0.0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) t += sh[i];
+  }
+  consumer_sync(kConsumers);
+  return t;
+}
+
+__device__ __forceinline__ unsigned long long consumer_sum_u64(unsigned long long v,
+                                                               unsigned long long *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  consumer_sync(kConsumers);
+  unsigned long long t = 0;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) t += sh[i];
+  }
+  consumer_sync(kConsumers);
+  return t;
+}
+
 // Stream-K split of `items` over `G` CTAs: CTA c owns [T*c/G, T*(c+1)/G).
 __host__ __device__ __forceinline__ int64_t sk_begin(int64_t T, int G, int c) {
   return T * c / G;
@@ -143,12 +188,164 @@ struct G1Args {
   int nchunks;     // CHUNK-column chunks per row (ceil(P / CHUNK))
   int maxseg;      // max CTA segments per row block
   int64_t items;   // row_blocks * nchunks, split evenly over the CTAs
+  int64_t row_blocks;
+  int mode;        // Mode: which row epilogue the last segment of a row block runs
+  int ustride;     // row stride of rowout (K for h, padded KP for R / U)
   double *zp;      // [row_blocks][maxseg][kRB][K] segment partial logits
+  unsigned *rb_count;  // [row_blocks] segment arrivals (zero at rest)
+  unsigned *done_rb;   // finished row blocks (zero at rest)
+  const int32_t *labels;
+  const void *H;       // kHessApply: nrows*K probabilities
+  void *rowout;        // R (gradient), h (prep), U (apply)
+  double *loss_part;   // [row_blocks]
+  unsigned long long *corr_part;
+  double *loss_out;
+  long long *corr_out;
   const double *skip;
 };
 
+// Per-row softmax algebra on the summed logits z (softmax.py:85-99 and the
+// mode-specific lines); returns the row loss / correct flag.
+template <typename T, int K>
+__device__ __forceinline__ void row_epilogue(const G1Args &a, int64_t r, const double (&z)[K],
+                                             double &loss, unsigned long long &corr) {
+  if (a.mode == kHessApply) {
+    // softmax.py:206-208: VW = V*W; U = VW - W*rowsum(VW)
+    const T *h = static_cast<const T *>(a.H) + r * K;
+    double hw[K], vw[K], s = 0.0;
+#pragma unroll
+    for (int c = 0; c < K; ++c) {
+      hw[c] = (double)h[c];
+      vw[c] = z[c] * hw[c];
+      s += vw[c];
+    }
+    T *u = static_cast<T *>(a.rowout) + r * a.ustride;
+#pragma unroll
+    for (int c = 0; c < K; ++c) u[c] = (T)(vw[c] - hw[c] * s);
+    return;
+  }
+  // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
+  double M = 0.0;
+#pragma unroll
+  for (int c = 0; c < K; ++c) M = (z[c] > M || isnan(z[c])) ? z[c] : M;  // NaN propagates
+  double E[K], se = 0.0;
+#pragma unroll
+  for (int c = 0; c < K; ++c) {
+    E[c] = exp(z[c] - M);
+    se += E[c];
+  }
+  const double alpha = exp(-M) + se;
+  if (a.mode == kHessPrep) {
+    T *h = static_cast<T *>(a.rowout) + r * a.ustride;
+#pragma unroll
+    for (int c = 0; c < K; ++c) h[c] = (T)(E[c] / alpha);
+    return;
+  }
+  const int y = a.labels[r];
+  double lin = 0.0;
+#pragma unroll
+  for (int c = 0; c < K; ++c)
+    if (c == y) lin = z[c];
+  loss = (M + log(alpha)) - lin;  // softmax.py:134
+  if (a.mode == kGradient) {
+    T *R = static_cast<T *>(a.rowout) + r * a.ustride;
+#pragma unroll
+    for (int c = 0; c < K; ++c) R[c] = (T)(E[c] / alpha - (c == y ? 1.0 : 0.0));
+  } else if (a.corr_out != nullptr) {
+    // softmax.py:224-240: argmax over [E/alpha, e^-M/alpha], first max wins
+    int best = 0;
+    double bv = E[0] / alpha;
+    bool nan_hit = isnan(bv);
+#pragma unroll
+    for (int c = 1; c <= K; ++c) {
+      const double pc = (c < K ? E[c] : exp(-M)) / alpha;
+      if (!nan_hit && (isnan(pc) || pc > bv)) {
+        best = c;
+        bv = pc;
+        nan_hit = isnan(pc);
+      }
+    }
+    corr = (best == y) ? 1ull : 0ull;
+  }
+}
+
+// Epilogue of row block rb by the CTA that delivered its last segment: 2
+// consumer threads per row sum the CTA segments (fixed order), then the row
+// algebra; loss / correct counts reduce per row block and, by the CTA that
+// finishes the last row block, over all row blocks (fixed order).
+template <typename T, int K>
+__device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, double *zsum,
+                                            double *shd, unsigned long long *shu, int *flag) {
+  const int tid = threadIdx.x;
+  const int nrows = (int)min((int64_t)kRB, a.nrows - rb * kRB);
+  // 1) segment sums: element e = row*K + c, all segment loads independent and
+  //    coalesced, summed in segment order
+  {
+    const int c_lo = sk_owner(a.items, G, rb * a.nchunks);
+    const int nseg = sk_owner(a.items, G, (rb + 1) * a.nchunks - 1) - c_lo + 1;
+    const double *zb = a.zp + rb * a.maxseg * (int64_t)kRB * K;
+    constexpr int kPer = (kRB * K + kConsumers - 1) / kConsumers;
+    double acc[kPer];
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) acc[q] = 0.0;
+    for (int sg = 0; sg < nseg; sg += 2) {
+      double v0[kPer], v1[kPer];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * kConsumers;
+        const bool ok = e < nrows * K;
+        v0[q] = ok ? __ldcg(zb + (int64_t)sg * kRB * K + e) : 0.0;
+        v1[q] = (ok && sg + 1 < nseg) ? __ldcg(zb + (int64_t)(sg + 1) * kRB * K + e) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) acc[q] = (acc[q] + v0[q]) + v1[q];
+    }
+#pragma unroll
+    for (int q = 0; q < kPer; ++q) {
+      const int e = tid + q * kConsumers;
+      if (e < kRB * K) zsum[e] = acc[q];
+    }
+  }
+  consumer_sync(kConsumers);
+  // 2) row algebra, one thread per row
+  double loss = 0.0;
+  unsigned long long corr = 0;
+  if (tid < nrows) {
+    double z[K];
+#pragma unroll
+    for (int c = 0; c < K; ++c) z[c] = zsum[tid * K + c];
+    row_epilogue<T, K>(a, rb * kRB + tid, z, loss, corr);
+  }
+  if (tid == 0) a.rb_count[rb] = 0u;  // rest state for the next launch
+  if (a.mode != kObjective && a.mode != kGradient) return;
+  const double bl = consumer_sum(loss, shd);
+  const unsigned long long bc = consumer_sum_u64(corr, shu);
+  if (tid == 0) {
+    a.loss_part[rb] = bl;
+    a.corr_part[rb] = bc;
+    *flag = atomic_add_acq_rel(a.done_rb, 1u) == (unsigned)(a.row_blocks - 1);
+  }
+  consumer_sync(kConsumers);
+  if (!*flag) return;
+  double t = 0.0;
+  unsigned long long tc = 0;
+  for (int64_t i = tid; i < a.row_blocks; i += kConsumers) {
+    t += __ldcg(a.loss_part + i);
+    tc += __ldcg(a.corr_part + i);
+  }
+  const double tot = consumer_sum(t, shd);
+  const unsigned long long ct = consumer_sum_u64(tc, shu);
+  if (tid == 0) {
+    a.loss_out[0] = tot;
+    if (a.corr_out) a.corr_out[0] = (long long)ct;
+    *a.done_rb = 0u;
+  }
+}
+
 template <typename T, int K>
 __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constant__ G1Args a) {
+  pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
+  pdl_wait();
   if (a.skip != nullptr && *a.skip != 0.0) return;
   using Sh = G1Shape<T, K>;
   constexpr int V = Sh::V, S = Sh::S;
@@ -169,9 +366,14 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
   __syncthreads();
 
   const int G = gridDim.x, cta = blockIdx.x;
+  if (tid == 0) SNX_TL(0, 0);
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;  // more CTAs than items (the host never launches that)
   const int64_t rb0 = i0 / a.nchunks;
+  __shared__ double shd[kWarps];
+  __shared__ unsigned long long shu[kWarps];
+  __shared__ int flag;
+  __shared__ long long epi_rb;
   const int ch0 = (int)(i0 - rb0 * a.nchunks);
 
   if (warp == kWarps) {
@@ -208,10 +410,15 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
   T acc0[K], acc1[K], acc2[K];
 #pragma unroll
   for (int c = 0; c < K; ++c) acc0[c] = acc1[c] = acc2[c] = T(0);
+  // deferred last-arriver check (thread 0): the segment counter of the row
+  // block flushed last time, read one flush later so its latency is hidden
+  long long pend_rb = -1;
+  unsigned pend_prev = 0;
   int64_t rb = rb0;
   int ch = ch0;
   for (int64_t i = i0, it = 0; i <= i1; ++i) {
     if (i == i1 || (ch == 0 && i > i0)) {
+      if (i == i1 && tid == 0) SNX_TL(0, 2);
       // flush the segment partial of the row block just finished: warp pairs
       // (w, w+4) in smem, then the 4 pair sums in order
       const int64_t frb = (i == i1 && ch != 0) ? rb : rb - 1;
@@ -236,40 +443,71 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
 #pragma unroll
       for (int c = 0; c < K; ++c) acc0[c] = acc1[c] = acc2[c] = T(0);
       consumer_sync(kConsumers);
-      const int seg = cta - sk_owner(a.items, G, frb * a.nchunks);
-      double *zb = a.zp + (frb * a.maxseg + seg) * (int64_t)kRB * K;
+      const int c_lo = sk_owner(a.items, G, frb * a.nchunks);
+      double *zb = a.zp + (frb * a.maxseg + (cta - c_lo)) * (int64_t)kRB * K;
       const int valid = (int)min((int64_t)kRB, a.nrows - frb * kRB) * K;
       for (int t = tid; t < valid; t += kConsumers) {
         const double z = ((red[t] + red[kRB * K + t]) + red[2 * kRB * K + t]) +
                          red[3 * kRB * K + t];
         zb[t] = z;
       }
-      consumer_sync(kConsumers);  // red free again
+      consumer_sync(kConsumers);  // segment written; red free again
+      // resolve the previous arrival, publish this one (release), and on the
+      // final flush also resolve this one
+      if (tid == 0) {
+        epi_rb = -1;
+        if (pend_rb >= 0) {
+          const int n_prev = sk_owner(a.items, G, (pend_rb + 1) * a.nchunks - 1) -
+                             sk_owner(a.items, G, pend_rb * a.nchunks) + 1;
+          if (pend_prev == (unsigned)(n_prev - 1)) epi_rb = pend_rb;
+        }
+        pend_rb = frb;
+        pend_prev = atomic_add_acq_rel(&a.rb_count[frb], 1u);  // release our segment
+      }
+      consumer_sync(kConsumers);
+      for (int pass = 0; pass < 2; ++pass) {
+        if (epi_rb >= 0) {  // the acq_rel arrival already acquired the other segments
+          block_epilogue<T, K>(a, epi_rb, G, red, shd, shu, &flag);
+          consumer_sync(kConsumers);
+        }
+        if (i != i1 || pass == 1) break;
+        // final flush: wait for this CTA's own arrival and resolve it too
+        if (tid == 0) {
+          const int n_cur = sk_owner(a.items, G, (frb + 1) * a.nchunks - 1) - c_lo + 1;
+          epi_rb = (pend_prev == (unsigned)(n_cur - 1)) ? frb : -1;
+        }
+        consumer_sync(kConsumers);
+      }
     }
-    if (i == i1) break;
+    if (i == i1) {
+      if (tid == 0) SNX_TL(0, 3);
+      break;
+    }
     const int s = (int)(it % S);
     mbar_wait(&full[s], (unsigned)((it / S) & 1));
+    if (tid == 0 && it == 0) SNX_TL(0, 1);
     const unsigned char *st = smem + s * Sh::STAGE;
     const unsigned char *xa = st + box * Sh::BOX + lane * 128;
     const T *wp = reinterpret_cast<const T *>(st + Sh::NB * Sh::BOX) + warp * Sh::WC;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int off = ((c0 + q) ^ sw) * 16;
-      T v0[V], v1[V], v2[V];
+      T v0[V], v1[V], v2[V], w[K][V];
       lds(reinterpret_cast<const T *>(xa + off), v0);
       lds(reinterpret_cast<const T *>(xa + 32 * 128 + off), v1);
       lds(reinterpret_cast<const T *>(xa + 64 * 128 + off), v2);
 #pragma unroll
-      for (int c = 0; c < K; ++c) {
-        T w[V];
-        lds(wp + c * Sh::CHUNK + q * V, w);  // warp-uniform address: broadcast
+      for (int c = 0; c < K; ++c) lds(wp + c * Sh::CHUNK + q * V, w[c]);  // broadcasts
+      // column-outer order: consecutive FMAs hit different accumulators, the
+      // same accumulator recurs only every 3K instructions
 #pragma unroll
-        for (int v = 0; v < V; ++v) {
-          acc0[c] = fma(v0[v], w[v], acc0[c]);
-          acc1[c] = fma(v1[v], w[v], acc1[c]);
-          acc2[c] = fma(v2[v], w[v], acc2[c]);
+      for (int v = 0; v < V; ++v)
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+          acc0[c] = fma(v0[v], w[c][v], acc0[c]);
+          acc1[c] = fma(v1[v], w[c][v], acc1[c]);
+          acc2[c] = fma(v2[v], w[c][v], acc2[c]);
         }
-      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -278,157 +516,6 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
       ch = 0;
       ++rb;
     }
-  }
-}
-
-// ---------------------------------------------------------------- epilogue
-struct E1Args {
-  int64_t nrows;
-  int nchunks;
-  int maxseg;
-  int grid;        // CTAs of the GEMM1 launch
-  int64_t items;
-  int ustride;     // row stride of rowout (K for h, padded KP for R / U)
-  const double *zp;
-  const int32_t *labels;
-  const void *H;   // kHessApply: nrows*K probabilities
-  void *rowout;    // R (gradient), h (prep), U (apply)
-  double *loss_part;   // [blocks]
-  unsigned long long *corr_part;
-  unsigned *counter;
-  double *loss_out;
-  long long *corr_out;
-  const double *skip;
-};
-
-// Row epilogue: block b owns rows [96b, 96b+96); 4 threads per row sum the
-// CTA segment partials (fixed order), part 0 runs the softmax algebra.
-template <typename T, int K, int MODE>
-__global__ void __launch_bounds__(kEpiThreads) g1_epilogue_kernel(const E1Args a) {
-  if (a.skip != nullptr && *a.skip != 0.0) return;
-  __shared__ double shd[kEpiThreads / 32];
-  __shared__ unsigned long long shu[kEpiThreads / 32];
-  __shared__ bool last;
-  const int tid = threadIdx.x;
-  const int lr = tid >> 2, part = tid & 3;
-  const int64_t rb = blockIdx.x;
-  const int64_t r = rb * kRB + lr;
-  const bool valid = r < a.nrows;
-  double z[K];
-#pragma unroll
-  for (int c = 0; c < K; ++c) z[c] = 0.0;
-  if (valid) {
-    // segments of this row block = the CTAs that covered its chunks, in order
-    const int c_lo = sk_owner(a.items, a.grid, rb * a.nchunks);
-    const int nseg = sk_owner(a.items, a.grid, (rb + 1) * a.nchunks - 1) - c_lo + 1;
-    const double *zb = a.zp + (rb * a.maxseg * kRB + lr) * K;
-    int sg = part;
-    for (; sg + 4 < nseg; sg += 8) {  // two segments' loads in flight
-      double v0[K], v1[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        v0[c] = __ldcg(zb + (int64_t)sg * kRB * K + c);
-        v1[c] = __ldcg(zb + (int64_t)(sg + 4) * kRB * K + c);
-      }
-#pragma unroll
-      for (int c = 0; c < K; ++c) z[c] = (z[c] + v0[c]) + v1[c];
-    }
-    for (; sg < nseg; sg += 4) {
-#pragma unroll
-      for (int c = 0; c < K; ++c) z[c] += __ldcg(zb + (int64_t)sg * kRB * K + c);
-    }
-  }
-#pragma unroll
-  for (int c = 0; c < K; ++c) {  // (p0+p1)+(p2+p3), identical on the 4 lanes
-    z[c] += __shfl_xor_sync(0xffffffffu, z[c], 1);
-    z[c] += __shfl_xor_sync(0xffffffffu, z[c], 2);
-  }
-  double loss = 0.0;
-  unsigned long long corr = 0;
-  if (valid && part == 0) {
-    if (MODE == kHessApply) {
-      // softmax.py:206-208: VW = V*W; U = VW - W*rowsum(VW)
-      const T *h = static_cast<const T *>(a.H) + r * K;
-      double hw[K], vw[K], s = 0.0;
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        hw[c] = (double)h[c];
-        vw[c] = z[c] * hw[c];
-        s += vw[c];
-      }
-      T *u = static_cast<T *>(a.rowout) + r * a.ustride;
-#pragma unroll
-      for (int c = 0; c < K; ++c) u[c] = (T)(vw[c] - hw[c] * s);
-    } else {
-      // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
-      double M = 0.0;
-#pragma unroll
-      for (int c = 0; c < K; ++c) M = (z[c] > M || isnan(z[c])) ? z[c] : M;  // NaN propagates
-      double E[K], se = 0.0;
-#pragma unroll
-      for (int c = 0; c < K; ++c) {
-        E[c] = exp(z[c] - M);
-        se += E[c];
-      }
-      const double alpha = exp(-M) + se;
-      if (MODE == kHessPrep) {
-        T *h = static_cast<T *>(a.rowout) + r * a.ustride;
-#pragma unroll
-        for (int c = 0; c < K; ++c) h[c] = (T)(E[c] / alpha);
-      } else {
-        const int y = a.labels[r];
-        double lin = 0.0;
-#pragma unroll
-        for (int c = 0; c < K; ++c)
-          if (c == y) lin = z[c];
-        loss = (M + log(alpha)) - lin;  // softmax.py:134
-        if (MODE == kGradient) {
-          T *R = static_cast<T *>(a.rowout) + r * a.ustride;
-#pragma unroll
-          for (int c = 0; c < K; ++c) R[c] = (T)(E[c] / alpha - (c == y ? 1.0 : 0.0));
-        } else if (a.corr_out != nullptr) {
-          // softmax.py:224-240: argmax over [E/alpha, e^-M/alpha], first max wins
-          int best = 0;
-          double bv = E[0] / alpha;
-          bool nan_hit = isnan(bv);
-#pragma unroll
-          for (int c = 1; c <= K; ++c) {
-            const double pc = (c < K ? E[c] : exp(-M)) / alpha;
-            if (!nan_hit && (isnan(pc) || pc > bv)) {
-              best = c;
-              bv = pc;
-              nan_hit = isnan(pc);
-            }
-          }
-          corr = (best == y) ? 1ull : 0ull;
-        }
-      }
-    }
-  }
-  if (MODE != kObjective && MODE != kGradient) return;
-  const double bl = block_sum<kEpiThreads>(loss, shd);
-  const unsigned long long bc = block_sum_u64<kEpiThreads>(corr, shu);
-  if (tid == 0) {
-    a.loss_part[rb] = bl;
-    a.corr_part[rb] = bc;
-    __threadfence();  // release (cumulative over the barrier above)
-    last = atomicAdd(a.counter, 1u) == gridDim.x - 1;
-    if (last) __threadfence();  // acquire
-  }
-  __syncthreads();
-  if (!last) return;
-  double t = 0.0;
-  unsigned long long tc = 0;
-  for (int64_t i = tid; i < (int64_t)gridDim.x; i += kEpiThreads) {
-    t += __ldcg(a.loss_part + i);
-    tc += __ldcg(a.corr_part + i);
-  }
-  const double tot = block_sum<kEpiThreads>(t, shd);
-  const unsigned long long ct = block_sum_u64<kEpiThreads>(tc, shu);
-  if (tid == 0) {
-    a.loss_out[0] = tot;
-    if (a.corr_out) a.corr_out[0] = (long long)ct;
-    *a.counter = 0u;  // rest state for the next launch
   }
 }
 
@@ -446,6 +533,8 @@ struct G2Args {
 
 template <typename T, int K>
 __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constant__ G2Args a) {
+  pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
+  pdl_wait();
   if (a.skip != nullptr && *a.skip != 0.0) return;
   using Sh = G2Shape<T, K>;
   constexpr int V = Sh::V, LC = Sh::LC, TCOL = Sh::TCOL, KP = Sh::KP, S = Sh::S;
@@ -466,6 +555,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
   __syncthreads();
 
   const int G = gridDim.x, cta = blockIdx.x;
+  if (tid == 0) SNX_TL(1, 0);
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;
   const int tile0 = (int)(i0 / a.rchunks);
@@ -505,6 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
   int tile = tile0, rc = rc0;
   for (int64_t i = i0, it = 0; i <= i1; ++i) {
     if (i == i1 || (rc == 0 && i > i0)) {
+      if (i == i1 && tid == 0) SNX_TL(1, 2);
       // flush the segment partial of the tile just finished: warp pairs
       // (w, w+4), then the 4 pair sums in order
       const int ftile = (i == i1 && rc != 0) ? tile : tile - 1;
@@ -534,9 +625,13 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
         gb[t] = ((red[t] + red[K * TCOL + t]) + red[2 * K * TCOL + t]) + red[3 * K * TCOL + t];
       consumer_sync(kConsumers);  // red free again
     }
-    if (i == i1) break;
+    if (i == i1) {
+      if (tid == 0) SNX_TL(1, 3);
+      break;
+    }
     const int s = (int)(it % S);
     mbar_wait(&full[s], (unsigned)((it / S) & 1));
+    if (tid == 0 && it == 0) SNX_TL(1, 1);
     const int nr = (int)min((int64_t)kG2Rows, a.nrows - (int64_t)rc * kG2Rows);
     const T *xs = reinterpret_cast<const T *>(smem + s * Sh::STAGE);
     const T *us = reinterpret_cast<const T *>(smem + s * Sh::STAGE + Sh::XB);
@@ -580,6 +675,7 @@ __global__ void __launch_bounds__(kDotThreads)
                     int maxseg, int tcol, int K, int p, double scale, double lam,
                     const double *__restrict__ base, double *__restrict__ out, double *dots,
                     const double *skip) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   if (skip != nullptr && *skip != 0.0) return;
   __shared__ double sh[kDotThreads / 32];
   double bo = 0.0, bb = 0.0;
@@ -624,6 +720,7 @@ __global__ void __launch_bounds__(kDotThreads)
 __global__ void __launch_bounds__(kDotThreads)
     lam_only_kernel(int K, int p, double lam, const double *__restrict__ base,
                     double *__restrict__ out, double *dots, const double *skip) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   if (skip != nullptr && *skip != 0.0) return;
   __shared__ double sh[kDotThreads / 32];
   double bo = 0.0, bb = 0.0;
@@ -780,7 +877,7 @@ static int launch_persistent(KernelT kernel, int grid, size_t smem, size_t *conf
     *configured = smem;
   }
   carveout(kernel);
-  kernel<<<grid, kThreads, smem, st>>>(args);  // persistent: one CTA per SM
+  launch_pdl(kernel, dim3(grid), dim3(kThreads), smem, st, args);  // one CTA per SM
   return check_launch(what);
 }
 
@@ -796,18 +893,6 @@ static int launch_gemm2(const G2Args &a, int grid, cudaStream_t st) {
   static size_t configured = 0;
   return launch_persistent(gemm2_kernel<T, K>, grid, G2Shape<T, K>::SMEM, &configured, st, a,
                            "gemm2");
-}
-
-template <typename T, int K>
-static int launch_epilogue(int mode, const E1Args &e, int64_t blocks, cudaStream_t st) {
-  const dim3 grid((unsigned)blocks), block(kEpiThreads);
-  switch (mode) {
-    case kObjective: g1_epilogue_kernel<T, K, kObjective><<<grid, block, 0, st>>>(e); break;
-    case kGradient: g1_epilogue_kernel<T, K, kGradient><<<grid, block, 0, st>>>(e); break;
-    case kHessPrep: g1_epilogue_kernel<T, K, kHessPrep><<<grid, block, 0, st>>>(e); break;
-    default: g1_epilogue_kernel<T, K, kHessApply><<<grid, block, 0, st>>>(e); break;
-  }
-  return check_launch("epilogue");
 }
 
 #define SNX_K_SWITCH(K, CALL)                         \
@@ -908,7 +993,7 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
         return check_launch("memset");
     }
     if (mode == kGradient || mode == kHessApply) {
-      lam_only_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(K, p, lam, base, vec_out, dots, skip);
+      launch_pdl(lam_only_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, K, p, lam, base, vec_out, dots, skip);
       return check_launch("lam_only");
     }
     return 0;
@@ -926,32 +1011,23 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   a.items = g.g1_items;
   a.zp = zp;
   a.skip = skip;
-  E1Args e{};
-  e.nrows = nrows;
-  e.nchunks = g.nchunks;
-  e.maxseg = g.g1_maxseg;
-  e.grid = g.grid1;
-  e.items = g.g1_items;
-  e.ustride = mode == kHessPrep ? K : u_stride(dtype, K);
-  e.zp = zp;
-  e.labels = labels;
-  e.H = H;
-  e.rowout = rowbuf;
-  e.loss_part = reinterpret_cast<double *>(wsb + lay.loss_part);
-  e.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
-  e.counter = counters + 2;
-  e.loss_out = out;
-  e.corr_out = corr_out;
-  e.skip = skip;
+  a.row_blocks = g.row_blocks;
+  a.mode = mode;
+  a.ustride = mode == kHessPrep ? K : u_stride(dtype, K);
+  a.rb_count = counters + 16 + kMaxTiles;  // [row_blocks]
+  a.done_rb = counters + 2;
+  a.labels = labels;
+  a.H = H;
+  a.rowout = rowbuf;
+  a.loss_part = reinterpret_cast<double *>(wsb + lay.loss_part);
+  a.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
+  a.loss_out = out;
+  a.corr_out = corr_out;
   int rc = 1;
   if (dtype == SNX_F64) {
     SNX_K_SWITCH(K, (rc = launch_gemm1<double, KK>(a, g.grid1, st)));
-    if (rc) return rc;
-    SNX_K_SWITCH(K, (rc = launch_epilogue<double, KK>(mode, e, g.row_blocks, st)));
   } else {
     SNX_K_SWITCH(K, (rc = launch_gemm1<float, KK>(a, g.grid1, st)));
-    if (rc) return rc;
-    SNX_K_SWITCH(K, (rc = launch_epilogue<float, KK>(mode, e, g.row_blocks, st)));
   }
   if (rc) return rc;
   if (mode != kGradient && mode != kHessApply) return 0;
@@ -971,7 +1047,7 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
     SNX_K_SWITCH(K, (rc = launch_gemm2<float, KK>(b, g.grid2, st)));
   }
   if (rc) return rc;
-  finalize_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(b.gp, g.g2_items, g.grid2, g.rchunks,
+  launch_pdl(finalize_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, b.gp, g.g2_items, g.grid2, g.rchunks,
                                                       g.g2_maxseg, g.tcol, K, p, scale, lam,
                                                       base, vec_out, dots, skip);
   return check_launch("finalize");
@@ -1011,6 +1087,12 @@ static int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels,
 using namespace snx;
 
 extern "C" {
+
+#ifdef SNX_TIMELINE
+int snx_debug_timeline(unsigned long long *host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_timeline, sizeof(g_timeline)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 size_t snx_workspace_bytes(int dtype, int64_t nrows, int32_t p, int32_t K) {
   return workspace_layout(dtype, nrows, p, K).total;

@@ -3,9 +3,11 @@
 // grid of SNX_DOT_BLOCKS blocks so every reduction has one summation order.
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "snx_common.cuh"
 #include "snx_internal.h"
+#include "snx_pipe.cuh"
 
 namespace snx {
 
@@ -16,6 +18,17 @@ void set_error(const char *fmt, ...) {
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+bool pdl_enabled() {
+  // Off by default: measured on B200, dependent CTAs made resident early slow
+  // the short epilogue/finalize kernels 2-4x; SNX_PDL=1 re-enables it.
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SNX_PDL");
+    on = (e != nullptr && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
 }
 
 void prefer_max_smem(const void *kernel) {
@@ -46,6 +59,7 @@ __global__ void __launch_bounds__(kDotThreads)
     prep_weights_kernel(const double *__restrict__ w, const double *__restrict__ dir,
                         double alpha, int K, int p, int P, T *__restrict__ Wt, double *part,
                         unsigned *counter, double *wsq_out) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   __shared__ double sh[kDotThreads / 32];
   __shared__ bool last;
   double acc = 0.0;
@@ -90,10 +104,10 @@ int launch_prep_weights(int dtype, const double *w, const double *dir, double al
                         int p, int P, void *Wt, double *part, unsigned *counter,
                         double *wsq_out, cudaStream_t st) {
   if (dtype == SNX_F64) {
-    prep_weights_kernel<double><<<kDotBlocks, kDotThreads, 0, st>>>(
+    launch_pdl(prep_weights_kernel<double>, dim3(kDotBlocks), dim3(kDotThreads), 0, st, 
         w, dir, alpha, K, p, P, static_cast<double *>(Wt), part, counter, wsq_out);
   } else {
-    prep_weights_kernel<float><<<kDotBlocks, kDotThreads, 0, st>>>(
+    launch_pdl(prep_weights_kernel<float>, dim3(kDotBlocks), dim3(kDotThreads), 0, st, 
         w, dir, alpha, K, p, P, static_cast<float *>(Wt), part, counter, wsq_out);
   }
   return check_launch("prep_weights");
@@ -102,6 +116,7 @@ int launch_prep_weights(int dtype, const double *w, const double *dir, double al
 __global__ void __launch_bounds__(kDotThreads)
     dot_part_kernel(const double *__restrict__ x, const double *__restrict__ y, int64_t d,
                     double *part) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   __shared__ double sh[kDotThreads / 32];
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
@@ -112,6 +127,7 @@ __global__ void __launch_bounds__(kDotThreads)
 }
 
 __global__ void dot_final_kernel(const double *part, double *out) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   const double t = warp_sum_partials(part);
   if (threadIdx.x == 0) *out = t;
 }
@@ -119,6 +135,7 @@ __global__ void dot_final_kernel(const double *part, double *out) {
 __global__ void __launch_bounds__(kDotThreads)
     axpy_kernel(const double *__restrict__ x, const double *__restrict__ p, double alpha,
                 int64_t d, double *__restrict__ out) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
        i += (int64_t)kDotBlocks * kDotThreads)
     out[i] = np_axpy(x[i], alpha, p[i]);
@@ -127,6 +144,7 @@ __global__ void __launch_bounds__(kDotThreads)
 __global__ void __launch_bounds__(kDotThreads)
     axpby_kernel(double a, const double *__restrict__ x, double b, const double *__restrict__ y,
                  int64_t d, double *__restrict__ out) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
        i += (int64_t)kDotBlocks * kDotThreads)
     out[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
@@ -146,6 +164,7 @@ __device__ __forceinline__ double *scratch(double *state, int max_iters) {
 __global__ void __launch_bounds__(kDotThreads)
     cg_init_kernel(const double *__restrict__ g, int64_t d, int max_iters, double *r,
                    double *s, double *p, double *pb, double *state) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   __shared__ double sh[kDotThreads / 32];
   double acc = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
@@ -166,6 +185,7 @@ __global__ void __launch_bounds__(kDotThreads)
 }
 
 __global__ void cg_init_final_kernel(double theta, int max_iters, double *state) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   const double gg = warp_sum_partials(scratch(state, max_iters));
   if (threadIdx.x == 0) {
     double *s0 = slot(state, 0);
@@ -184,6 +204,7 @@ __global__ void __launch_bounds__(kDotThreads)
     cg_step1_kernel(int t, int max_iters, int64_t d, const double *__restrict__ Hs,
                     const double *__restrict__ dots, double *r, const double *s, double *p,
                     double *state) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   const double *st = slot(state, t);
   if (st[kDone] != 0.0) return;
   __shared__ double sh[kDotThreads / 32];
@@ -220,6 +241,7 @@ __global__ void __launch_bounds__(kDotThreads)
 __global__ void __launch_bounds__(kDotThreads)
     cg_step2_kernel(int t, int max_iters, int64_t d, const double *__restrict__ r, double *s,
                     const double *__restrict__ p, double *pb, double *state) {
+  pdl_wait();  // successor launches when this grid exits (implicit trigger)
   const double *st = slot(state, t);
   double *nx = slot(state, t + 1);
   if (st[kDone] != 0.0) {
@@ -288,26 +310,26 @@ const char *snx_last_error(void) { return g_err; }
 int snx_dot(const double *x, const double *y, int64_t d, double *out, void *stream) {
   // out holds 1 + SNX_DOT_BLOCKS doubles: the partials go to out[1..]
   cudaStream_t st = (cudaStream_t)stream;
-  dot_part_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(x, y, d, out + 1);
+  launch_pdl(dot_part_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, x, y, d, out + 1);
   if (check_launch("dot")) return 1;
-  dot_final_kernel<<<1, 32, 0, st>>>(out + 1, out);
+  launch_pdl(dot_final_kernel, dim3(1), dim3(32), 0, st, out + 1, out);
   return check_launch("dot_final");
 }
 
 int snx_dot_partials(const double *x, const double *y, int64_t d, double *part, void *stream) {
-  dot_part_kernel<<<kDotBlocks, kDotThreads, 0, (cudaStream_t)stream>>>(x, y, d, part);
+  launch_pdl(dot_part_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, (cudaStream_t)stream, x, y, d, part);
   return check_launch("dot_partials");
 }
 
 int snx_axpy(const double *x, const double *p, double alpha, int64_t d, double *x_out,
              void *stream) {
-  axpy_kernel<<<kDotBlocks, kDotThreads, 0, (cudaStream_t)stream>>>(x, p, alpha, d, x_out);
+  launch_pdl(axpy_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, (cudaStream_t)stream, x, p, alpha, d, x_out);
   return check_launch("axpy");
 }
 
 int snx_axpby(double a, const double *x, double b, const double *y, int64_t d, double *out,
               void *stream) {
-  axpby_kernel<<<kDotBlocks, kDotThreads, 0, (cudaStream_t)stream>>>(a, x, b, y, d, out);
+  launch_pdl(axpby_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, (cudaStream_t)stream, a, x, b, y, d, out);
   return check_launch("axpby");
 }
 
@@ -318,9 +340,9 @@ int snx_cg_init(const double *g, int64_t d, double theta, int32_t max_iters, dou
     return 1;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  cg_init_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(g, d, max_iters, r, s, p, p_best, state);
+  launch_pdl(cg_init_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, g, d, max_iters, r, s, p, p_best, state);
   if (check_launch("cg_init")) return 1;
-  cg_init_final_kernel<<<1, 32, 0, st>>>(theta, max_iters, state);
+  launch_pdl(cg_init_final_kernel, dim3(1), dim3(32), 0, st, theta, max_iters, state);
   return check_launch("cg_init_final");
 }
 
@@ -332,10 +354,10 @@ int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
     return 1;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  cg_step1_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(t, max_iters, d, Hs, dots, r, s, p,
+  launch_pdl(cg_step1_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, t, max_iters, d, Hs, dots, r, s, p,
                                                       state);
   if (check_launch("cg_step1")) return 1;
-  cg_step2_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(t, max_iters, d, r, s, p, p_best, state);
+  launch_pdl(cg_step2_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, t, max_iters, d, r, s, p, p_best, state);
   return check_launch("cg_step2");
 }
 
