@@ -41,36 +41,39 @@ def peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    """nvidia-smi clocks / throttle reasons sampled every 50 ms by ONE
+    background nvidia-smi process started before the timed region (no fork
+    inside it); the summary keeps the samples taken while the region ran."""
 
     Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index=0):
-        self.index, self.samples, self._stop = index, [], threading.Event()
-        self._t = threading.Thread(target=self._run, daemon=True)
-
-    def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(
-                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                     "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                    timeout=5).stdout.strip()
-                if out:
-                    self.samples.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        self.index, self.samples, self.proc = index, [], None
 
     def __enter__(self):
-        self._t.start()
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            time.sleep(0.3)  # first sample lands before the timed region
+        except OSError:
+            self.proc = None
         return self
 
     def __exit__(self, *a):
-        self._stop.set()
-        self._t.join(timeout=10)
+        if self.proc is None:
+            return
+        time.sleep(0.1)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=10)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out = ""
+        self.samples = [[t.strip() for t in ln.split(",")] for ln in out.splitlines() if ln]
 
     def summary(self):
         if not self.samples:
@@ -90,7 +93,7 @@ def make_problem(seed=0):
     return oracle.synthetic_problem(N, P, C, seed=seed)
 
 
-def cpu_baseline(A, y, x, steps_budget_s=12.0, max_steps=50):
+def cpu_baseline(A, y, x, steps_budget_s=10.0, max_steps=1000):
     """The oracle port (numpy/OpenBLAS fp64) on the same step: h-prep on a fresh
     S_H + CG with <= 10 Hessian products; bounded to ~steps_budget_s."""
     import oracle
@@ -175,23 +178,43 @@ def run_ours(args):
 
     A, y = make_problem()
     x_host = 0.01 * np.random.default_rng(7).standard_normal((C - 1) * P)
-    ds = snx.DeviceDataset.from_numpy(A, y, C, dtype=args.dtype)
-    prob = snx.SoftmaxProblem(ds, LAM)
     dev = torch.device("cuda", local)
     x = torch.from_numpy(x_host).to(dev)
-    g, _ = softmax.gradient_parts(ds, x, 1.0, LAM)
     total = args.warmup + args.steps
-    # inputs of every step (fresh S_H per step) resident before timing
-    views = [ds.take(snx.draw_samples(snx.SampleConfig(1.0, F_H), N, k)[1]) for k in range(total)]
-    m = views[0].n_rows
-    ops = [None] * total
+    samples = snx.SampleConfig(1.0, F_H)
     iters = torch.zeros(total, dtype=torch.float64, device=dev)
+    if world == 1:
+        ds = snx.DeviceDataset.from_numpy(A, y, C, dtype=args.dtype)
+        prob = snx.SoftmaxProblem(ds, LAM)
+        g, _ = softmax.gradient_parts(ds, x, 1.0, LAM)
+        # inputs of every step (fresh S_H per step) resident before timing
+        views = [ds.take(snx.draw_samples(samples, N, k)[1]) for k in range(total)]
+        m = views[0].n_rows
+        ops = [None] * total
 
-    def step(k):
-        op = softmax.HessianOperator(views[k], x, LAM, scale=N / m)
-        ops[k] = op
-        ws = cgmod.cg_graph_for(op, T_CG, THETA).run(g)  # CUDA-graph replay of the CG loop
-        iters[k:k + 1].copy_(ws.slot(T_CG)[3:4])
+        def step(k):
+            op = softmax.HessianOperator(views[k], x, LAM, scale=N / m)
+            ops[k] = op
+            ws = cgmod.cg_graph_for(op, T_CG, THETA).run(g)  # CUDA-graph replay of the CG loop
+            iters[k:k + 1].copy_(ws.slot(T_CG)[3:4])
+    else:
+        # rows sharded over the ranks (strong scaling: the CIFAR problem is fixed)
+        from paper_1802_09113_b200 import distributed as sd
+
+        sp = sd.ShardedProblem.from_global(A, y, C, LAM, dtype=args.dtype)
+        ds = sp.local
+        prob = None
+        oracles = [sd.ShardedOracle(sp, samples, k) for k in range(total)]
+        g = oracles[0].gradient_device(x)
+        m = len(oracles[0].s_h)
+        cgws = cgmod.CgWorkspace(ds.dim, T_CG, dev)
+        ops = [None] * total
+
+        def step(k):
+            op = oracles[k].hessian_operator(x)
+            ops[k] = op
+            cgmod.enqueue_cg(op, g, THETA, T_CG, cgws)
+            iters[k:k + 1].copy_(cgws.slot(T_CG)[3:4])
 
     for k in range(args.warmup):
         step(k)
@@ -219,6 +242,8 @@ def run_ours(args):
     op = ops[-1]
     v = g.clone()
     out = torch.empty_like(v)
+    if world > 1:
+        op = op.op  # the local product (the all-reduce is timed in `value`)
     reps = 50
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
     for _ in range(5):
@@ -231,6 +256,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     hv_ms = ev[0].elapsed_time(ev[1]) / reps
     tb = 8 if args.dtype == "f64" else 4
+    m = op.view.n_rows  # rows this GPU streams per product
     alg_bytes = m * P * tb + m * (C - 1) * tb + 2 * ds.dim * 8
     pk, pk_kind = peaks()
     achieved = alg_bytes / (hv_ms / 1e3) / 1e9
@@ -242,6 +268,8 @@ def run_ours(args):
                 "note": "X_S rows re-read from L2 across CG iterations; bytes counted once"}
 
     # ---- e2e: the public numpy API, host buffers in and out
+    if world > 1:
+        args.skip_solve = True
     g_host = g.cpu().numpy()
     cfg = snx.CgConfig(THETA, T_CG)
     torch.cuda.synchronize()
@@ -249,7 +277,10 @@ def run_ours(args):
     e2e_hv = 0
     e2e_steps = max(3, min(args.steps, 20))
     for k in range(e2e_steps):
-        orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, F_H), 500 + k)
+        if world == 1:
+            orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, F_H), 500 + k)
+        else:
+            orc = sd.ShardedOracle(sp, snx.SampleConfig(1.0, F_H), 500 + k)
         rep = snx.cg_solve(orc.hessian_operator(x_host), g_host, cfg)
         e2e_hv += rep.iterations
     e2e_s = time.perf_counter() - t0
@@ -285,7 +316,7 @@ def run_ours(args):
             "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": "cifar10-shape 50000x3072 C=10, 5% S_H (m=2500)",
                        "n": N, "p": P, "C": C, "hessian_fraction": F_H, "lam": LAM,
-                       "theta": THETA, "cg_max_iters": T_CG, "parallelism": f"rows/{world}",
+                       "theta": THETA, "cg_max_iters": T_CG, "parallelism": f"rows sharded over {world} GPU(s), NCCL all-reduce per Hv",
                        "l2": "inputs > L2: 1.23 GB X in HBM, fresh S_H gathered every step"},
             "hv_applied": hv_count, "gpu_launches": args.steps * (4 + 2 + 6 * T_CG),
             "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
@@ -299,7 +330,7 @@ def run_ours(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])

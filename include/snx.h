@@ -116,6 +116,13 @@ int snx_axpy(const double *x, const double *p, double alpha, int64_t d, double *
 int snx_axpby(double a, const double *x, double b, const double *y, int64_t d, double *out,
               void *stream);
 
+/* Finish a row-sharded product after the cross-rank sum:
+ *   out = out + lam * v   (numpy rounding of `sum + lam * v`)
+ * and, when dots != NULL, the SNX_DOT_BLOCKS-partials layout of snx_hess_apply
+ * (v.out | v.v) for the CG update. */
+int snx_finish_hv(const double *v, double lam, int64_t d, double *out, double *dots,
+                  const double *skip, void *stream);
+
 /* Device CG (cg.py:51-98).  state: (max_iters+2)*SNX_CG_SLOT + SNX_DOT_BLOCKS
  * doubles (the tail is reduction scratch); slot t
  * holds the scalars entering iteration t: [rs, best_norm, done, iters,

@@ -38,6 +38,7 @@ SIGNATURES = {
     "snx_dot_partials": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "snx_axpy": (_c_int, [_c_p, _c_p, _c_dbl, _c_i64, _c_p, _c_p]),
     "snx_axpby": (_c_int, [_c_dbl, _c_p, _c_dbl, _c_p, _c_i64, _c_p, _c_p]),
+    "snx_finish_hv": (_c_int, [_c_p, _c_dbl, _c_i64, _c_p, _c_p, _c_p, _c_p]),
     "snx_cg_init": (_c_int, [_c_p, _c_i64, _c_dbl, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p]),
     "snx_cg_update": (_c_int, [_c_i32, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                _c_p]),

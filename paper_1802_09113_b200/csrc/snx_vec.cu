@@ -150,6 +150,30 @@ __global__ void __launch_bounds__(kDotThreads)
     out[i] = __dadd_rn(__dmul_rn(a, x[i]), __dmul_rn(b, y[i]));
 }
 
+__global__ void __launch_bounds__(kDotThreads)
+    finish_hv_kernel(const double *__restrict__ v, double lam, int64_t d, double *out,
+                     double *dots, const double *skip) {
+  pdl_wait();
+  if (skip != nullptr && *skip != 0.0) return;
+  __shared__ double sh[kDotThreads / 32];
+  double bo = 0.0, bb = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    const double b = v[i];
+    const double o = np_axpy(out[i], lam, b);
+    out[i] = o;
+    bo += b * o;
+    bb += b * b;
+  }
+  if (dots == nullptr) return;
+  const double so = block_sum<kDotThreads>(bo, sh);
+  const double sb = block_sum<kDotThreads>(bb, sh);
+  if (threadIdx.x == 0) {
+    dots[blockIdx.x] = so;
+    dots[kDotBlocks + blockIdx.x] = sb;
+  }
+}
+
 // ------------------------------------------------------------------ CG (cg.py)
 // slot layout (SNX_CG_SLOT doubles)
 enum { kRs = 0, kBest = 1, kDone = 2, kIters = 3, kConv = 4, kThr = 5, kErr = 6, kCurv = 7 };
@@ -331,6 +355,13 @@ int snx_axpby(double a, const double *x, double b, const double *y, int64_t d, d
               void *stream) {
   launch_pdl(axpby_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, (cudaStream_t)stream, a, x, b, y, d, out);
   return check_launch("axpby");
+}
+
+int snx_finish_hv(const double *v, double lam, int64_t d, double *out, double *dots,
+                  const double *skip, void *stream) {
+  launch_pdl(finish_hv_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, (cudaStream_t)stream, v,
+             lam, d, out, dots, skip);
+  return check_launch("finish_hv");
 }
 
 int snx_cg_init(const double *g, int64_t d, double theta, int32_t max_iters, double *r,
