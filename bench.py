@@ -87,6 +87,11 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+# dram__bytes_read.sum + dram__bytes_write.sum of one Hessian product's two GEMM
+# kernels, from the committed ncu --set full capture (per launch, cold cache)
+TRAFFIC = {"f64": 61.660672e6 + 0.47232e6 + 61.907456e6 + 0.493312e6}
+
+
 def make_problem(seed=0):
     import oracle  # synthetic data generator only (the checker's data recipe)
 
@@ -190,11 +195,11 @@ def run_ours(args):
         # inputs of every step (fresh S_H per step) resident before timing
         views = [ds.take(snx.draw_samples(samples, N, k)[1]) for k in range(total)]
         m = views[0].n_rows
-        ops = [None] * total
+        ops = [None]
 
         def step(k):
             op = softmax.HessianOperator(views[k], x, LAM, scale=N / m)
-            ops[k] = op
+            ops[0] = op  # keep only the latest operator alive
             ws = cgmod.cg_graph_for(op, T_CG, THETA).run(g)  # CUDA-graph replay of the CG loop
             iters[k:k + 1].copy_(ws.slot(T_CG)[3:4])
     else:
@@ -208,11 +213,11 @@ def run_ours(args):
         g = oracles[0].gradient_device(x)
         m = len(oracles[0].s_h)
         cgws = cgmod.CgWorkspace(ds.dim, T_CG, dev)
-        ops = [None] * total
+        ops = [None]
 
         def step(k):
             op = oracles[k].hessian_operator(x)
-            ops[k] = op
+            ops[0] = op
             cgmod.enqueue_cg(op, g, THETA, T_CG, cgws)
             iters[k:k + 1].copy_(cgws.slot(T_CG)[3:4])
 
@@ -225,11 +230,24 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
+        prof = None
+        if os.environ.get("SNX_BENCH_PROFILE"):
+            import cProfile
+
+            prof = cProfile.Profile()
+            prof.enable()
         e0.record(st)
+        h0 = time.perf_counter()
         for k in range(args.warmup, total):
             step(k)
+        host_ms = (time.perf_counter() - h0) * 1e3
         e1.record(st)
         torch.cuda.synchronize()
+        if prof is not None:
+            import pstats
+
+            prof.disable()
+            pstats.Stats(prof, stream=sys.stderr).sort_stats("cumulative").print_stats(25)
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -239,7 +257,7 @@ def run_ours(args):
     value = hv_count / (ms / 1e3)
 
     # ---- roofline of the dominant op: one Hessian product (snx_hess_apply)
-    op = ops[-1]
+    op = ops[0]
     v = g.clone()
     out = torch.empty_like(v)
     if world > 1:
@@ -261,7 +279,9 @@ def run_ours(args):
     pk, pk_kind = peaks()
     achieved = alg_bytes / (hv_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                "frac": achieved / pk["hbm_gbs"], "traffic": None,
+                "frac": achieved / pk["hbm_gbs"], "traffic": TRAFFIC.get(args.dtype),
+                "traffic_source": "profiles/r01_hv_gemms_ncu_full.txt: dram read+write of gemm1+gemm2 "
+                                  "per product, ncu cold cache (X_S read once per GEMM)",
                 "kernel": "snx_hess_apply (rowpass GEMM1+ComputeU, xtu GEMM2, finalize)",
                 "peak_kind": pk_kind, "ms_per_launch": hv_ms,
                 "flops_per_launch": 4 * m * P * (C - 1),
@@ -312,6 +332,7 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "host_ms_per_step": host_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
             "config": {"workload": "cifar10-shape 50000x3072 C=10, 5% S_H (m=2500)",
