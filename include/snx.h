@@ -98,6 +98,22 @@ int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_
                    const void *H, const double *v, double scale, double lam, double *Hv_out,
                    double *dots, const double *skip, void *ws, size_t ws_bytes, void *stream);
 
+/* Tensor-core variant of the two calls above for f32 data (the declared 1e-4
+ * path; tcgen05 kind::tf32 MMAs with a 3xTF32 split, see csrc/snx_tc.cu).
+ * snx_hess_prepare_tc = snx_hess_prepare(SNX_F32, ...) plus
+ *   Xlo_out[r][j] = Xs[r][j] - tf32(Xs[r][j])   (same shape and ld as Xs),
+ * the low part every product of this sample reuses.  When rows == NULL the
+ * sample is X itself and Xlo_out has X's shape and ldx. */
+int snx_hess_prepare_tc(const float *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+                        int32_t p, int32_t K, const double *w, float *Xs_out, float *Xlo_out,
+                        int64_t ld_out, float *H_out, void *ws, size_t ws_bytes, void *stream);
+
+/* snx_hess_apply(SNX_F32, ...) on the tensor cores; Xlo from snx_hess_prepare_tc. */
+int snx_hess_apply_tc(const float *Xs, const float *Xlo, int64_t ldx, int64_t nrows, int32_t p,
+                      int32_t K, const float *H, const double *v, double scale, double lam,
+                      double *Hv_out, double *dots, const double *skip, void *ws,
+                      size_t ws_bytes, void *stream);
+
 /* Fixed-order dot product: out[0] = x . y (np.dot / np.linalg.norm**2).
  * out must hold 1 + SNX_DOT_BLOCKS doubles (out[1..] = block partials). */
 int snx_dot(const double *x, const double *y, int64_t d, double *out, void *stream);

@@ -44,9 +44,38 @@ struct Workspace {
   size_t corr_part;   // row_blocks uint64
   size_t dot_part;    // 4*kDotBlocks doubles (w.w partials)
   size_t counters;    // uint32 scheduler words + arrival counters (zero at rest)
+  // f32 tensor-core Hessian product (snx_tc.cu); zero-sized for f64
+  size_t tc_b;        // [32][P] f32: B operand of GEMM1 (v rows, then v - tf32(v) rows)
+  size_t tc_ut;       // [32][round_up(nrows,4)] f32: U^T rows, then U^T - tf32(U^T) rows
+  size_t tc_zp;       // GEMM1 segment partials [row_blocks][maxseg1][128][K] doubles
+  size_t tc_gp;       // GEMM2 segment partials [col_tiles][maxseg2][K][128] doubles
   size_t total;
 };
+// Geometry of the tensor-core Hessian product: GEMM1 items = (128-row block x
+// 32-column k-tile), GEMM2 items = (128-column tile x 32-row chunk), each
+// split stream-K over <= one CTA per SM.
+struct TcGeometry {
+  int grid1, nk;
+  int64_t row_blocks, items1;
+  int maxseg1;
+  int grid2, col_tiles, rchunks;
+  int64_t items2;
+  int maxseg2;
+};
+TcGeometry tc_geometry(int64_t nrows, int32_t P);
+int sk_maxseg(int64_t items, int grid, int per_group);
+int sm_count();
+
 Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K);
+int validate(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
+             void *ws, size_t ws_bytes);
+int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels, const int64_t *rows,
+           int64_t nrows, void *dst, int64_t ldd, int32_t *labels_out, cudaStream_t st);
+int launch_finalize(const double *gp, int64_t items, int grid, int rchunks, int maxseg, int tcol,
+                    int K, int p, double scale, double lam, const double *base, double *out,
+                    double *dots, const double *skip, cudaStream_t st);
+int launch_lam_only(int K, int p, double lam, const double *base, double *out, double *dots,
+                    const double *skip, cudaStream_t st);
 inline int32_t padded(int32_t p) { return (p + 3) / 4 * 4; }
 
 // Ask for the maximum shared-memory carveout once per kernel: every libsnx

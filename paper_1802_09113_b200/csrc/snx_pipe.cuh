@@ -5,6 +5,14 @@
 
 namespace snx {
 
+// Stream-K split of `items` over `G` CTAs: CTA c owns [T*c/G, T*(c+1)/G).
+__host__ __device__ __forceinline__ int64_t sk_begin(int64_t T, int G, int c) {
+  return T * c / G;
+}
+__host__ __device__ __forceinline__ int sk_owner(int64_t T, int G, int64_t i) {
+  return (int)(((i + 1) * G - 1) / T);
+}
+
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
 }

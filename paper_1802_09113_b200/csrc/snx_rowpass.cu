@@ -172,13 +172,6 @@ __device__ __forceinline__ unsigned long long consumer_sum_u64(unsigned long lon
   return t;
 }
 
-// Stream-K split of `items` over `G` CTAs: CTA c owns [T*c/G, T*(c+1)/G).
-__host__ __device__ __forceinline__ int64_t sk_begin(int64_t T, int G, int c) {
-  return T * c / G;
-}
-__host__ __device__ __forceinline__ int sk_owner(int64_t T, int G, int64_t i) {
-  return (int)(((i + 1) * G - 1) / T);
-}
 
 // ---------------------------------------------------------------- GEMM1
 struct G1Args {
@@ -743,6 +736,21 @@ __global__ void __launch_bounds__(kDotThreads)
   }
 }
 
+int launch_finalize(const double *gp, int64_t items, int grid, int rchunks, int maxseg, int tcol,
+                    int K, int p, double scale, double lam, const double *base, double *out,
+                    double *dots, const double *skip, cudaStream_t st) {
+  launch_pdl(finalize_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, gp, items, grid,
+             rchunks, maxseg, tcol, K, p, scale, lam, base, out, dots, skip);
+  return check_launch("finalize");
+}
+
+int launch_lam_only(int K, int p, double lam, const double *base, double *out, double *dots,
+                    const double *skip, cudaStream_t st) {
+  launch_pdl(lam_only_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, K, p, lam, base, out,
+             dots, skip);
+  return check_launch("lam_only");
+}
+
 // Row gather (dataset.py:90-97 `take`): dst[r][0:ldd] = X[rows[r]][0:ldd],
 // labels_out[r] = labels[rows[r]]; one warp per row, 16-B vectors.
 template <typename T>
@@ -764,9 +772,9 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------- host side
-static int g_sms = 0;
+static int g_sms = 0;  // cached SM count
 
-static int sm_count() {
+int sm_count() {
   if (g_sms == 0) {
     int dev = 0;
     cudaGetDevice(&dev);
@@ -779,8 +787,8 @@ static int sm_count() {
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-static int make_map(CUtensorMap *m, int dtype, const void *base, uint64_t cols, uint64_t rows,
-                    uint64_t ld, uint32_t box_cols, uint32_t box_rows, bool swizzle) {
+int make_tmap(CUtensorMap *m, bool f64, const void *base, uint64_t cols, uint64_t rows,
+              uint64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
   if (g_encode == nullptr) {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -792,15 +800,14 @@ static int make_map(CUtensorMap *m, int dtype, const void *base, uint64_t cols, 
     }
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
-  const size_t tb = dtype_bytes(dtype);
+  const size_t tb = f64 ? 8 : 4;
   const cuuint64_t dims[2] = {cols, rows > 0 ? rows : 1};
   const cuuint64_t strides[1] = {ld * tb};
   const cuuint32_t box[2] = {box_cols, box_rows};
   const cuuint32_t es[2] = {1, 1};
   const CUresult r = g_encode(
-      m, dtype == SNX_F64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-      const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-      swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+      m, f64 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+      const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     set_error("snx: cuTensorMapEncodeTiled failed (%d) for %llux%llu ld=%llu box %ux%u", (int)r,
@@ -811,7 +818,13 @@ static int make_map(CUtensorMap *m, int dtype, const void *base, uint64_t cols, 
   return 0;
 }
 
-static int sk_maxseg(int64_t items, int grid, int per_group) {
+static int make_map(CUtensorMap *m, int dtype, const void *base, uint64_t cols, uint64_t rows,
+                    uint64_t ld, uint32_t box_cols, uint32_t box_rows, bool swizzle) {
+  return make_tmap(m, dtype == SNX_F64, base, cols, rows, ld, box_cols, box_rows,
+                   swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
+}
+
+int sk_maxseg(int64_t items, int grid, int per_group) {
   const int64_t per = items / grid > 0 ? items / grid : 1;
   return (int)((per_group + per - 1) / per + 1);
 }
@@ -863,6 +876,13 @@ Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K) {
   w.loss_part = take((size_t)(g.row_blocks + 1) * 8);
   w.corr_part = take((size_t)(g.row_blocks + 1) * 8);
   w.dot_part = take((size_t)4 * kDotBlocks * 8);
+  if (dtype == SNX_F32) {  // tensor-core Hessian product (snx_tc.cu)
+    const TcGeometry t = tc_geometry(nrows, P);
+    w.tc_b = take((size_t)32 * P * 4);
+    w.tc_ut = take((size_t)32 * round_up((size_t)nr, 4) * 4);
+    w.tc_zp = take((size_t)(t.row_blocks > 0 ? t.row_blocks : 1) * t.maxseg1 * 128 * K * 8);
+    w.tc_gp = take((size_t)t.col_tiles * t.maxseg2 * K * 128 * 8);
+  }
   w.total = off;
   return w;
 }
@@ -916,7 +936,7 @@ static int launch_gemm2(const G2Args &a, int grid, cudaStream_t st) {
     default: break;                                   \
   }
 
-static int validate(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+int validate(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
                     int32_t K, void *ws, size_t ws_bytes) {
   if (dtype != SNX_F64 && dtype != SNX_F32) {
     set_error("snx: unknown dtype %d", dtype);
@@ -1053,7 +1073,7 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   return check_launch("finalize");
 }
 
-static int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels,
+int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels,
                   const int64_t *rows, int64_t nrows, void *dst, int64_t ldd,
                   int32_t *labels_out, cudaStream_t st) {
   if (nrows == 0) return 0;

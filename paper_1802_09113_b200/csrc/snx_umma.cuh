@@ -1,0 +1,129 @@
+// tcgen05 (5th-generation tensor core) building blocks for sm_100a: TMEM
+// allocation, shared-memory matrix descriptors, the kind::tf32 instruction
+// descriptor, MMA issue / commit and TMEM -> register loads.
+//
+// Descriptor bit layouts follow the sm_100 UMMA encoding:
+//   smem descriptor: [0,14) start>>4, [16,30) LBO>>4, [32,46) SBO>>4,
+//                    [46,48) version = 1, [49,52) base offset, [61,64) layout
+//                    (2 = 128-byte swizzle);
+//   instr descriptor: [4,6) D format (1 = f32), [7,10) A format, [10,13) B
+//                    format (2 = tf32), bit 15 / 16 A / B MN-major,
+//                    [17,23) N>>3, [24,29) M>>4.
+// Canonical 128-byte-swizzle layouts (16-byte units):
+//   K-major : ((8 rows, n),(8 chunks)) : ((8, SBO),(1)) -- rows of 128 B, 8-row
+//             atoms SBO apart; the K step of one MMA (32 B) advances `start`.
+//   MN-major (tf32 admits only the 32-byte-atom variant, layout type 1):
+//             ((8 chunks, n),(4 rows, k)) : ((1, LBO),(8, SBO)) -- 128 B of
+//             MN-contiguous elements per K row, 32-element MN blocks LBO apart,
+//             4-row K groups SBO apart.
+// Verified on B200 by tools/umma_test.cu (hardware truncates tf32 operands)
+// and tools/tma_swz_test.cu (TMA swizzle patterns).
+#pragma once
+#include <cstdint>
+
+namespace snx {
+namespace umma {
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((saddr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>((lbo >> 4) & 0x3FFF) << 16;
+  d |= static_cast<uint64_t>((sbo >> 4) & 0x3FFF) << 32;
+  d |= static_cast<uint64_t>(1) << 46;  // version (sm_100)
+  d |= static_cast<uint64_t>(2) << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// K-major operand, rows of 128 B (32 tf32), 8-row atoms packed 1 KB apart.
+__device__ __forceinline__ uint64_t desc_k_sw128(uint32_t saddr) {
+  return desc_sw128(saddr, 16, 1024);
+}
+
+// MN-major tf32 operand in the 128-byte swizzle with 32-byte atomicity
+// (UMMA layout type 1 = TMA CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B: 16-B chunk
+// pairs XOR (row & 3)): 128 B of MN-contiguous elements per K row, 4-row K
+// groups 512 B apart, 32-element MN blocks `lbo` bytes apart.
+__device__ __forceinline__ uint64_t desc_mn_sw128_32b(uint32_t saddr, uint32_t lbo) {
+  uint64_t d = desc_sw128(saddr, lbo, 512);
+  d &= ~(static_cast<uint64_t>(7) << 61);
+  return d | (static_cast<uint64_t>(1) << 61);
+}
+
+// kind::tf32, f32 accumulate, M x N tile.
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                         uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Arrive on an mbarrier once all previously issued MMAs of this thread finish.
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+// One full warp: allocate `ncols` TMEM columns (power of 2, >= 32); the base
+// address is written to *slot (shared memory).
+__device__ __forceinline__ void tmem_alloc(uint32_t* slot, uint32_t ncols) {
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                   smem_u32(slot)),
+               "r"(ncols)
+               : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_dealloc(uint32_t base, uint32_t ncols) {
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(base), "r"(ncols)
+               : "memory");
+}
+
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+
+// Generic-proxy shared-memory writes -> visible to the tensor core (async proxy).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
+
+// Warp-collective: thread i of the warp reads 16 consecutive 32-bit columns of
+// TMEM lane (lane_base + i) starting at column `col` of `taddr`.
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// tf32 split: hi keeps the top 10 mantissa bits (exactly representable), lo the rest.
+__device__ __forceinline__ float tf32_hi(float x) {
+  return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+}
+
+}  // namespace umma
+}  // namespace snx

@@ -169,6 +169,10 @@ class HessBuffers:
         self.xs = torch.empty((mm, base.ld), dtype=base.X.dtype, device=dev) if gathered \
             else base.X
         self.h = torch.empty((mm, base.K), dtype=base.X.dtype, device=dev)
+        # f32: low tf32 parts of the sample rows for the tensor-core product
+        self.xs_lo = torch.empty((mm if gathered else base.X.shape[0], base.ld),
+                                 dtype=torch.float32, device=dev) \
+            if base.code == _lib.F32 else None
         self.owner = None
         self.graphs = {}
 

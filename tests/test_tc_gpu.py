@@ -1,0 +1,71 @@
+"""Tensor-core (tcgen05 kind::tf32, 3xTF32) Hessian product of the f32 path
+against the fp64 oracle: ragged row / column counts around the 128-row,
+32-column and 128-column tile edges, every class count K = 1..16, sampled
+and unsampled operators, bit-identical reruns."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_1802_09113_b200 as snx
+from conftest import rel_err
+
+pytestmark = pytest.mark.gpu
+
+# the declared f32 bar is 1e-4; the split products land near f32 rounding
+TOL_TC = 2e-5
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+@pytest.mark.parametrize("n,p,C", [(1, 1, 2), (127, 33, 3), (128, 32, 17), (129, 100, 10),
+                                   (1000, 257, 7), (3001, 130, 5), (4097, 784, 16),
+                                   (2500, 3072, 10)])
+def test_tc_hess_apply_vs_oracle(n, p, C):
+    A, y = oracle.synthetic_problem(n, p, C, seed=n + p)
+    rng = np.random.default_rng(n)
+    x = 0.2 * rng.standard_normal((C - 1) * p)
+    v = rng.standard_normal((C - 1) * p)
+    ds = snx.DeviceDataset.from_numpy(A, y, C, dtype="f32")
+    lam = 1e-3
+    op = snx.HessianOperator(ds, x, lam, scale=1.7)
+    assert op._bufs.xs_lo is not None  # the tensor-core path is the one under test
+    h = oracle.hess_probs(A, y, C, x)
+    ref = oracle.hess_apply(A, h, C, v, 1.7, lam)
+    got = op.apply(v)
+    assert rel_err(got, ref) <= TOL_TC, rel_err(got, ref)
+    assert np.array_equal(op.apply(v), got)  # fixed-order reductions
+
+
+@pytest.mark.parametrize("frac", [0.05, 0.3])
+def test_tc_sampled_operator(frac):
+    n, p, C = 6000, 300, 10
+    A, y = oracle.synthetic_problem(n, p, C, seed=5)
+    x = 0.1 * np.random.default_rng(1).standard_normal((C - 1) * p)
+    v = np.random.default_rng(2).standard_normal((C - 1) * p)
+    prob = snx.SoftmaxProblem(snx.DeviceDataset.from_numpy(A, y, C, dtype="f32"), 1e-3)
+    orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, frac, seed=4), 3)
+    s_h = orc.s_h
+    h = oracle.hess_probs(A[s_h], y[s_h], C, x)
+    ref = oracle.hess_apply(A[s_h], h, C, v, n / len(s_h), 1e-3)
+    assert rel_err(orc.hessian_operator(x).apply(v), ref) <= TOL_TC
+
+
+def test_tc_cg_graph_matches_oracle_cg():
+    n, p, C = 5000, 200, 10
+    A, y = oracle.synthetic_problem(n, p, C, seed=8)
+    x = 0.05 * np.random.default_rng(1).standard_normal((C - 1) * p)
+    prob = snx.SoftmaxProblem(snx.DeviceDataset.from_numpy(A, y, C, dtype="f32"), 1e-3)
+    orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, 0.1, seed=0), 0)
+    g = oracle.grad(A, y, C, x, 1e-3)
+    rep = snx.cg_solve(orc.hessian_operator(x), g, snx.CgConfig(1e-4, 10))
+    s_h = orc.s_h
+    h = oracle.hess_probs(A[s_h], y[s_h], C, x)
+    ref = oracle.cg(lambda u: oracle.hess_apply(A[s_h], h, C, u, n / len(s_h), 1e-3), g,
+                    1e-4, 10)
+    assert rel_err(rep.solution, ref[0]) <= 1e-3  # CG amplifies the 1e-5 product error
