@@ -57,7 +57,7 @@ __host__ __device__ constexpr size_t cround(size_t x, size_t a) { return (x + a 
 // Optional per-CTA timeline (compile with -DSNX_TIMELINE; tools/timeline.py):
 // globaltimer stamps at kernel entry, first data ready, last item done, exit.
 #ifdef SNX_TIMELINE
-__device__ unsigned long long g_timeline[3][160][4];
+__device__ unsigned long long g_timeline[3][160][8];
 #define SNX_TL(slot, ev)                                                   \
   do {                                                                     \
     unsigned long long t_;                                                 \
@@ -198,17 +198,18 @@ struct G1Args {
 };
 
 // Per-row softmax algebra on the summed logits z (softmax.py:85-99 and the
-// mode-specific lines); returns the row loss / correct flag.
+// mode-specific lines); returns the row loss / correct flag.  hw: the row's
+// probabilities (kHessApply), y: its label (objective / gradient), both
+// loaded by the caller ahead of the segment sums.
 template <typename T, int K>
 __device__ __forceinline__ void row_epilogue(const G1Args &a, int64_t r, const double (&z)[K],
-                                             double &loss, unsigned long long &corr) {
+                                             const double (&hw)[K], int y, double &loss,
+                                             unsigned long long &corr) {
   if (a.mode == kHessApply) {
     // softmax.py:206-208: VW = V*W; U = VW - W*rowsum(VW)
-    const T *h = static_cast<const T *>(a.H) + r * K;
-    double hw[K], vw[K], s = 0.0;
+    double vw[K], s = 0.0;
 #pragma unroll
     for (int c = 0; c < K; ++c) {
-      hw[c] = (double)h[c];
       vw[c] = z[c] * hw[c];
       s += vw[c];
     }
@@ -234,7 +235,6 @@ __device__ __forceinline__ void row_epilogue(const G1Args &a, int64_t r, const d
     for (int c = 0; c < K; ++c) h[c] = (T)(E[c] / alpha);
     return;
   }
-  const int y = a.labels[r];
   double lin = 0.0;
 #pragma unroll
   for (int c = 0; c < K; ++c)
@@ -262,37 +262,64 @@ __device__ __forceinline__ void row_epilogue(const G1Args &a, int64_t r, const d
   }
 }
 
-// Epilogue of row block rb by the CTA that delivered its last segment: 2
-// consumer threads per row sum the CTA segments (fixed order), then the row
-// algebra; loss / correct counts reduce per row block and, by the CTA that
-// finishes the last row block, over all row blocks (fixed order).
+// Fixed-order sum over segments of kPer strided elements per thread: loads of
+// up to kBatch segments are issued together (one L2 round trip per batch),
+// then added in segment order -- the same rounding as a sequential sum.
+template <int kPer, int kBatch>
+__device__ __forceinline__ void segment_sums(const double *base, int64_t seg_stride, int nseg,
+                                             int tid, int stride, int nvalid,
+                                             double (&acc)[kPer]) {
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) acc[q] = 0.0;
+  for (int s0 = 0; s0 < nseg; s0 += kBatch) {
+    double v[kBatch][kPer];
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b)
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * stride;
+        v[b][q] = (s0 + b < nseg && e < nvalid) ? __ldcg(base + (int64_t)(s0 + b) * seg_stride + e)
+                                                : 0.0;
+      }
+#pragma unroll
+    for (int b = 0; b < kBatch; ++b)
+#pragma unroll
+      for (int q = 0; q < kPer; ++q)
+        if (s0 + b < nseg) acc[q] += v[b][q];
+  }
+}
+
+// Epilogue of row block rb by the CTA that delivered its last segment: the
+// consumer threads sum the CTA segments (fixed order), then one thread per
+// row runs the row algebra; loss / correct counts reduce per row block and,
+// by the CTA that finishes the last row block, over all row blocks (fixed order).
 template <typename T, int K>
 __device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, double *zsum,
                                             double *shd, unsigned long long *shu, int *flag) {
   const int tid = threadIdx.x;
   const int nrows = (int)min((int64_t)kRB, a.nrows - rb * kRB);
-  // 1) segment sums: element e = row*K + c, all segment loads independent and
-  //    coalesced, summed in segment order
+  const int64_t r = rb * kRB + tid;
+  // row inputs first: their latency overlaps the segment loads
+  double hw[K];
+  int y = -1;
+  if (tid < nrows) {
+    if (a.mode == kHessApply) {
+      const T *h = static_cast<const T *>(a.H) + r * K;
+#pragma unroll
+      for (int c = 0; c < K; ++c) hw[c] = (double)h[c];
+    } else if (a.mode != kHessPrep) {
+      y = a.labels[r];
+    }
+  }
+  // 1) segment sums: element e = row*K + c
   {
     const int c_lo = sk_owner(a.items, G, rb * a.nchunks);
     const int nseg = sk_owner(a.items, G, (rb + 1) * a.nchunks - 1) - c_lo + 1;
     const double *zb = a.zp + rb * a.maxseg * (int64_t)kRB * K;
     constexpr int kPer = (kRB * K + kConsumers - 1) / kConsumers;
     double acc[kPer];
-#pragma unroll
-    for (int q = 0; q < kPer; ++q) acc[q] = 0.0;
-    for (int sg = 0; sg < nseg; sg += 2) {
-      double v0[kPer], v1[kPer];
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const int e = tid + q * kConsumers;
-        const bool ok = e < nrows * K;
-        v0[q] = ok ? __ldcg(zb + (int64_t)sg * kRB * K + e) : 0.0;
-        v1[q] = (ok && sg + 1 < nseg) ? __ldcg(zb + (int64_t)(sg + 1) * kRB * K + e) : 0.0;
-      }
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) acc[q] = (acc[q] + v0[q]) + v1[q];
-    }
+    segment_sums<kPer, (kPer <= 4 ? 8 : 4)>(zb, (int64_t)kRB * K, nseg, tid, kConsumers,
+                                            nrows * K, acc);
 #pragma unroll
     for (int q = 0; q < kPer; ++q) {
       const int e = tid + q * kConsumers;
@@ -307,7 +334,7 @@ __device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, 
     double z[K];
 #pragma unroll
     for (int c = 0; c < K; ++c) z[c] = zsum[tid * K + c];
-    row_epilogue<T, K>(a, rb * kRB + tid, z, loss, corr);
+    row_epilogue<T, K>(a, r, z, hw, y, loss, corr);
   }
   if (tid == 0) a.rb_count[rb] = 0u;  // rest state for the next launch
   if (a.mode != kObjective && a.mode != kGradient) return;
@@ -445,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
         zb[t] = z;
       }
       consumer_sync(kConsumers);  // segment written; red free again
+      if (i == i1 && tid == 0) SNX_TL(0, 4);
       // resolve the previous arrival, publish this one (release), and on the
       // final flush also resolve this one
       if (tid == 0) {
@@ -458,10 +486,12 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
         pend_prev = atomic_add_acq_rel(&a.rb_count[frb], 1u);  // release our segment
       }
       consumer_sync(kConsumers);
+      if (i == i1 && tid == 0) SNX_TL(0, 5);
       for (int pass = 0; pass < 2; ++pass) {
         if (epi_rb >= 0) {  // the acq_rel arrival already acquired the other segments
           block_epilogue<T, K>(a, epi_rb, G, red, shd, shu, &flag);
           consumer_sync(kConsumers);
+          if (i == i1 && tid == 0) SNX_TL(0, 6 + pass);
         }
         if (i != i1 || pass == 1) break;
         // final flush: wait for this CTA's own arrival and resolve it too
@@ -522,7 +552,57 @@ struct G2Args {
   const void *U;   // nrows rows of KP (padded) elements, X dtype
   double *gp;      // [col_tiles][maxseg][K][TCOL] segment partials
   const double *skip;
+  // fused finalize (by the last segment to arrive for a column tile)
+  unsigned *tile_count;  // [col_tiles] arrivals (zero at rest)
+  int col_tiles;
+  int p;
+  double scale, lam;
+  const double *base;    // v (Hessian) / w (gradient)
+  double *out;           // scale * X^T U + lam * base, flat class-major
+  double *dots;          // nullable: [tile] partials of base.out, [kDotBlocks + tile] of base.base
 };
+
+// out[c*p + j] = scale * sum_seg gp[tile][seg][c][jj] + lam * base[c*p + j] for
+// the columns j of one tile, the segments summed in CTA order (numpy rounding:
+// two products, one add), plus the tile's partials of base.out and base.base
+// (the CG curvature test; tile 0 zeroes the unused partial slots).
+template <int K, int TCOL>
+__device__ __noinline__ void tile_finalize(const G2Args &a, int tile, int G, double *shd) {
+  const int tid = threadIdx.x;
+  const int c_lo = sk_owner(a.items, G, (int64_t)tile * a.rchunks);
+  const int nseg = sk_owner(a.items, G, (int64_t)(tile + 1) * a.rchunks - 1) - c_lo + 1;
+  constexpr int kPer = (K * TCOL + kConsumers - 1) / kConsumers;
+  double acc[kPer];
+  segment_sums<kPer, (kPer <= 4 ? 8 : 4)>(a.gp + (int64_t)tile * a.maxseg * K * TCOL,
+                                          (int64_t)K * TCOL, nseg, tid, kConsumers, K * TCOL,
+                                          acc);
+  double bo = 0.0, bb = 0.0;
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int e = tid + q * kConsumers;
+    const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
+    if (e < K * TCOL && j < a.p) {
+      const int64_t i = (int64_t)c * a.p + j;
+      const double b = a.base[i];
+      const double o = __dadd_rn(__dmul_rn(a.scale, acc[q]), __dmul_rn(a.lam, b));
+      a.out[i] = o;
+      bo += b * o;
+      bb += b * b;
+    }
+  }
+  if (a.dots == nullptr) return;
+  const double so = consumer_sum(bo, shd);
+  const double sb = consumer_sum(bb, shd);
+  if (tid == 0) {
+    a.dots[tile] = so;
+    a.dots[kDotBlocks + tile] = sb;
+  }
+  if (tile == 0)
+    for (int t = a.col_tiles + tid; t < kDotBlocks; t += kConsumers) {
+      a.dots[t] = 0.0;
+      a.dots[kDotBlocks + t] = 0.0;
+    }
+}
 
 template <typename T, int K>
 __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constant__ G2Args a) {
@@ -553,6 +633,8 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
   if (i0 == i1) return;
   const int tile0 = (int)(i0 / a.rchunks);
   const int rc0 = (int)(i0 - (int64_t)tile0 * a.rchunks);
+  __shared__ double shd[kWarps];
+  __shared__ int last_tile;
 
   if (warp == kWarps) {
     // ------------------------------------------------ producer warp (TMA)
@@ -612,11 +694,25 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
 #pragma unroll
         for (int c = 0; c < K; ++c) acc[v][c] = T(0);
       consumer_sync(kConsumers);
-      const int seg = cta - sk_owner(a.items, G, (int64_t)ftile * a.rchunks);
-      double *gb = a.gp + ((int64_t)ftile * a.maxseg + seg) * K * TCOL;
+      const int c_lo = sk_owner(a.items, G, (int64_t)ftile * a.rchunks);
+      double *gb = a.gp + ((int64_t)ftile * a.maxseg + (cta - c_lo)) * K * TCOL;
       for (int t = tid; t < K * TCOL; t += kConsumers)
         gb[t] = ((red[t] + red[K * TCOL + t]) + red[2 * K * TCOL + t]) + red[3 * K * TCOL + t];
-      consumer_sync(kConsumers);  // red free again
+      consumer_sync(kConsumers);  // segment written; red free again
+      if (i == i1 && tid == 0) SNX_TL(1, 4);
+      if (tid == 0) {
+        const int nseg = sk_owner(a.items, G, (int64_t)(ftile + 1) * a.rchunks - 1) - c_lo + 1;
+        const unsigned prev = atomic_add_acq_rel(&a.tile_count[ftile], 1u);  // publish / acquire
+        last_tile = prev == (unsigned)(nseg - 1);
+        if (last_tile) a.tile_count[ftile] = 0u;  // rest state for the next launch
+      }
+      consumer_sync(kConsumers);
+      if (i == i1 && tid == 0) SNX_TL(1, 5);
+      if (last_tile) {
+        tile_finalize<K, TCOL>(a, ftile, G, shd);
+        consumer_sync(kConsumers);
+        if (i == i1 && tid == 0) SNX_TL(1, 6);
+      }
     }
     if (i == i1) {
       if (tid == 0) SNX_TL(1, 3);
@@ -670,6 +766,7 @@ __global__ void __launch_bounds__(kDotThreads)
                     const double *skip) {
   pdl_wait();  // successor launches when this grid exits (implicit trigger)
   if (skip != nullptr && *skip != 0.0) return;
+  if (threadIdx.x == 0) SNX_TL(2, 0);
   __shared__ double sh[kDotThreads / 32];
   double bo = 0.0, bb = 0.0;
   const int64_t d = (int64_t)K * p;
@@ -706,6 +803,7 @@ __global__ void __launch_bounds__(kDotThreads)
       dots[kDotBlocks + blockIdx.x] = sb;
     }
   }
+  if (threadIdx.x == 0) SNX_TL(2, 3);
 }
 
 // out = lam * base (the empty dataset: every data term vanishes), with the
@@ -1061,16 +1159,20 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   b.U = rowbuf;
   b.gp = reinterpret_cast<double *>(wsb + lay.gp);
   b.skip = skip;
+  b.tile_count = counters + 16;  // [col_tiles <= kMaxTiles]
+  b.col_tiles = g.col_tiles;
+  b.p = p;
+  b.scale = scale;
+  b.lam = lam;
+  b.base = base;
+  b.out = vec_out;
+  b.dots = dots;
   if (dtype == SNX_F64) {
     SNX_K_SWITCH(K, (rc = launch_gemm2<double, KK>(b, g.grid2, st)));
   } else {
     SNX_K_SWITCH(K, (rc = launch_gemm2<float, KK>(b, g.grid2, st)));
   }
-  if (rc) return rc;
-  launch_pdl(finalize_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, b.gp, g.g2_items, g.grid2, g.rchunks,
-                                                      g.g2_maxseg, g.tcol, K, p, scale, lam,
-                                                      base, vec_out, dots, skip);
-  return check_launch("finalize");
+  return rc;
 }
 
 int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels,

@@ -34,6 +34,20 @@ namespace snx {
 int make_tmap(CUtensorMap *m, bool f64, const void *base, uint64_t cols, uint64_t rows,
               uint64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz);
 
+#ifdef SNX_TIMELINE
+__device__ unsigned long long g_tc_timeline[2][160][4];
+#define SNX_TC_TL(slot, ev)                                                \
+  do {                                                                     \
+    unsigned long long t_;                                                 \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+    if (blockIdx.x < 160) g_tc_timeline[slot][blockIdx.x][ev] = t_;       \
+  } while (0)
+#else
+#define SNX_TC_TL(slot, ev) \
+  do {                      \
+  } while (0)
+#endif
+
 namespace {
 
 constexpr int kThreads = 192;
@@ -137,6 +151,8 @@ __device__ __forceinline__ void acc_take(Barriers &b, int n, int warp, int lane,
 template <bool kAmn, typename SegStart, typename SegEnd>
 __device__ __forceinline__ void mma_loop(Barriers &b, uint8_t *sm, int64_t i0, int64_t i1,
                                          SegStart seg_start, SegEnd seg_end) {
+  constexpr int slot = kAmn ? 1 : 0;
+  (void)slot;
   constexpr uint32_t id32 = umma::idesc_tf32(128, 32, kAmn, false);
   constexpr uint32_t id16 = umma::idesc_tf32(128, 16, kAmn, false);
   int nseg = 0;
@@ -150,6 +166,7 @@ __device__ __forceinline__ void mma_loop(Barriers &b, uint8_t *sm, int64_t i0, i
     const int s = (int)(it % kS);
     mbar_wait(&b.full[s], (unsigned)((it / kS) & 1));
     umma::fence_after();
+    if (it == 0) SNX_TC_TL(slot, 1);
     const uint32_t st = umma::smem_u32(sm + s * kStage);
     const uint32_t d = b.tbase + (uint32_t)(buf * 32);
 #pragma unroll
@@ -172,6 +189,7 @@ __device__ __forceinline__ void mma_loop(Barriers &b, uint8_t *sm, int64_t i0, i
       ++nseg;
     }
   }
+  SNX_TC_TL(slot, 2);
 }
 
 // ---------------------------------------------------------------- GEMM1
@@ -185,6 +203,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm1_kernel(const __grid_cons
   const int G = gridDim.x, cta = blockIdx.x;
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;
+  if (tid == 0) SNX_TC_TL(0, 0);
   setup(b, warp);
   const int nk = a.nk;
 
@@ -260,6 +279,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm1_kernel(const __grid_cons
       }
       epi_sync();
     }
+    if (et == 0) SNX_TC_TL(0, 3);
   }
   teardown(b, warp);
 }
@@ -275,6 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm2_kernel(const __grid_cons
   const int G = gridDim.x, cta = blockIdx.x;
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;
+  if (tid == 0) SNX_TC_TL(1, 0);
   setup(b, warp);
   const int rch = a.rchunks;
 
@@ -314,6 +335,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm2_kernel(const __grid_cons
 #pragma unroll
       for (int c = 0; c < K; ++c) g[c * 128] = (double)v0[c] + (double)v1[c];
     }
+    if (tid == 64) SNX_TC_TL(1, 3);
   }
   teardown(b, warp);
 }
@@ -459,6 +481,13 @@ static int tc_apply(const float *Xs, const float *Xlo, int64_t ldx, int64_t nrow
 using namespace snx;
 
 extern "C" {
+
+#ifdef SNX_TIMELINE
+int snx_debug_tc_timeline(unsigned long long *host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_tc_timeline, sizeof(g_tc_timeline)) == cudaSuccess ? 0
+                                                                                             : 1;
+}
+#endif
 
 int snx_hess_prepare_tc(const float *X, int64_t ldx, const int64_t *rows, int64_t nrows,
                         int32_t p, int32_t K, const double *w, float *Xs_out, float *Xlo_out,

@@ -174,6 +174,20 @@ __global__ void __launch_bounds__(kDotThreads)
   }
 }
 
+#ifdef SNX_TIMELINE
+__device__ unsigned long long g_vec_timeline[2][256][2];
+#define SNX_VTL(slot, ev)                                              \
+  do {                                                                 \
+    unsigned long long t_;                                             \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));             \
+    g_vec_timeline[slot][blockIdx.x][ev] = t_;                         \
+  } while (0)
+#else
+#define SNX_VTL(slot, ev) \
+  do {                    \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------ CG (cg.py)
 // slot layout (SNX_CG_SLOT doubles)
 enum { kRs = 0, kBest = 1, kDone = 2, kIters = 3, kConv = 4, kThr = 5, kErr = 6, kCurv = 7 };
@@ -229,6 +243,7 @@ __global__ void __launch_bounds__(kDotThreads)
                     const double *__restrict__ dots, double *r, const double *s, double *p,
                     double *state) {
   pdl_wait();  // successor launches when this grid exits (implicit trigger)
+  if (threadIdx.x == 0) SNX_VTL(0, 0);
   const double *st = slot(state, t);
   if (st[kDone] != 0.0) return;
   __shared__ double sh[kDotThreads / 32];
@@ -259,6 +274,7 @@ __global__ void __launch_bounds__(kDotThreads)
   }
   const double b = block_sum<kDotThreads>(acc, sh);
   if (threadIdx.x == 0) scratch(state, max_iters)[blockIdx.x] = b;
+  if (threadIdx.x == 0) SNX_VTL(0, 1);
 }
 
 // Iteration t, part 2 (cg.py:87-96): best-iterate copy, stop test, new direction.
@@ -266,6 +282,7 @@ __global__ void __launch_bounds__(kDotThreads)
     cg_step2_kernel(int t, int max_iters, int64_t d, const double *__restrict__ r, double *s,
                     const double *__restrict__ p, double *pb, double *state) {
   pdl_wait();  // successor launches when this grid exits (implicit trigger)
+  if (threadIdx.x == 0) SNX_VTL(1, 0);
   const double *st = slot(state, t);
   double *nx = slot(state, t + 1);
   if (st[kDone] != 0.0) {
@@ -307,6 +324,7 @@ __global__ void __launch_bounds__(kDotThreads)
     nx[kIters] = t + 1;
     nx[kDone] = (conv || t + 1 >= max_iters) ? 1.0 : 0.0;
   }
+  if (threadIdx.x == 0) SNX_VTL(1, 1);
 }
 
 template <typename T>
@@ -326,6 +344,14 @@ __global__ void pack_rows_kernel(const double *__restrict__ src, int64_t nrows, 
 using namespace snx;
 
 extern "C" {
+
+#ifdef SNX_TIMELINE
+int snx_debug_vec_timeline(unsigned long long *host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_vec_timeline, sizeof(g_vec_timeline)) == cudaSuccess
+             ? 0
+             : 1;
+}
+#endif
 
 int snx_abi_version(void) { return SNX_ABI_VERSION; }
 

@@ -22,7 +22,9 @@ def _need_cuda():
         pytest.skip("no CUDA device")
 
 
-def test_world1_sharded_newton_is_bit_identical():
+def test_world1_sharded_newton_matches_unsharded():
+    # same kernels; only the CG curvature dot is reduced in a different fixed
+    # order (snx_finish_hv's 256 blocks vs the GEMM2 tile partials)
     A, y = oracle.synthetic_problem(3000, 40, 7, seed=21)
     cfg = snx.make_variant("subsampled-20", snx.NewtonConfig(max_outer_iters=5))
     ds = snx.DeviceDataset.from_numpy(A, y, 7)
@@ -30,9 +32,12 @@ def test_world1_sharded_newton_is_bit_identical():
     sp = sd.ShardedProblem.from_global(A, y, 7, 1e-3)
     got = sd.newton_solve_sharded(sp, cfg)
     assert got.reason == ref.reason
-    assert np.array_equal(got.x_final, ref.x_final)
-    assert [r.objective for r in got.records] == [r.objective for r in ref.records]
-    assert [r.cg_iters for r in got.records] == [r.cg_iters for r in ref.records]
+    assert rel_err(got.x_final, ref.x_final) <= 1e-12
+    for a, b in zip(got.records, ref.records):
+        assert abs(a.objective - b.objective) <= 1e-13 * abs(b.objective)
+        assert a.cg_iters == b.cg_iters and a.step_size == b.step_size
+    got2 = sd.newton_solve_sharded(sp, cfg)
+    assert np.array_equal(got2.x_final, got.x_final)  # deterministic
 
 
 def test_two_shards_sum_to_full():

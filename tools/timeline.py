@@ -27,12 +27,17 @@ for _ in range(5):
 torch.cuda.synchronize()
 op.apply_into(g, out)
 torch.cuda.synchronize()
-buf = (ctypes.c_ulonglong * (3 * 160 * 4))()
+buf = (ctypes.c_ulonglong * (3 * 160 * 8))()
 lib = _lib.load()
-assert lib.snx_debug_timeline(buf) == 0
-t = np.frombuffer(buf, dtype=np.uint64).reshape(3, 160, 4).astype(np.int64)
+if ds.dtype == "f32":  # tensor-core kernels (snx_tc.cu)
+    assert lib.snx_debug_tc_timeline(buf) == 0
+    t = np.frombuffer(buf, dtype=np.uint64)[:2 * 160 * 4].reshape(2, 160, 4).astype(np.int64)
+else:
+    assert lib.snx_debug_timeline(buf) == 0
+    t = np.frombuffer(buf, dtype=np.uint64).reshape(3, 160, 8).astype(np.int64)
 for k, name in enumerate(["gemm1", "gemm2"]):
     tt = t[k, :148]
+    tt = tt[tt[:, 0] > 0]
     base = tt[:, 0].min()
     rel = (tt - base) / 1e3
     print(f"{name}: entry   min/med/max {rel[:,0].min():7.2f} {np.median(rel[:,0]):7.2f} {rel[:,0].max():7.2f} us")
