@@ -86,4 +86,24 @@ __device__ __forceinline__ double warp_sum_partials(const double *a) {
   return warp_allsum(t);
 }
 
+// The same, reading through L2 (partials written by other CTAs of a running
+// persistent kernel).
+__device__ __forceinline__ double warp_sum_partials_cg(const double *a) {
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < kDotBlocks / 32; ++i) t += __ldcg(a + lane + 32 * i);
+  return warp_allsum(t);
+}
+
+// CG state slot layout (SNX_CG_SLOT doubles per iteration)
+enum { kRs = 0, kBest = 1, kDone = 2, kIters = 3, kConv = 4, kThr = 5, kErr = 6, kCurv = 7 };
+
+__device__ __forceinline__ double *slot(double *state, int t) { return state + t * SNX_CG_SLOT; }
+
+// scratch after the slots: [0, B) g.g / r.r partials
+__device__ __forceinline__ double *scratch(double *state, int max_iters) {
+  return state + (max_iters + 2) * SNX_CG_SLOT;
+}
+
 }  // namespace snx

@@ -50,7 +50,7 @@ constexpr int kG2Rows = 32;                  // rows per GEMM2 item
 constexpr int kMaxTiles = kDotBlocks;
 constexpr size_t kSmemBudget = 220 * 1024;
 constexpr int64_t kMaxRowBlocks = 1 << 17;   // 12.5M rows per call
-constexpr int kCounterWords = 16 + kMaxTiles + kMaxRowBlocks;
+constexpr int kCounterWords = 16 + kMaxTiles + 2 * kMaxRowBlocks;  // + u_ready flags
 
 __host__ __device__ constexpr size_t cround(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -64,7 +64,17 @@ __device__ unsigned long long g_timeline[3][160][8];
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
     if (blockIdx.x < 160) g_timeline[slot][blockIdx.x][ev] = t_;          \
   } while (0)
+__device__ unsigned long long g_cg_timeline[160][10];
+#define SNX_CTL(ev)                                                        \
+  do {                                                                     \
+    unsigned long long t_;                                                 \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
+    if (blockIdx.x < 160) g_cg_timeline[blockIdx.x][ev] = t_;             \
+  } while (0)
 #else
+#define SNX_CTL(ev) \
+  do {              \
+  } while (0)
 #define SNX_TL(slot, ev) \
   do {                   \
   } while (0)
@@ -195,6 +205,7 @@ struct G1Args {
   double *loss_out;
   long long *corr_out;
   const double *skip;
+  unsigned *u_ready;   // persistent CG kernel: publish U rows of a row block (epoch)
 };
 
 // Per-row softmax algebra on the summed logits z (softmax.py:85-99 and the
@@ -295,7 +306,8 @@ __device__ __forceinline__ void segment_sums(const double *base, int64_t seg_str
 // by the CTA that finishes the last row block, over all row blocks (fixed order).
 template <typename T, int K>
 __device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, double *zsum,
-                                            double *shd, unsigned long long *shu, int *flag) {
+                                            double *shd, unsigned long long *shu, int *flag,
+                                            unsigned epoch) {
   const int tid = threadIdx.x;
   const int nrows = (int)min((int64_t)kRB, a.nrows - rb * kRB);
   const int64_t r = rb * kRB + tid;
@@ -337,6 +349,12 @@ __device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, 
     row_epilogue<T, K>(a, r, z, hw, y, loss, corr);
   }
   if (tid == 0) a.rb_count[rb] = 0u;  // rest state for the next launch
+  if (a.u_ready != nullptr) {  // publish this row block's U rows (release)
+    consumer_sync(kConsumers);
+    if (tid == 0)
+      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(a.u_ready + rb), "r"(epoch)
+                   : "memory");
+  }
   if (a.mode != kObjective && a.mode != kGradient) return;
   const double bl = consumer_sum(loss, shd);
   const unsigned long long bc = consumer_sum_u64(corr, shu);
@@ -362,31 +380,19 @@ __device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, 
   }
 }
 
-template <typename T, int K>
-__global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constant__ G1Args a) {
-  pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
-  pdl_wait();
-  if (a.skip != nullptr && *a.skip != 0.0) return;
+// GEMM1 work of one CTA (items of the stream-K split over G CTAs), shared by
+// gemm1_kernel and the persistent CG kernel.  itp / itc: the producer's and
+// the consumers' running stage counters of the (full, empty) ring, kept
+// across calls by the persistent kernel.
+template <typename T, int K, int S>
+__device__ __forceinline__ void gemm1_body(const G1Args &a, unsigned char *smem, double *red,
+                                           uint64_t *full, uint64_t *empty, int G, int64_t &itp,
+                                           int64_t &itc, unsigned epoch) {
   using Sh = G1Shape<T, K>;
-  constexpr int V = Sh::V, S = Sh::S;
+  constexpr int V = Sh::V;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  double *red = reinterpret_cast<double *>(smem + S * Sh::STAGE);  // [4][kRB][K]
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * Sh::STAGE + Sh::RED);
-  uint64_t *empty = full + S;
-
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWarps);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-
-  const int G = gridDim.x, cta = blockIdx.x;
-  if (tid == 0) SNX_TL(0, 0);
+  const int cta = blockIdx.x;
+  if (cta >= G) return;
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;  // more CTAs than items (the host never launches that)
   const int64_t rb0 = i0 / a.nchunks;
@@ -404,9 +410,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
       constexpr unsigned kTx = (unsigned)(Sh::NB * Sh::BOX + Sh::WBYTES);
       int64_t rb = rb0;
       int ch = ch0;
-      for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
-        const int s = (int)(it % S);
-        mbar_wait(&empty[s], (unsigned)((it / S) & 1) ^ 1u);
+      for (int64_t i = i0; i < i1; ++i, ++itp) {
+        const int s = (int)(itp % S);
+        mbar_wait(&empty[s], (unsigned)((itp / S) & 1) ^ 1u);
         mbar_arrive_expect_tx(&full[s], kTx);
         unsigned char *st = smem + s * Sh::STAGE;
         const int col = ch * Sh::CHUNK, row = (int)(rb * kRB);
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
   unsigned pend_prev = 0;
   int64_t rb = rb0;
   int ch = ch0;
-  for (int64_t i = i0, it = 0; i <= i1; ++i) {
+  for (int64_t i = i0; i <= i1; ++i) {
     if (i == i1 || (ch == 0 && i > i0)) {
       if (i == i1 && tid == 0) SNX_TL(0, 2);
       // flush the segment partial of the row block just finished: warp pairs
@@ -489,7 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
       if (i == i1 && tid == 0) SNX_TL(0, 5);
       for (int pass = 0; pass < 2; ++pass) {
         if (epi_rb >= 0) {  // the acq_rel arrival already acquired the other segments
-          block_epilogue<T, K>(a, epi_rb, G, red, shd, shu, &flag);
+          block_epilogue<T, K>(a, epi_rb, G, red, shd, shu, &flag, epoch);
           consumer_sync(kConsumers);
           if (i == i1 && tid == 0) SNX_TL(0, 6 + pass);
         }
@@ -506,9 +512,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
       if (tid == 0) SNX_TL(0, 3);
       break;
     }
-    const int s = (int)(it % S);
-    mbar_wait(&full[s], (unsigned)((it / S) & 1));
-    if (tid == 0 && it == 0) SNX_TL(0, 1);
+    const int s = (int)(itc % S);
+    mbar_wait(&full[s], (unsigned)((itc / S) & 1));
+    if (tid == 0 && i == i0) SNX_TL(0, 1);
     const unsigned char *st = smem + s * Sh::STAGE;
     const unsigned char *xa = st + box * Sh::BOX + lane * 128;
     const T *wp = reinterpret_cast<const T *>(st + Sh::NB * Sh::BOX) + warp * Sh::WC;
@@ -534,12 +540,37 @@ __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constan
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    ++it;
+    ++itc;
     if (++ch == a.nchunks) {
       ch = 0;
       ++rb;
     }
   }
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constant__ G1Args a) {
+  pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
+  pdl_wait();
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  using Sh = G1Shape<T, K>;
+  constexpr int S = Sh::S;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double *red = reinterpret_cast<double *>(smem + S * Sh::STAGE);  // [4][kRB][K]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * Sh::STAGE + Sh::RED);
+  uint64_t *empty = full + S;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) SNX_TL(0, 0);
+  int64_t itp = 0, itc = 0;
+  gemm1_body<T, K, S>(a, smem, red, full, empty, gridDim.x, itp, itc, 0u);
 }
 
 // ---------------------------------------------------------------- GEMM2
@@ -560,6 +591,7 @@ struct G2Args {
   const double *base;    // v (Hessian) / w (gradient)
   double *out;           // scale * X^T U + lam * base, flat class-major
   double *dots;          // nullable: [tile] partials of base.out, [kDotBlocks + tile] of base.base
+  const unsigned *u_ready;  // persistent CG kernel: [row_blocks] U publication epochs
 };
 
 // out[c*p + j] = scale * sum_seg gp[tile][seg][c][jj] + lam * base[c*p + j] for
@@ -583,7 +615,7 @@ __device__ __noinline__ void tile_finalize(const G2Args &a, int tile, int G, dou
     const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
     if (e < K * TCOL && j < a.p) {
       const int64_t i = (int64_t)c * a.p + j;
-      const double b = a.base[i];
+      const double b = __ldcg(a.base + i);  // may be written by other CTAs (persistent CG)
       const double o = __dadd_rn(__dmul_rn(a.scale, acc[q]), __dmul_rn(a.lam, b));
       a.out[i] = o;
       bo += b * o;
@@ -604,31 +636,30 @@ __device__ __noinline__ void tile_finalize(const G2Args &a, int tile, int G, dou
     }
 }
 
-template <typename T, int K>
-__global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constant__ G2Args a) {
-  pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
-  pdl_wait();
-  if (a.skip != nullptr && *a.skip != 0.0) return;
-  using Sh = G2Shape<T, K>;
-  constexpr int V = Sh::V, LC = Sh::LC, TCOL = Sh::TCOL, KP = Sh::KP, S = Sh::S;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  double *red = reinterpret_cast<double *>(smem + S * Sh::STAGE);  // [4][K][TCOL]
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * Sh::STAGE + Sh::RED);
-  uint64_t *empty = full + S;
-
-  if (tid == 0) {
-#pragma unroll
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kWarps);
-    }
-    mbar_fence_init();
+// Acquire a U-ready flag written by another CTA of the same kernel (the
+// persistent CG kernel), then order the TMA (async proxy) reads after it.
+__device__ __forceinline__ void wait_flag_geq(const unsigned *f, unsigned v) {
+  unsigned x;
+  for (;;) {
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(x) : "l"(f) : "memory");
+    if (x >= v) break;
+    __nanosleep(32);
   }
-  __syncthreads();
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");
+}
 
-  const int G = gridDim.x, cta = blockIdx.x;
-  if (tid == 0) SNX_TL(1, 0);
+// GEMM2 work of one CTA (see gemm1_body).  With a.u_ready set, the U rows of
+// a 32-row chunk are loaded only once their row block's epilogue has
+// published them (u_ready[rb] >= a.epoch).
+template <typename T, int K, int S>
+__device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem, double *red,
+                                           uint64_t *full, uint64_t *empty, int G, int64_t &itp,
+                                           int64_t &itc, unsigned epoch) {
+  using Sh = G2Shape<T, K>;
+  constexpr int V = Sh::V, LC = Sh::LC, TCOL = Sh::TCOL, KP = Sh::KP;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int cta = blockIdx.x;
+  if (cta >= G) return;
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;
   const int tile0 = (int)(i0 / a.rchunks);
@@ -642,15 +673,16 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
       tma_prefetch_desc(&a.xmap);
       const T *U = static_cast<const T *>(a.U);
       int tile = tile0, rc = rc0;
-      for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
+      for (int64_t i = i0; i < i1; ++i, ++itp) {
         const int64_t c0 = (int64_t)rc * kG2Rows;
         const int nr = (int)min((int64_t)kG2Rows, a.nrows - c0);
-        const int s = (int)(it % S);
-        mbar_wait(&empty[s], (unsigned)((it / S) & 1) ^ 1u);
+        const int s = (int)(itp % S);
+        mbar_wait(&empty[s], (unsigned)((itp / S) & 1) ^ 1u);
         const unsigned ub = (unsigned)(nr * KP * sizeof(T));
         mbar_arrive_expect_tx(&full[s], (unsigned)Sh::XB + ub);
         unsigned char *st = smem + s * Sh::STAGE;
         tma_load_2d(st, &a.xmap, tile * TCOL, (int)c0, &full[s]);
+        if (a.u_ready != nullptr) wait_flag_geq(a.u_ready + c0 / kRB, epoch);
         bulk_g2s(st + Sh::XB, U + c0 * KP, ub, &full[s]);
         if (++rc == a.rchunks) {
           rc = 0;
@@ -668,7 +700,7 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
 #pragma unroll
     for (int c = 0; c < K; ++c) acc[v][c] = T(0);
   int tile = tile0, rc = rc0;
-  for (int64_t i = i0, it = 0; i <= i1; ++i) {
+  for (int64_t i = i0; i <= i1; ++i) {
     if (i == i1 || (rc == 0 && i > i0)) {
       if (i == i1 && tid == 0) SNX_TL(1, 2);
       // flush the segment partial of the tile just finished: warp pairs
@@ -718,9 +750,9 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
       if (tid == 0) SNX_TL(1, 3);
       break;
     }
-    const int s = (int)(it % S);
-    mbar_wait(&full[s], (unsigned)((it / S) & 1));
-    if (tid == 0 && it == 0) SNX_TL(1, 1);
+    const int s = (int)(itc % S);
+    mbar_wait(&full[s], (unsigned)((itc / S) & 1));
+    if (tid == 0 && i == i0) SNX_TL(1, 1);
     const int nr = (int)min((int64_t)kG2Rows, a.nrows - (int64_t)rc * kG2Rows);
     const T *xs = reinterpret_cast<const T *>(smem + s * Sh::STAGE);
     const T *us = reinterpret_cast<const T *>(smem + s * Sh::STAGE + Sh::XB);
@@ -747,12 +779,37 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    ++it;
+    ++itc;
     if (++rc == a.rchunks) {
       rc = 0;
       ++tile;
     }
   }
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constant__ G2Args a) {
+  pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
+  pdl_wait();
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  using Sh = G2Shape<T, K>;
+  constexpr int S = Sh::S;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double *red = reinterpret_cast<double *>(smem + S * Sh::STAGE);  // [4][K][TCOL]
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + S * Sh::STAGE + Sh::RED);
+  uint64_t *empty = full + S;
+  if (threadIdx.x == 0) {
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) SNX_TL(1, 0);
+  int64_t itp = 0, itc = 0;
+  gemm2_body<T, K, S>(a, smem, red, full, empty, gridDim.x, itp, itc, 0u);
 }
 
 // out[c*p + j] = scale * sum_seg gp[tile][seg][c][j % TCOL] + lam * base[c*p + j]
@@ -804,6 +861,301 @@ __global__ void __launch_bounds__(kDotThreads)
     }
   }
   if (threadIdx.x == 0) SNX_TL(2, 3);
+}
+
+// ---------------------------------------------------------------- persistent CG
+// cg.py:51-98 with the Hessian product of softmax.py:197-210: the whole CG
+// solve in ONE launch of one CTA per SM (co-resident, cooperative launch).
+// Per iteration: GEMM1 items -> U rows published per row block (release
+// flag, no grid barrier: GEMM2 producers acquire the flags of the rows they
+// load, so the GEMM1 epilogues overlap the GEMM2 stream) -> GEMM2 items with
+// the fused finalize (Hs tiles + curvature partials) -> grid barrier ->
+// alpha, p / r update -> grid barrier -> beta, best copy, new direction ->
+// grid barrier.  The arithmetic (stream-K splits, segment orders, the 256
+// fixed dot partials emulated as virtual blocks) is exactly that of
+// snx_hess_apply + snx_cg_update, so results are bit-identical to the
+// multi-kernel path.
+template <typename T, int K> struct CgShape {
+  using G1 = G1Shape<T, K>;
+  using G2 = G2Shape<T, K>;
+  static constexpr int S1 = G1::S;
+  static constexpr size_t RING = (size_t)S1 * G1::STAGE;  // both rings' stages
+  // GEMM2 stages + its reduction buffer fit inside RING; GEMM1's reduction
+  // buffer (in use by its epilogue while GEMM2 tiles stream in) sits after it
+  static constexpr int S2 = (4 * G2::STAGE + G2::RED <= RING)   ? 4
+                            : (3 * G2::STAGE + G2::RED <= RING) ? 3
+                                                                : 2;
+  static constexpr bool OK = S2 * G2::STAGE + G2::RED <= RING;
+  static constexpr size_t RED2 = (size_t)S2 * G2::STAGE;
+  static constexpr size_t SMEM = RING + G1::RED;
+};
+
+struct CgArgs {
+  G1Args g1;  // mode kHessApply; W = sw, U -> rowout; u_ready set
+  G2Args g2;  // base = s, out = Hs, dots; u_ready set
+  int grid1, grid2;
+  int T;
+  double theta;
+  int64_t d;
+  int p, P;
+  const double *g;
+  double *r, *s, *pv, *pb, *Hs, *dots, *state;
+  void *sw;           // s in the X dtype, [K][P] (GEMM1's W operand)
+  unsigned *bar;      // grid barrier [count, generation]
+  unsigned *u_ready;  // [row_blocks] (zero at rest)
+  int64_t row_blocks;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
+  unsigned x;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(x) : "l"(p) : "memory");
+  return x;
+}
+
+// Sense-free grid barrier over nblk co-resident CTAs: the last arriver resets
+// the count and bumps the generation (release); the others wait for the bump.
+__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblk) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned gen = ld_acquire_u32(bar + 1);
+    if (atomic_add_acq_rel(bar, 1u) == nblk - 1) {
+      bar[0] = 0u;
+      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(bar + 1), "r"(gen + 1u)
+                   : "memory");
+    } else {
+      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(20);
+    }
+  }
+  __syncthreads();
+}
+
+// Producer: wait until the consumers released every stage still in flight.
+__device__ __forceinline__ void ring_drain(uint64_t *empty, int S, int64_t itp) {
+  for (int64_t k = itp > S ? itp - S : 0; k < itp; ++k)
+    mbar_wait(&empty[k % S], (unsigned)((k / S) & 1));
+}
+
+struct CgSlot {
+  double rs, best, thr, iters, conv, done, err, curv;
+};
+
+template <typename T>
+__device__ __forceinline__ void store_sw(const CgArgs &a, int64_t i, double v) {
+  const int64_t c = i / a.p;
+  static_cast<T *>(a.sw)[c * a.P + (i - c * a.p)] = (T)v;
+}
+
+template <typename T, int K>
+__global__ void __launch_bounds__(kThreads, 1) cg_solve_kernel(const __grid_constant__ CgArgs a) {
+  using Sh = CgShape<T, K>;
+  constexpr int S1 = Sh::S1, S2 = Sh::S2;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  double *red1 = reinterpret_cast<double *>(smem + Sh::RING);
+  double *red2 = reinterpret_cast<double *>(smem + Sh::RED2);
+  __shared__ uint64_t full1[S1], empty1[S1], full2[S2], empty2[S2];
+  __shared__ double shd[kWarps];
+  __shared__ CgSlot cur;
+  const int tid = threadIdx.x;
+  const bool consumer = tid < kConsumers;
+  const int Gp = gridDim.x, cta = blockIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < S1; ++s) {
+      mbar_init(&full1[s], 1);
+      mbar_init(&empty1[s], kWarps);
+    }
+    for (int s = 0; s < S2; ++s) {
+      mbar_init(&full2[s], 1);
+      mbar_init(&empty2[s], kWarps);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int64_t d = a.d;
+  constexpr int64_t kStride = (int64_t)kDotBlocks * kDotThreads;
+  double *scr = scratch(a.state, a.T);
+
+  // ---- init (cg_init_kernel): r = s = -g, p = 0, p_best = -g, g.g partials
+  if (cta == 0)
+    for (int i = tid; i < (a.T + 2) * SNX_CG_SLOT; i += kThreads) a.state[i] = 0.0;
+  if (consumer) {
+    for (int vb = cta; vb < kDotBlocks; vb += Gp) {
+      double acc = 0.0;
+      for (int64_t i = (int64_t)vb * kDotThreads + tid; i < d; i += kStride) {
+        const double gi = a.g[i];
+        a.r[i] = -gi;
+        a.s[i] = -gi;
+        a.pv[i] = 0.0;
+        a.pb[i] = -gi;
+        store_sw<T>(a, i, -gi);
+        acc += gi * gi;
+      }
+      const double b = consumer_sum(acc, shd);
+      if (tid == 0) scr[vb] = b;
+    }
+    if (cta == 0 && a.P != a.p)  // zero pad columns of sw
+      for (int i = tid; i < K * (a.P - a.p); i += kConsumers)
+        static_cast<T *>(a.sw)[(i / (a.P - a.p)) * a.P + a.p + i % (a.P - a.p)] = T(0);
+  }
+  grid_barrier(a.bar, Gp);
+  if (tid < 32) {  // cg_init_final_kernel, computed by every CTA
+    const double gg = warp_sum_partials_cg(scr);
+    if (tid == 0) {
+      const double gn = sqrt(gg);
+      cur.rs = gg;
+      cur.best = gn;
+      cur.thr = a.theta * gn;
+      cur.iters = 0.0;
+      cur.conv = gn == 0.0 ? 1.0 : 0.0;
+      cur.done = gn == 0.0 ? 1.0 : 0.0;
+      cur.err = 0.0;
+      cur.curv = 0.0;
+      if (cta == 0) {
+        double *s0 = slot(a.state, 0);
+        s0[kRs] = cur.rs;
+        s0[kBest] = cur.best;
+        s0[kThr] = cur.thr;
+        s0[kIters] = 0.0;
+        s0[kConv] = cur.conv;
+        s0[kDone] = cur.done;
+      }
+    }
+  }
+  __syncthreads();
+
+  int64_t itp1 = 0, itc1 = 0, itp2 = 0, itc2 = 0;
+  int t = 0;
+  for (; t < a.T; ++t) {
+    if (cur.done != 0.0) break;
+    const unsigned epoch = (unsigned)t + 1u;
+    const bool tl = t == 5 && tid == 0;
+    if (tl) SNX_CTL(0);
+    // ---- Hs = H s (snx_hess_apply with the dots of s.Hs and s.s)
+    if (tid == kConsumers) asm volatile("fence.proxy.async.global;\n" ::: "memory");  // sw via TMA
+    gemm1_body<T, K, S1>(a.g1, smem, red1, full1, empty1, a.grid1, itp1, itc1, epoch);
+    if (tl) SNX_CTL(1);
+    if (tid == kConsumers && cta < a.grid1) ring_drain(empty1, S1, itp1);
+    gemm2_body<T, K, S2>(a.g2, smem, red2, full2, empty2, a.grid2, itp2, itc2, epoch);
+    if (tl) SNX_CTL(2);
+    grid_barrier(a.bar, Gp);
+    if (tl) SNX_CTL(3);
+    // ---- cg_step1: curvature test, alpha, p += a s, r -= a Hs
+    __shared__ double s_alpha;
+    __shared__ int s_bad;
+    if (tid < 32) {
+      const double curv = warp_sum_partials_cg(a.dots);
+      const double ss = warp_sum_partials_cg(a.dots + kDotBlocks);
+      if (tid == 0) {
+        s_bad = curv <= 1e-32 * ss;  // cg.py:16, :79
+        s_alpha = cur.rs / curv;
+        if (s_bad) {
+          cur.err = 1.0;
+          cur.curv = curv;
+          if (cta == 0) {
+            slot(a.state, t + 1)[kErr] = 1.0;
+            slot(a.state, t + 1)[kCurv] = curv;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    const bool bad = s_bad != 0;
+    if (!bad) {
+      if (consumer) {
+        const double alpha = s_alpha;
+        for (int vb = cta; vb < kDotBlocks; vb += Gp) {
+          double acc = 0.0;
+          for (int64_t i = (int64_t)vb * kDotThreads + tid; i < d; i += kStride) {
+            a.pv[i] = np_axpy(a.pv[i], alpha, a.s[i]);
+            const double ri = np_axmy(a.r[i], alpha, __ldcg(a.Hs + i));
+            a.r[i] = ri;
+            acc += ri * ri;
+          }
+          const double b = consumer_sum(acc, shd);
+          if (tid == 0) scr[vb] = b;
+        }
+      }
+      if (tl) SNX_CTL(4);
+      grid_barrier(a.bar, Gp);
+      if (tl) SNX_CTL(5);
+    }
+    // ---- cg_step2: best-iterate copy, stop test, new direction
+    if (bad) {
+      if (tid == 0) {
+        cur.conv = 0.0;
+        cur.iters = t + 1;
+        cur.done = 1.0;
+        if (cta == 0) {
+          double *nx = slot(a.state, t + 1);
+          nx[kRs] = cur.rs;
+          nx[kBest] = cur.best;
+          nx[kThr] = cur.thr;
+          nx[kConv] = 0.0;
+          nx[kIters] = t + 1;
+          nx[kDone] = 1.0;
+        }
+      }
+      __syncthreads();
+      ++t;
+      break;
+    }
+    __shared__ double s_rr;
+    if (tid < 32) {
+      const double rr = warp_sum_partials_cg(scr);
+      if (tid == 0) s_rr = rr;
+    }
+    __syncthreads();
+    const double rr = s_rr;
+    const double rn = sqrt(rr);
+    const bool best = rn <= cur.best;
+    const bool conv = rn <= cur.thr;
+    const double beta = rr / cur.rs;
+    if (consumer) {
+      for (int vb = cta; vb < kDotBlocks; vb += Gp)
+        for (int64_t i = (int64_t)vb * kDotThreads + tid; i < d; i += kStride) {
+          if (best) a.pb[i] = a.pv[i];
+          if (!conv) {
+            const double si = np_axpy(a.r[i], beta, a.s[i]);
+            a.s[i] = si;
+            store_sw<T>(a, i, si);
+          }
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      cur.rs = conv ? cur.rs : rr;
+      cur.best = best ? rn : cur.best;
+      cur.conv = conv ? 1.0 : 0.0;
+      cur.iters = t + 1;
+      cur.done = (conv || t + 1 >= a.T) ? 1.0 : 0.0;
+      if (cta == 0) {
+        double *nx = slot(a.state, t + 1);
+        nx[kRs] = cur.rs;
+        nx[kBest] = cur.best;
+        nx[kThr] = cur.thr;
+        nx[kConv] = cur.conv;
+        nx[kIters] = cur.iters;
+        nx[kDone] = cur.done;
+      }
+    }
+    __syncthreads();
+    if (tl) SNX_CTL(6);
+    if (cur.done != 0.0) {
+      ++t;
+      break;
+    }
+    grid_barrier(a.bar, Gp);  // s / sw complete before the next GEMM1
+    if (tl) SNX_CTL(7);
+  }
+  // slots after the last iteration repeat it (cg_step2 copies a done slot)
+  if (cta == 0 && tid == 0) {
+    const double *last = slot(a.state, t);
+    for (int u = t + 1; u <= a.T; ++u)
+      for (int k = 0; k < SNX_CG_SLOT; ++k) slot(a.state, u)[k] = last[k];
+  }
+  // every CTA is past its last GEMM phase once all arrive here
+  grid_barrier(a.bar, Gp);
+  if (cta == 0)
+    for (int64_t i = tid; i < a.row_blocks; i += kThreads) a.u_ready[i] = 0u;
 }
 
 // out = lam * base (the empty dataset: every data term vanishes), with the
@@ -1175,6 +1527,116 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   return rc;
 }
 
+template <typename T, int K>
+static int launch_cg_solve(const CgArgs &a, int grid, cudaStream_t st) {
+  using Sh = CgShape<T, K>;
+  if constexpr (!Sh::OK) {
+    set_error("snx_cg_solve: no shared-memory layout for this dtype / K");
+    return 1;
+  } else {
+    static bool configured = false;
+    if (!configured) {
+      if (cudaFuncSetAttribute(cg_solve_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)Sh::SMEM) != cudaSuccess)
+        return check_launch("cg_solve attributes");
+      configured = true;
+    }
+    carveout(cg_solve_kernel<T, K>);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = Sh::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, cg_solve_kernel<T, K>, a);
+    return check_launch("cg_solve");
+  }
+}
+
+static int cg_solve(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
+                    const void *H, double scale, double lam, const double *g, double theta,
+                    int32_t T, double *r, double *s, double *pv, double *pb, double *Hs,
+                    double *dots, double *state, void *ws, size_t ws_bytes, cudaStream_t st) {
+  if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
+  if (dtype != SNX_F64) {
+    set_error("snx_cg_solve: fp64 data only (the f32 path uses the tensor-core product)");
+    return 1;
+  }
+  if (nrows == 0 || T < 1 || H == nullptr || g == nullptr) {
+    set_error("snx_cg_solve: needs nrows > 0, max_iters >= 1, H and g");
+    return 1;
+  }
+  const int32_t P = padded(p);
+  const Geometry geo = geometry(dtype, nrows, P, K);
+  const Workspace lay = workspace_layout(dtype, nrows, p, K);
+  char *wsb = static_cast<char *>(ws);
+  unsigned *counters = reinterpret_cast<unsigned *>(wsb + lay.counters);
+  void *sw = wsb + lay.weights;
+  void *rowbuf = wsb + lay.rowbuf;
+  unsigned *u_ready = counters + 16 + kMaxTiles + kMaxRowBlocks;
+  CgArgs a{};
+  if (make_map(&a.g1.xmap, dtype, X, P, nrows, ldx, 128 / 8, kRB, true)) return 1;
+  if (make_map(&a.g1.wmap, dtype, sw, P, K, P, 512 / 8, K, false)) return 1;
+  a.g1.nrows = nrows;
+  a.g1.nchunks = geo.nchunks;
+  a.g1.maxseg = geo.g1_maxseg;
+  a.g1.items = geo.g1_items;
+  a.g1.row_blocks = geo.row_blocks;
+  a.g1.mode = kHessApply;
+  a.g1.ustride = u_stride(dtype, K);
+  a.g1.zp = reinterpret_cast<double *>(wsb + lay.zp);
+  a.g1.rb_count = counters + 16 + kMaxTiles;
+  a.g1.done_rb = counters + 2;
+  a.g1.H = H;
+  a.g1.rowout = rowbuf;
+  a.g1.loss_part = reinterpret_cast<double *>(wsb + lay.loss_part);
+  a.g1.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
+  a.g1.u_ready = u_ready;
+  if (make_map(&a.g2.xmap, dtype, X, P, nrows, ldx, (uint32_t)geo.tcol, kG2Rows, false)) return 1;
+  a.g2.nrows = nrows;
+  a.g2.rchunks = geo.rchunks;
+  a.g2.maxseg = geo.g2_maxseg;
+  a.g2.items = geo.g2_items;
+  a.g2.U = rowbuf;
+  a.g2.gp = reinterpret_cast<double *>(wsb + lay.gp);
+  a.g2.tile_count = counters + 16;
+  a.g2.col_tiles = geo.col_tiles;
+  a.g2.p = p;
+  a.g2.scale = scale;
+  a.g2.lam = lam;
+  a.g2.base = s;
+  a.g2.out = Hs;
+  a.g2.dots = dots;
+  a.g2.u_ready = u_ready;
+  a.grid1 = geo.grid1;
+  a.grid2 = geo.grid2;
+  a.T = T;
+  a.theta = theta;
+  a.d = (int64_t)K * p;
+  a.p = p;
+  a.P = P;
+  a.g = g;
+  a.r = r;
+  a.s = s;
+  a.pv = pv;
+  a.pb = pb;
+  a.Hs = Hs;
+  a.dots = dots;
+  a.state = state;
+  a.sw = sw;
+  a.bar = counters + 4;
+  a.u_ready = u_ready;
+  a.row_blocks = geo.row_blocks;
+  const int grid = geo.grid1 > geo.grid2 ? geo.grid1 : geo.grid2;
+  int rc = 1;
+  SNX_K_SWITCH(K, (rc = launch_cg_solve<double, KK>(a, grid, st)));
+  return rc;
+}
+
 int gather(int dtype, const void *X, int64_t ldx, const int32_t *labels,
                   const int64_t *rows, int64_t nrows, void *dst, int64_t ldd,
                   int32_t *labels_out, cudaStream_t st) {
@@ -1211,6 +1673,11 @@ using namespace snx;
 extern "C" {
 
 #ifdef SNX_TIMELINE
+int snx_debug_cg_timeline(unsigned long long *host_out) {
+  return cudaMemcpyFromSymbol(host_out, g_cg_timeline, sizeof(g_cg_timeline)) == cudaSuccess ? 0
+                                                                                             : 1;
+}
+
 int snx_debug_timeline(unsigned long long *host_out) {
   return cudaMemcpyFromSymbol(host_out, g_timeline, sizeof(g_timeline)) == cudaSuccess ? 0 : 1;
 }
@@ -1274,6 +1741,15 @@ int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
   return rowpass(kHessPrep, dtype, Xs, lds, nrows, p, K, nullptr, w, nullptr, 0.0, nullptr,
                  H_out, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ws,
                  ws_bytes, st);
+}
+
+int snx_cg_solve(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
+                 const void *H, double scale, double lam, const double *g, double theta,
+                 int32_t max_iters, double *r, double *s, double *p_vec, double *p_best,
+                 double *Hs, double *dots, double *state, void *ws, size_t ws_bytes,
+                 void *stream) {
+  return cg_solve(dtype, Xs, ldx, nrows, p, K, H, scale, lam, g, theta, max_iters, r, s, p_vec,
+                  p_best, Hs, dots, state, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,

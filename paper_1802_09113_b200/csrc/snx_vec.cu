@@ -189,15 +189,6 @@ __device__ unsigned long long g_vec_timeline[2][256][2];
 #endif
 
 // ------------------------------------------------------------------ CG (cg.py)
-// slot layout (SNX_CG_SLOT doubles)
-enum { kRs = 0, kBest = 1, kDone = 2, kIters = 3, kConv = 4, kThr = 5, kErr = 6, kCurv = 7 };
-
-__device__ __forceinline__ double *slot(double *state, int t) { return state + t * SNX_CG_SLOT; }
-
-// scratch after the slots: [0, B) g.g / r.r partials
-__device__ __forceinline__ double *scratch(double *state, int max_iters) {
-  return state + (max_iters + 2) * SNX_CG_SLOT;
-}
 
 __global__ void __launch_bounds__(kDotThreads)
     cg_init_kernel(const double *__restrict__ g, int64_t d, int max_iters, double *r,

@@ -16,6 +16,8 @@ contract) or CUDA torch tensors (results stay on the device).
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 import torch
 
@@ -182,6 +184,27 @@ class HessianOperator:
                       self.p, self.view.K, ptr(hb.h), ptr(v), self.scale, self.lam, ptr(out),
                       ptr(dots), skip, *_ws(self.view), stream_handle())
         return out
+
+    def cg_solve_into(self, g, theta, T, ws):
+        """Enqueue the whole CG solve as one persistent kernel (snx_cg_solve,
+        fp64 data) when SNX_CG_PERSISTENT=1; False -> the per-iteration path.
+
+        Opt-in: bit-identical to the per-iteration path, but measured slower
+        on B200 (484 vs 432 us per 10-product CIFAR solve): its three software
+        grid barriers per iteration cost ~2.2 us each, more than the ~1 us
+        kernel boundaries of the captured per-iteration graph."""
+        hb, view = self._bufs, self.view
+        if (hb.xs_lo is not None or view.n_rows == 0
+                or os.environ.get("SNX_CG_PERSISTENT", "0") != "1"):
+            return False
+        if hb.owner is not self:
+            self._prepare()
+        base = view.base
+        _lib.call("snx_cg_solve", base.code, ptr(hb.xs), base.ld, view.n_rows, self.p, view.K,
+                  ptr(hb.h), self.scale, self.lam, ptr(g), float(theta), T, ptr(ws.r),
+                  ptr(ws.s), ptr(ws.p), ptr(ws.pb), ptr(ws.Hs), ptr(ws.dots), ptr(ws.state),
+                  *_ws(view), stream_handle())
+        return True
 
     def apply(self, v):
         if isinstance(v, torch.Tensor) or np.asarray(v).shape == (self.dim,):
