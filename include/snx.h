@@ -99,17 +99,20 @@ int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_
                    double *dots, const double *skip, void *ws, size_t ws_bytes, void *stream);
 
 /* Tensor-core variant of the two calls above for f32 data (the declared 1e-4
- * path; tcgen05 kind::tf32 MMAs with a 3xTF32 split, see csrc/snx_tc.cu).
- * snx_hess_prepare_tc = snx_hess_prepare(SNX_F32, ...) plus
- *   Xlo_out[r][j] = Xs[r][j] - tf32(Xs[r][j])   (same shape and ld as Xs),
- * the low part every product of this sample reuses.  When rows == NULL the
- * sample is X itself and Xlo_out has X's shape and ldx. */
+ * path; tcgen05 kind::f16 MMAs on a two-term bf16 split, see csrc/snx_tc.cu).
+ * snx_hess_prepare_tc = snx_hess_prepare(SNX_F32, ...) plus the split of the
+ * sample rows Xs (or X when rows == NULL):
+ *   X1[r][j] = bf16(Xs[r][j]),  X2[r][j] = bf16(Xs[r][j] - X1[r][j])
+ * as [nrows][ldb] bf16 arrays, ldb >= snx_tc_ld(p) (a multiple of 8); every
+ * product of this sample reuses them. */
+int64_t snx_tc_ld(int32_t p);
 int snx_hess_prepare_tc(const float *X, int64_t ldx, const int64_t *rows, int64_t nrows,
-                        int32_t p, int32_t K, const double *w, float *Xs_out, float *Xlo_out,
-                        int64_t ld_out, float *H_out, void *ws, size_t ws_bytes, void *stream);
+                        int32_t p, int32_t K, const double *w, float *Xs_out, int64_t ld_out,
+                        float *H_out, void *X1_out, void *X2_out, int64_t ldb, void *ws,
+                        size_t ws_bytes, void *stream);
 
-/* snx_hess_apply(SNX_F32, ...) on the tensor cores; Xlo from snx_hess_prepare_tc. */
-int snx_hess_apply_tc(const float *Xs, const float *Xlo, int64_t ldx, int64_t nrows, int32_t p,
+/* snx_hess_apply(SNX_F32, ...) on the tensor cores from the split sample. */
+int snx_hess_apply_tc(const void *X1, const void *X2, int64_t ldb, int64_t nrows, int32_t p,
                       int32_t K, const float *H, const double *v, double scale, double lam,
                       double *Hv_out, double *dots, const double *skip, void *ws,
                       size_t ws_bytes, void *stream);

@@ -45,14 +45,14 @@ struct Workspace {
   size_t dot_part;    // 4*kDotBlocks doubles (w.w partials)
   size_t counters;    // uint32 scheduler words + arrival counters (zero at rest)
   // f32 tensor-core Hessian product (snx_tc.cu); zero-sized for f64
-  size_t tc_b;        // [32][P] f32: B operand of GEMM1 (v rows, then v - tf32(v) rows)
-  size_t tc_ut;       // [32][round_up(nrows,4)] f32: U^T rows, then U^T - tf32(U^T) rows
+  size_t tc_b;        // [32][round_up(P,8)] bf16: GEMM1's B = [Q1 ; Q2] (bf16 split of v)
+  size_t tc_ut;       // [32][round_up(nrows,8)] bf16: GEMM2's B = [U1^T ; U2^T]
   size_t tc_zp;       // GEMM1 segment partials [row_blocks][maxseg1][128][K] doubles
   size_t tc_gp;       // GEMM2 segment partials [col_tiles][maxseg2][K][128] doubles
   size_t total;
 };
 // Geometry of the tensor-core Hessian product: GEMM1 items = (128-row block x
-// 32-column k-tile), GEMM2 items = (128-column tile x 32-row chunk), each
+// 64-column k-tile), GEMM2 items = (128-column tile x 64-row chunk), each
 // split stream-K over <= one CTA per SM.
 struct TcGeometry {
   int grid1, nk;
@@ -101,8 +101,8 @@ bool pdl_enabled();
 
 // Launch with programmatic stream serialization (PDL); see snx_pipe.cuh.
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
-                              cudaStream_t st, Args... args) {
+inline cudaError_t launch_pdl_if(bool pdl, void (*kernel)(KArgs...), dim3 grid, dim3 block,
+                                 size_t smem, cudaStream_t st, Args... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -112,8 +112,19 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  cfg.numAttrs = pdl ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
 }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args... args) {
+  return launch_pdl_if(pdl_enabled(), kernel, grid, block, smem, st, args...);
+}
+
+// The row-pass GEMM2 overlaps its prologue and X tiles with GEMM1's tail
+// (programmatic dependent launch; it waits before its first U load).
+// SNX_GEMM2_PDL=0 disables.
+bool gemm2_pdl();
 
 }  // namespace snx

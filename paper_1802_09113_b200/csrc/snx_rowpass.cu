@@ -683,6 +683,7 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
         unsigned char *st = smem + s * Sh::STAGE;
         tma_load_2d(st, &a.xmap, tile * TCOL, (int)c0, &full[s]);
         if (a.u_ready != nullptr) wait_flag_geq(a.u_ready + c0 / kRB, epoch);
+        if (i == i0) pdl_wait();  // no-op unless launched as a programmatic dependent
         bulk_g2s(st + Sh::XB, U + c0 * KP, ub, &full[s]);
         if (++rc == a.rchunks) {
           rc = 0;
@@ -790,7 +791,9 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
 template <typename T, int K>
 __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constant__ G2Args a) {
   pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
-  pdl_wait();
+  // launched as a programmatic dependent of GEMM1: everything read here was
+  // complete before GEMM1 started, except the U rows -- the producer waits
+  // for GEMM1 (griddepcontrol.wait) right before its first U load
   if (a.skip != nullptr && *a.skip != 0.0) return;
   using Sh = G2Shape<T, K>;
   constexpr int S = Sh::S;
@@ -1237,8 +1240,7 @@ int sm_count() {
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
-int make_tmap(CUtensorMap *m, bool f64, const void *base, uint64_t cols, uint64_t rows,
-              uint64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
+static bool have_encode() {
   if (g_encode == nullptr) {
     void *fn = nullptr;
     cudaDriverEntryPointQueryResult q;
@@ -1246,10 +1248,16 @@ int make_tmap(CUtensorMap *m, bool f64, const void *base, uint64_t cols, uint64_
             cudaSuccess ||
         fn == nullptr) {
       set_error("snx: cuTensorMapEncodeTiled unavailable (driver too old?)");
-      return 1;
+      return false;
     }
     g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
   }
+  return true;
+}
+
+int make_tmap(CUtensorMap *m, bool f64, const void *base, uint64_t cols, uint64_t rows,
+              uint64_t ld, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz) {
+  if (!have_encode()) return 1;
   const size_t tb = f64 ? 8 : 4;
   const cuuint64_t dims[2] = {cols, rows > 0 ? rows : 1};
   const cuuint64_t strides[1] = {ld * tb};
@@ -1262,6 +1270,27 @@ int make_tmap(CUtensorMap *m, bool f64, const void *base, uint64_t cols, uint64_
   if (r != CUDA_SUCCESS) {
     set_error("snx: cuTensorMapEncodeTiled failed (%d) for %llux%llu ld=%llu box %ux%u", (int)r,
               (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)ld,
+              box_rows, box_cols);
+    return 1;
+  }
+  return 0;
+}
+
+// bf16 [rows][ld] tensor, 128-B swizzled boxes (box_cols * 2 == 128)
+int make_tmap_bf16(CUtensorMap *m, const void *base, uint64_t cols, uint64_t rows, uint64_t ld,
+                   uint32_t box_cols, uint32_t box_rows) {
+  if (!have_encode()) return 1;
+  const cuuint64_t dims[2] = {cols, rows > 0 ? rows : 1};
+  const cuuint64_t strides[1] = {ld * 2};
+  const cuuint32_t box[2] = {box_cols, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  const CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void *>(base),
+                              dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("snx: cuTensorMapEncodeTiled(bf16) failed (%d) for %llux%llu ld=%llu box %ux%u",
+              (int)r, (unsigned long long)rows, (unsigned long long)cols, (unsigned long long)ld,
               box_rows, box_cols);
     return 1;
   }
@@ -1328,8 +1357,8 @@ Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K) {
   w.dot_part = take((size_t)4 * kDotBlocks * 8);
   if (dtype == SNX_F32) {  // tensor-core Hessian product (snx_tc.cu)
     const TcGeometry t = tc_geometry(nrows, P);
-    w.tc_b = take((size_t)32 * P * 4);
-    w.tc_ut = take((size_t)32 * round_up((size_t)nr, 4) * 4);
+    w.tc_b = take((size_t)32 * round_up((size_t)P, 8) * 2);
+    w.tc_ut = take((size_t)32 * round_up((size_t)nr, 8) * 2);
     w.tc_zp = take((size_t)(t.row_blocks > 0 ? t.row_blocks : 1) * t.maxseg1 * 128 * K * 8);
     w.tc_gp = take((size_t)t.col_tiles * t.maxseg2 * K * 128 * 8);
   }
@@ -1339,7 +1368,8 @@ Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K) {
 
 template <typename KernelT, typename ArgT>
 static int launch_persistent(KernelT kernel, int grid, size_t smem, size_t *configured,
-                             cudaStream_t st, const ArgT &args, const char *what) {
+                             cudaStream_t st, const ArgT &args, const char *what,
+                             bool pdl = false) {
   if (smem > *configured) {
     if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem) != cudaSuccess)
@@ -1347,7 +1377,8 @@ static int launch_persistent(KernelT kernel, int grid, size_t smem, size_t *conf
     *configured = smem;
   }
   carveout(kernel);
-  launch_pdl(kernel, dim3(grid), dim3(kThreads), smem, st, args);  // one CTA per SM
+  launch_pdl_if(pdl || pdl_enabled(), kernel, dim3(grid), dim3(kThreads), smem, st,
+                args);  // one CTA per SM
   return check_launch(what);
 }
 
@@ -1362,7 +1393,7 @@ template <typename T, int K>
 static int launch_gemm2(const G2Args &a, int grid, cudaStream_t st) {
   static size_t configured = 0;
   return launch_persistent(gemm2_kernel<T, K>, grid, G2Shape<T, K>::SMEM, &configured, st, a,
-                           "gemm2");
+                           "gemm2", gemm2_pdl());
 }
 
 #define SNX_K_SWITCH(K, CALL)                         \

@@ -31,6 +31,15 @@ bool pdl_enabled() {
   return on == 1;
 }
 
+bool gemm2_pdl() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SNX_GEMM2_PDL");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 void prefer_max_smem(const void *kernel) {
   static const void *seen[256];
   static int nseen = 0;

@@ -169,10 +169,12 @@ class HessBuffers:
         self.xs = torch.empty((mm, base.ld), dtype=base.X.dtype, device=dev) if gathered \
             else base.X
         self.h = torch.empty((mm, base.K), dtype=base.X.dtype, device=dev)
-        # f32: low tf32 parts of the sample rows for the tensor-core product
-        self.xs_lo = torch.empty((mm if gathered else base.X.shape[0], base.ld),
-                                 dtype=torch.float32, device=dev) \
-            if base.code == _lib.F32 else None
+        # f32: bf16 split X1 + X2 of the sample rows for the tensor-core product
+        self.xs_tc = None
+        if base.code == _lib.F32:
+            self.ldb = int(_lib.load().snx_tc_ld(base.n_features))
+            rows = mm if gathered else max(base.X.shape[0], 1)
+            self.xs_tc = torch.empty((2, rows, self.ldb), dtype=torch.bfloat16, device=dev)
         self.owner = None
         self.graphs = {}
 

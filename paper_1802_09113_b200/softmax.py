@@ -154,10 +154,10 @@ class HessianOperator:
     def _prepare(self):
         """Materialise this operator's sample and probabilities in the shared buffers."""
         view, base, hb = self.view, self.view.base, self._bufs
-        if hb.xs_lo is not None:  # f32: tensor-core product (csrc/snx_tc.cu)
+        if hb.xs_tc is not None:  # f32: tensor-core product (csrc/snx_tc.cu)
             _lib.call("snx_hess_prepare_tc", ptr(base.X), base.ld, ptr(view.rows), view.n_rows,
-                      view.n_features, view.K, ptr(self._w), ptr(hb.xs), ptr(hb.xs_lo),
-                      base.ld, ptr(hb.h), *_ws(view), stream_handle())
+                      view.n_features, view.K, ptr(self._w), ptr(hb.xs), base.ld, ptr(hb.h),
+                      ptr(hb.xs_tc[0]), ptr(hb.xs_tc[1]), hb.ldb, *_ws(view), stream_handle())
         else:
             _lib.call("snx_hess_prepare", base.code, ptr(base.X), base.ld, ptr(view.rows),
                       view.n_rows, view.n_features, view.K, ptr(self._w), ptr(hb.xs), base.ld,
@@ -175,10 +175,10 @@ class HessianOperator:
         if self._bufs.owner is not self:
             self._prepare()
         base, hb = self.view.base, self._bufs
-        if hb.xs_lo is not None:
-            _lib.call("snx_hess_apply_tc", ptr(hb.xs), ptr(hb.xs_lo), base.ld, self.view.n_rows,
-                      self.p, self.view.K, ptr(hb.h), ptr(v), self.scale, self.lam, ptr(out),
-                      ptr(dots), skip, *_ws(self.view), stream_handle())
+        if hb.xs_tc is not None:
+            _lib.call("snx_hess_apply_tc", ptr(hb.xs_tc[0]), ptr(hb.xs_tc[1]), hb.ldb,
+                      self.view.n_rows, self.p, self.view.K, ptr(hb.h), ptr(v), self.scale,
+                      self.lam, ptr(out), ptr(dots), skip, *_ws(self.view), stream_handle())
         else:
             _lib.call("snx_hess_apply", base.code, ptr(hb.xs), base.ld, self.view.n_rows,
                       self.p, self.view.K, ptr(hb.h), ptr(v), self.scale, self.lam, ptr(out),
@@ -194,7 +194,7 @@ class HessianOperator:
         grid barriers per iteration cost ~2.2 us each, more than the ~1 us
         kernel boundaries of the captured per-iteration graph."""
         hb, view = self._bufs, self.view
-        if (hb.xs_lo is not None or view.n_rows == 0
+        if (hb.xs_tc is not None or view.n_rows == 0
                 or os.environ.get("SNX_CG_PERSISTENT", "0") != "1"):
             return False
         if hb.owner is not self:

@@ -1,4 +1,4 @@
-"""Tensor-core (tcgen05 kind::tf32, 3xTF32) Hessian product of the f32 path
+"""Tensor-core (tcgen05 kind::f16, two-term bf16 split) Hessian product of the f32 path
 against the fp64 oracle: ragged row / column counts around the 128-row,
 32-column and 128-column tile edges, every class count K = 1..16, sampled
 and unsampled operators, bit-identical reruns."""
@@ -34,7 +34,7 @@ def test_tc_hess_apply_vs_oracle(n, p, C):
     ds = snx.DeviceDataset.from_numpy(A, y, C, dtype="f32")
     lam = 1e-3
     op = snx.HessianOperator(ds, x, lam, scale=1.7)
-    assert op._bufs.xs_lo is not None  # the tensor-core path is the one under test
+    assert op._bufs.xs_tc is not None  # the tensor-core path is the one under test
     h = oracle.hess_probs(A, y, C, x)
     ref = oracle.hess_apply(A, h, C, v, 1.7, lam)
     got = op.apply(v)
