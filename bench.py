@@ -166,6 +166,88 @@ def run_reference(args):
     }))
 
 
+def shape_rate(snx, torch, A, y, nC, dtype, steps=30, warmup=3, frac=F_H):
+    """Hv/s of the bench step (fresh S_H prepare + captured CG solve) at another
+    BASELINE shape; device-timed with CUDA events."""
+    from paper_1802_09113_b200 import cg as cgmod, softmax
+
+    n, p = A.shape
+    ds = snx.DeviceDataset.from_numpy(A, y, nC, dtype=dtype)
+    x = torch.from_numpy(0.01 * np.random.default_rng(7).standard_normal((nC - 1) * p)).cuda()
+    g, _ = softmax.gradient_parts(ds, x, 1.0, LAM)
+    views = [ds.take(snx.draw_samples(snx.SampleConfig(1.0, frac), n, k)[1])
+             for k in range(warmup + steps)]
+    m = views[0].n_rows
+    iters = torch.zeros(warmup + steps, dtype=torch.float64, device="cuda")
+    keep = [None]
+
+    def step(k):
+        op = softmax.HessianOperator(views[k], x, LAM, scale=n / m)
+        keep[0] = op
+        ws = cgmod.cg_graph_for(op, T_CG, THETA).run(g)
+        iters[k:k + 1].copy_(ws.slot(T_CG)[3:4])
+
+    for k in range(warmup):
+        step(k)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for k in range(warmup, warmup + steps):
+        step(k)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    hv = int(iters[warmup:].sum())
+    out = torch.empty_like(g)
+    op = keep[0]
+    for _ in range(3):
+        op.apply_into(g, out)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(20):
+        op.apply_into(g, out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    res = {"value": hv / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "steps": steps,
+           "m": m, "dtype": dtype, "hess_apply_us": e0.elapsed_time(e1) / 20 * 1e3}
+    del ds, views, keep, op
+    torch.cuda.empty_cache()
+    return res
+
+
+def secondary(snx, torch, args):
+    """The other BASELINE.json shapes and the tensor-core f32 path (one GPU)."""
+    import oracle
+
+    out = {}
+    for name, n, p, nC in (("mnist", 60000, 784, 10), ("covertype", 581012, 54, 7)):
+        A, y = oracle.synthetic_problem(n, p, nC, seed=0)
+        out[name] = shape_rate(snx, torch, A, y, nC, "f64")
+        out[name]["workload"] = f"{name}-shape {n}x{p} C={nC}, 5% S_H, fp64"
+        del A, y
+    if args.dtype == "f64":
+        A, y = make_problem()
+        out["cifar10_f32_tensor_core"] = shape_rate(snx, torch, A, y, C, "f32")
+        out["cifar10_f32_tensor_core"]["workload"] = (
+            "cifar10-shape, f32 data, Hessian GEMMs on tcgen05 (bf16 two-term split), 1e-4 path")
+    # BASELINE config #4: trust region (Steihaug-CG), ill-conditioned CIFAR shape, 10% S_H
+    A, y = oracle.synthetic_problem(N, P, C, seed=0, normalize=False, ill_conditioned=True)
+    prob = snx.SoftmaxProblem(snx.DeviceDataset.from_numpy(A, y, C), LAM)
+    cfg = snx.TrustRegionConfig(max_outer_iters=20)
+    snx.trust_region_solve(prob, snx.TrustRegionConfig(max_outer_iters=2))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tr = snx.trust_region_solve(prob, cfg)
+    torch.cuda.synchronize()
+    out["trust_region_cifar10_illcond"] = {
+        "seconds": time.perf_counter() - t0, "outer_iters": tr.iterations, "reason": tr.reason,
+        "final_objective": tr.final_objective, "hessian_fraction": 0.1,
+        "workload": "cifar10-shape ill-conditioned (logspace(2,-4,p) columns), TR Steihaug-CG, "
+                    "<= 20 outer iterations"}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -328,6 +410,10 @@ def run_ours(args):
 
     cpu = cpu_baseline(A, y, x_host) if (rank == 0 and world == 1 and not args.skip_cpu) \
         else None
+    shapes = None
+    if world == 1 and not args.skip_shapes:
+        del A, y
+        shapes = secondary(snx, torch, args)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -341,7 +427,7 @@ def run_ours(args):
                        "l2": "inputs > L2: 1.23 GB X in HBM, fresh S_H gathered every step"},
             "hv_applied": hv_count, "gpu_launches": args.steps * (4 + 2 + 6 * T_CG),
             "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
-            "cpu_baseline": cpu, "newton_solve": solve,
+            "cpu_baseline": cpu, "newton_solve": solve, "other_shapes": shapes,
         }
         print(json.dumps(line))
     if world > 1:
@@ -357,6 +443,7 @@ def main():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--skip-cpu", action="store_true")
     ap.add_argument("--skip-solve", action="store_true")
+    ap.add_argument("--skip-shapes", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
