@@ -81,7 +81,10 @@ def enqueue_cg(op, g, theta, T, ws):
         return
     _lib.call("snx_cg_init", ptr(g), d, float(theta), T, ptr(ws.r), ptr(ws.s), ptr(ws.p),
               ptr(ws.pb), ptr(ws.state), stream_handle())
+    fused = getattr(op, "apply_cg_into", None)
     for t in range(T):
+        if fused is not None and fused(t, T, ws):  # CG update inside the product's tail
+            continue
         op.apply_into(ws.s, ws.Hs, dots=ws.dots, skip=ws.done_ptr(t))
         _lib.call("snx_cg_update", t, T, d, ptr(ws.Hs), ptr(ws.dots), ptr(ws.r), ptr(ws.s),
                   ptr(ws.p), ptr(ws.pb), ptr(ws.state), stream_handle())
@@ -128,7 +131,8 @@ class CgGraph:
 def cg_graph_for(op, T, theta):
     """The CgGraph of op's shared buffers for (T, theta, scale, lam)."""
     hb = op._bufs
-    key = (T, float(theta), op.scale, op.lam, op.dim, os.environ.get("SNX_CG_PERSISTENT", "0"))
+    key = (T, float(theta), op.scale, op.lam, op.dim, os.environ.get("SNX_CG_PERSISTENT", "0"),
+           os.environ.get("SNX_CG_FUSED", "0"))
     cg = hb.graphs.get(key)
     if cg is None:
         cg = hb.graphs[key] = CgGraph(op, op.dim, T, theta, hb.h.device)

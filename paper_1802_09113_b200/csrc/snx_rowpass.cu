@@ -592,6 +592,11 @@ struct G2Args {
   double *out;           // scale * X^T U + lam * base, flat class-major
   double *dots;          // nullable: [tile] partials of base.out, [kDotBlocks + tile] of base.base
   const unsigned *u_ready;  // persistent CG kernel: [row_blocks] U publication epochs
+  // CG iteration fused into the tail (snx_hess_apply_cg; cg_state == NULL: off)
+  double *cg_state;      // slots (cg.py state), scratch = per-tile r.r partials
+  double *cg_r, *cg_p, *cg_pb;  // base == s
+  unsigned *cg_sync;     // [3] arrival counters (zero at rest)
+  int cg_t, cg_T;
 };
 
 // out[c*p + j] = scale * sum_seg gp[tile][seg][c][jj] + lam * base[c*p + j] for
@@ -599,7 +604,7 @@ struct G2Args {
 // two products, one add), plus the tile's partials of base.out and base.base
 // (the CG curvature test; tile 0 zeroes the unused partial slots).
 template <int K, int TCOL>
-__device__ __noinline__ void tile_finalize(const G2Args &a, int tile, int G, double *shd) {
+__device__ __forceinline__ void tile_finalize(const G2Args &a, int tile, int G, double *shd) {
   const int tid = threadIdx.x;
   const int c_lo = sk_owner(a.items, G, (int64_t)tile * a.rchunks);
   const int nseg = sk_owner(a.items, G, (int64_t)(tile + 1) * a.rchunks - 1) - c_lo + 1;
@@ -636,6 +641,138 @@ __device__ __noinline__ void tile_finalize(const G2Args &a, int tile, int G, dou
     }
 }
 
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
+  unsigned x;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(x) : "l"(p) : "memory");
+  return x;
+}
+
+// The CG iteration of cg.py:77-96 fused into GEMM2's tail (snx_hess_apply_cg),
+// run by the CTAs that finalized column tiles, once they have finished all
+// their items (so the waits below never wait on their own work): wait until
+// every tile's H s and curvature partials are out, then alpha, p += a s,
+// r -= a H s on the own tiles' elements and the tiles' r.r partials, wait for
+// every tile's partial, then beta, the best copy, the new direction and (by the
+// finalizer of tile 0) the next state slot.  Reductions are fixed-order over
+// tiles, so the result does not depend on which CTA finalized which tile.
+template <int K, int TCOL>
+__device__ __forceinline__ void cg_tail(const G2Args &a, const int *tiles, int n, double *shd,
+                                     double *shx) {
+  const int tid = threadIdx.x;
+  const int t = a.cg_t;
+  const double *st = slot(a.cg_state, t);
+  double *nx = slot(a.cg_state, t + 1);
+  double *rrp = scratch(a.cg_state, a.cg_T);
+  // shared scalars (the caller's smem: no static __shared__ in this function)
+  double &s_alpha = shx[0], &s_curv = shx[1], &s_rr = shx[2];
+  double &s_bad = shx[3], &s_last = shx[4];
+  constexpr int kPer = (K * TCOL + kConsumers - 1) / kConsumers;
+  bool own0 = false;
+  for (int k = 0; k < n; ++k) own0 |= tiles[k] == 0;
+  // ---- every tile's H s and s.Hs / s.s partials are out
+  consumer_sync(kConsumers);
+  if (tid == 0) {
+    atomic_add_acq_rel(a.cg_sync, (unsigned)n);
+    while (ld_acquire_gpu(a.cg_sync) < (unsigned)a.col_tiles) __nanosleep(32);
+  }
+  consumer_sync(kConsumers);
+  if (tid < 32) {  // cg_step1: the same fixed-order sums in every CTA
+    const double curv = warp_sum_partials_cg(a.dots);
+    const double ss = warp_sum_partials_cg(a.dots + kDotBlocks);
+    if (tid == 0) {
+      s_bad = curv <= 1e-32 * ss ? 1.0 : 0.0;  // cg.py:16, :79
+      s_alpha = __ldcg(st + kRs) / curv;
+      s_curv = curv;
+    }
+  }
+  consumer_sync(kConsumers);
+  if (s_bad != 0.0) {
+    if (own0 && tid == 0) {
+      nx[kErr] = 1.0;
+      nx[kCurv] = s_curv;
+      nx[kRs] = st[kRs];
+      nx[kBest] = st[kBest];
+      nx[kThr] = st[kThr];
+      nx[kConv] = 0.0;
+      nx[kIters] = t + 1;
+      nx[kDone] = 1.0;
+    }
+  } else {
+    const double alpha = s_alpha;
+    for (int k = 0; k < n; ++k) {
+      const int tile = tiles[k];
+      double acc = 0.0;
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * kConsumers;
+        const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
+        if (e < K * TCOL && j < a.p) {
+          const int64_t i = (int64_t)c * a.p + j;
+          a.cg_p[i] = np_axpy(a.cg_p[i], alpha, __ldcg(a.base + i));
+          const double ri = np_axmy(a.cg_r[i], alpha, __ldcg(a.out + i));
+          a.cg_r[i] = ri;
+          acc += ri * ri;
+        }
+      }
+      const double b = consumer_sum(acc, shd);
+      if (tid == 0) rrp[tile] = b;
+    }
+    // ---- every tile's r.r partial is out
+    consumer_sync(kConsumers);
+    if (tid == 0) {
+      atomic_add_acq_rel(a.cg_sync + 1, (unsigned)n);
+      while (ld_acquire_gpu(a.cg_sync + 1) < (unsigned)a.col_tiles) __nanosleep(32);
+    }
+    consumer_sync(kConsumers);
+    if (tid < 32) {
+      double v = 0.0;
+      for (int k = tid; k < a.col_tiles; k += 32) v += __ldcg(rrp + k);
+      v = warp_allsum(v);
+      if (tid == 0) s_rr = v;
+    }
+    consumer_sync(kConsumers);
+    // cg_step2
+    const double rr = s_rr;
+    const double rn = sqrt(rr);
+    const double rs0 = __ldcg(st + kRs), best0 = __ldcg(st + kBest), thr = __ldcg(st + kThr);
+    const bool best = rn <= best0;
+    const bool conv = rn <= thr;
+    const double beta = rr / rs0;
+    for (int k = 0; k < n; ++k) {
+      const int tile = tiles[k];
+#pragma unroll
+      for (int q = 0; q < kPer; ++q) {
+        const int e = tid + q * kConsumers;
+        const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
+        if (e < K * TCOL && j < a.p) {
+          const int64_t i = (int64_t)c * a.p + j;
+          if (best) a.cg_pb[i] = a.cg_p[i];
+          if (!conv) const_cast<double *>(a.base)[i] = np_axpy(a.cg_r[i], beta, a.base[i]);
+        }
+      }
+    }
+    if (own0 && tid == 0) {
+      nx[kRs] = conv ? rs0 : rr;
+      nx[kBest] = best ? rn : best0;
+      nx[kThr] = thr;
+      nx[kConv] = conv ? 1.0 : 0.0;
+      nx[kIters] = t + 1;
+      nx[kDone] = (conv || t + 1 >= a.cg_T) ? 1.0 : 0.0;
+    }
+  }
+  // ---- the last finalizer out resets the counters for the next launch
+  consumer_sync(kConsumers);
+  if (tid == 0) {
+    s_last = atomic_add_acq_rel(a.cg_sync + 2, (unsigned)n) == (unsigned)(a.col_tiles - n);
+    if (s_last != 0.0) {
+      a.cg_sync[0] = 0u;
+      a.cg_sync[1] = 0u;
+      a.cg_sync[2] = 0u;
+    }
+  }
+  consumer_sync(kConsumers);
+}
+
 // Acquire a U-ready flag written by another CTA of the same kernel (the
 // persistent CG kernel), then order the TMA (async proxy) reads after it.
 __device__ __forceinline__ void wait_flag_geq(const unsigned *f, unsigned v) {
@@ -666,6 +803,9 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
   const int rc0 = (int)(i0 - (int64_t)tile0 * a.rchunks);
   __shared__ double shd[kWarps];
   __shared__ int last_tile;
+  __shared__ int fin_tiles[4], nfin;  // tiles this CTA finalized (fused CG tail)
+  __shared__ double shx[8];
+  if (tid == 0) nfin = 0;
 
   if (warp == kWarps) {
     // ------------------------------------------------ producer warp (TMA)
@@ -743,11 +883,13 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
       if (i == i1 && tid == 0) SNX_TL(1, 5);
       if (last_tile) {
         tile_finalize<K, TCOL>(a, ftile, G, shd);
+        if (tid == 0) fin_tiles[nfin++] = ftile;
         consumer_sync(kConsumers);
         if (i == i1 && tid == 0) SNX_TL(1, 6);
       }
     }
     if (i == i1) {
+      if (a.cg_state != nullptr && nfin > 0) cg_tail<K, TCOL>(a, fin_tiles, nfin, shd, shx);
       if (tid == 0) SNX_TL(1, 3);
       break;
     }
@@ -794,7 +936,11 @@ __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constan
   // launched as a programmatic dependent of GEMM1: everything read here was
   // complete before GEMM1 started, except the U rows -- the producer waits
   // for GEMM1 (griddepcontrol.wait) right before its first U load
-  if (a.skip != nullptr && *a.skip != 0.0) return;
+  if (a.skip != nullptr && *a.skip != 0.0) {
+    if (a.cg_state != nullptr && blockIdx.x == 0 && threadIdx.x < SNX_CG_SLOT)  // cg_step2 on a done slot
+      slot(a.cg_state, a.cg_t + 1)[threadIdx.x] = slot(a.cg_state, a.cg_t)[threadIdx.x];
+    return;
+  }
   using Sh = G2Shape<T, K>;
   constexpr int S = Sh::S;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -1459,12 +1605,17 @@ int validate(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
 }
 
 // Common driver of the row-pass entry points (rows contiguous).
+struct CgFuse {  // snx_hess_apply_cg: the CG iteration fused into GEMM2's tail
+  double *state, *r, *p, *pb;
+  int t, T;
+};
+
 static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
                    int32_t K, const int32_t *labels, const double *w, const double *dir,
                    double alpha, const void *H, void *rowout, double scale, double lam,
                    const double *base, double *out, long long *corr_out, double *vec_out,
                    double *dots, const double *skip, void *ws, size_t ws_bytes,
-                   cudaStream_t st) {
+                   cudaStream_t st, const CgFuse *cg = nullptr) {
   if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
   const int32_t P = padded(p);
   const Geometry g = geometry(dtype, nrows, P, K);
@@ -1550,6 +1701,15 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   b.base = base;
   b.out = vec_out;
   b.dots = dots;
+  if (cg != nullptr) {
+    b.cg_state = cg->state;
+    b.cg_r = cg->r;
+    b.cg_p = cg->p;
+    b.cg_pb = cg->pb;
+    b.cg_sync = counters + 6;  // [3]
+    b.cg_t = cg->t;
+    b.cg_T = cg->T;
+  }
   if (dtype == SNX_F64) {
     SNX_K_SWITCH(K, (rc = launch_gemm2<double, KK>(b, g.grid2, st)));
   } else {
@@ -1772,6 +1932,33 @@ int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
   return rowpass(kHessPrep, dtype, Xs, lds, nrows, p, K, nullptr, w, nullptr, 0.0, nullptr,
                  H_out, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ws,
                  ws_bytes, st);
+}
+
+int snx_hess_apply_cg(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p,
+                      int32_t K, const void *H, double scale, double lam, int32_t t,
+                      int32_t max_iters, double *r, double *s, double *p_vec, double *p_best,
+                      double *Hs, double *dots, double *state, void *ws, size_t ws_bytes,
+                      void *stream) {
+  if (s == nullptr || Hs == nullptr || dots == nullptr || state == nullptr || r == nullptr ||
+      p_vec == nullptr || p_best == nullptr || (nrows > 0 && H == nullptr)) {
+    set_error("snx_hess_apply_cg: NULL argument");
+    return 1;
+  }
+  if (t < 0 || t >= max_iters) {
+    set_error("snx_hess_apply_cg: iteration %d outside [0, %d)", t, max_iters);
+    return 1;
+  }
+  if (nrows == 0) {  // no GEMM2 to fuse into: the separate update
+    if (snx_hess_apply(dtype, Xs, ldx, nrows, p, K, H, s, scale, lam, Hs, dots,
+                       snx_cg_done_flag(state, t), ws, ws_bytes, stream))
+      return 1;
+    return snx_cg_update(t, max_iters, (int64_t)K * p, Hs, dots, r, s, p_vec, p_best, state,
+                         stream);
+  }
+  const CgFuse cg{state, r, p_vec, p_best, t, max_iters};
+  return rowpass(kHessApply, dtype, Xs, ldx, nrows, p, K, nullptr, s, nullptr, 0.0, H, nullptr,
+                 scale, lam, s, nullptr, nullptr, Hs, dots, snx_cg_done_flag(state, t), ws,
+                 ws_bytes, (cudaStream_t)stream, &cg);
 }
 
 int snx_cg_solve(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,

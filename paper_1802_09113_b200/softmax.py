@@ -185,6 +185,25 @@ class HessianOperator:
                       ptr(dots), skip, *_ws(self.view), stream_handle())
         return out
 
+    def apply_cg_into(self, t, T, ws):
+        """Hs = H s and CG iteration t fused (snx_hess_apply_cg, fp64 data) when
+        SNX_CG_FUSED=1; False -> the caller runs apply_into + snx_cg_update.
+
+        Opt-in: measured slower on B200 (455 vs 423 us per 10-product CIFAR
+        solve) -- the tile finalizers' two waits for every other tile cost more
+        than the two ~1 us kernel boundaries they remove."""
+        hb, view = self._bufs, self.view
+        if hb.xs_tc is not None or os.environ.get("SNX_CG_FUSED", "0") != "1":
+            return False
+        if hb.owner is not self:
+            self._prepare()
+        base = view.base
+        _lib.call("snx_hess_apply_cg", base.code, ptr(hb.xs), base.ld, view.n_rows, self.p,
+                  view.K, ptr(hb.h), self.scale, self.lam, t, T, ptr(ws.r), ptr(ws.s),
+                  ptr(ws.p), ptr(ws.pb), ptr(ws.Hs), ptr(ws.dots), ptr(ws.state), *_ws(view),
+                  stream_handle())
+        return True
+
     def cg_solve_into(self, g, theta, T, ws):
         """Enqueue the whole CG solve as one persistent kernel (snx_cg_solve,
         fp64 data) when SNX_CG_PERSISTENT=1; False -> the per-iteration path.
