@@ -63,6 +63,7 @@ struct TcGeometry {
   int maxseg2;
 };
 TcGeometry tc_geometry(int64_t nrows, int32_t P);
+int tc_kp(int32_t K);  // classes padded for the tensor-core operands (16 or a multiple of 16)
 int sk_maxseg(int64_t items, int grid, int per_group);
 int sm_count();
 

@@ -1503,8 +1503,9 @@ Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K) {
   w.dot_part = take((size_t)4 * kDotBlocks * 8);
   if (dtype == SNX_F32) {  // tensor-core Hessian product (snx_tc.cu)
     const TcGeometry t = tc_geometry(nrows, P);
-    w.tc_b = take((size_t)32 * round_up((size_t)P, 8) * 2);
-    w.tc_ut = take((size_t)32 * round_up((size_t)nr, 8) * 2);
+    const size_t kp2 = 2 * (size_t)tc_kp(K);  // [B1 ; B2] rows
+    w.tc_b = take(kp2 * round_up((size_t)P, 8) * 2);
+    w.tc_ut = take(kp2 * round_up((size_t)nr, 8) * 2);
     w.tc_zp = take((size_t)(t.row_blocks > 0 ? t.row_blocks : 1) * t.maxseg1 * 128 * K * 8);
     w.tc_gp = take((size_t)t.col_tiles * t.maxseg2 * K * 128 * 8);
   }

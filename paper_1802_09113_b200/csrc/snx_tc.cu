@@ -42,7 +42,7 @@ int make_tmap_bf16(CUtensorMap *m, const void *base, uint64_t cols, uint64_t row
                    uint32_t box_cols, uint32_t box_rows);
 
 #ifdef SNX_TIMELINE
-__device__ unsigned long long g_tc_timeline[2][160][4];
+__device__ unsigned long long g_tc_timeline[2][160][8];
 #define SNX_TC_TL(slot, ev)                                                \
   do {                                                                     \
     unsigned long long t_;                                                 \
@@ -79,6 +79,13 @@ __device__ __forceinline__ void split_bf16(double x, __nv_bfloat16 &x1, __nv_bfl
   x2 = __double2bfloat16(x - (double)__bfloat162float(x1));
 }
 
+// The same split of an f32 value with the native f32 -> bf16 conversions
+// (the double -> bf16 path is emulated; the epilogues' U values only need f32).
+__device__ __forceinline__ void split_bf16f(float x, __nv_bfloat16 &x1, __nv_bfloat16 &x2) {
+  x1 = __float2bfloat16_rn(x);
+  x2 = __float2bfloat16_rn(x - __bfloat162float(x1));
+}
+
 struct Tc1Args {
   CUtensorMap xmap;   // X1 [nrows][PB] bf16: boxes 64 cols x 128 rows, 128-B swizzle
   CUtensorMap lmap;   // X2: same
@@ -93,6 +100,9 @@ struct Tc1Args {
   double *zp;         // [row_blocks][maxseg][K][128] segment partials
   unsigned *rb_count; // [row_blocks] arrivals (zero at rest)
   const double *skip;
+  int K;              // classes (wide kernels; the K <= 16 kernels take it as a template)
+  int prep;           // wide GEMM1: 1 = write the probabilities h (HessianOperator init)
+  float *hout;        // [nrows][K] (prep)
 };
 
 struct Tc2Args {
@@ -111,19 +121,22 @@ struct Tc2Args {
   double *out;        // Hv, flat class-major
   double *dots;       // nullable: [tile] v.Hv, [kDotBlocks + tile] v.v partials
   const double *skip;
+  int K;
 };
 
-struct Barriers {
-  uint64_t full[kS], empty[kS], accf[2], acce[2];
+template <int S> struct BarT {
+  uint64_t full[S], empty[S], accf[2], acce[2];
   uint32_t tbase;
   int flag;
   double red[4];
 };
+using Barriers = BarT<kS>;
 
-__device__ __forceinline__ void setup(Barriers &b, int warp) {
+template <int S>
+__device__ __forceinline__ void setup(BarT<S> &b, int warp, uint32_t tmem_cols = kTmemCols) {
   if (threadIdx.x == 0) {
 #pragma unroll
-    for (int s = 0; s < kS; ++s) {
+    for (int s = 0; s < S; ++s) {
       mbar_init(&b.full[s], 1);
       mbar_init(&b.empty[s], 1);
     }
@@ -134,18 +147,19 @@ __device__ __forceinline__ void setup(Barriers &b, int warp) {
     }
     mbar_fence_init();
   }
-  if (warp == 1) umma::tmem_alloc(&b.tbase, kTmemCols);
+  if (warp == 1) umma::tmem_alloc(&b.tbase, tmem_cols);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
 }
 
-__device__ __forceinline__ void teardown(Barriers &b, int warp) {
+template <int S>
+__device__ __forceinline__ void teardown(BarT<S> &b, int warp, uint32_t tmem_cols = kTmemCols) {
   umma::fence_before();
   __syncthreads();
   if (warp == 1) {
     umma::fence_after();
-    umma::tmem_dealloc(b.tbase, kTmemCols);
+    umma::tmem_dealloc(b.tbase, tmem_cols);
   }
 }
 
@@ -191,12 +205,15 @@ __device__ __forceinline__ void seg_sum(const double *base, int64_t seg_stride, 
   }
 }
 
-// MMA issuer loop (one thread).  kAmn selects the MN-major A layout (GEMM2).
-template <bool kAmn, int kSlot, typename SegStart, typename SegEnd>
-__device__ __forceinline__ void mma_loop(Barriers &b, uint8_t *sm, int64_t i0, int64_t i1,
+// MMA issuer loop (one thread).  kAmn selects the MN-major A layout (GEMM2);
+// N1 = rows of the stacked [B1 ; B2] operand (2 KP), accumulator buffers N1
+// TMEM columns apart; stage = X1 (16 KB), X2 (16 KB), B.
+template <bool kAmn, int kSlot, int S, uint32_t STAGE, int N1, typename SegStart,
+          typename SegEnd>
+__device__ __forceinline__ void mma_loop(BarT<S> &b, uint8_t *sm, int64_t i0, int64_t i1,
                                          SegStart seg_start, SegEnd seg_end) {
-  constexpr uint32_t id32 = umma::idesc_bf16(128, 32, kAmn, false);
-  constexpr uint32_t id16 = umma::idesc_bf16(128, 16, kAmn, false);
+  constexpr uint32_t idN1 = umma::idesc_bf16(128, N1, kAmn, false);
+  constexpr uint32_t idN2 = umma::idesc_bf16(128, N1 / 2, kAmn, false);
   int nseg = 0;
   for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
     const bool first = i == i0 || seg_start(i);
@@ -205,12 +222,12 @@ __device__ __forceinline__ void mma_loop(Barriers &b, uint8_t *sm, int64_t i0, i
       mbar_wait(&b.acce[buf], (unsigned)(((nseg >> 1) & 1) ^ 1));
       umma::fence_after();
     }
-    const int s = (int)(it % kS);
-    mbar_wait(&b.full[s], (unsigned)((it / kS) & 1));
+    const int s = (int)(it % S);
+    mbar_wait(&b.full[s], (unsigned)((it / S) & 1));
     umma::fence_after();
     if (it == 0) SNX_TC_TL(kSlot, 1);
-    const uint32_t st = umma::smem_u32(sm + s * kStage);
-    const uint32_t d = b.tbase + (uint32_t)(buf * 32);
+    const uint32_t st = umma::smem_u32(sm + s * STAGE);
+    const uint32_t d = b.tbase + (uint32_t)(buf * N1);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {  // 16 K-elements per MMA
       uint64_t a1, a2;
@@ -222,8 +239,8 @@ __device__ __forceinline__ void mma_loop(Barriers &b, uint8_t *sm, int64_t i0, i
         a2 = umma::desc_k_sw128(st + kXB + k * 32);
       }
       const uint64_t bd = umma::desc_k_sw128(st + 2 * kXB + k * 32);
-      umma::mma_bf16(d, a1, bd, id32, (first && k == 0) ? 0u : 1u);  // A1.[B1 | B2]
-      umma::mma_bf16(d, a2, bd, id16, 1u);                            // + A2.B1
+      umma::mma_bf16(d, a1, bd, idN1, (first && k == 0) ? 0u : 1u);  // A1.[B1 | B2]
+      umma::mma_bf16(d, a2, bd, idN2, 1u);                            // + A2.B1
     }
     umma::commit(&b.empty[s]);  // stage free once these MMAs completed
     if (i + 1 == i1 || seg_end(i)) {
@@ -268,7 +285,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm1_kernel(const __grid_cons
     }
   } else if (warp == 1) {
     if (lane == 0)
-      mma_loop<false, 0>(
+      mma_loop<false, 0, kS, kStage, 32>(
           b, sm, i0, i1, [&](int64_t i) { return i % nk == 0; },
           [&](int64_t i) { return (i + 1) % nk == 0; });
     __syncwarp();
@@ -314,7 +331,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm1_kernel(const __grid_cons
 #pragma unroll
         for (int c = 0; c < K; ++c) {
           __nv_bfloat16 u1, u2;
-          split_bf16(vw[c] - hw[c] * s, u1, u2);
+          split_bf16f((float)(vw[c] - hw[c] * s), u1, u2);
           a.ut[(int64_t)c * a.ldu + r] = u1;
           a.ut[(int64_t)(16 + c) * a.ldu + r] = u2;
         }
@@ -366,7 +383,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm2_kernel(const __grid_cons
     }
   } else if (warp == 1) {
     if (lane == 0)
-      mma_loop<true, 1>(
+      mma_loop<true, 1, kS, kStage, 32>(
           b, sm, i0, i1, [&](int64_t i) { return i % rch == 0; },
           [&](int64_t i) { return (i + 1) % rch == 0; });
     __syncwarp();
@@ -438,17 +455,18 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm2_kernel(const __grid_cons
 }
 
 // [Q1 ; Q2] from v (class-major d = K*p, fp64): rows c < K: bf16 split of
-// v[c*p + j]; other rows and columns >= p zero.
-__global__ void tc_prep_b_kernel(const double *__restrict__ v, int K, int p, int PB,
+// v[c*p + j] (Q1 in rows [0, KP), Q2 in rows [KP, 2 KP)); other rows and
+// columns >= p zero.
+__global__ void tc_prep_b_kernel(const double *__restrict__ v, int K, int p, int PB, int KP,
                                  __nv_bfloat16 *__restrict__ B) {
-  const int64_t n = (int64_t)16 * PB;
+  const int64_t n = (int64_t)KP * PB;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(e / PB), j = (int)(e - (int64_t)c * PB);
     __nv_bfloat16 x1 = __float2bfloat16(0.0f), x2 = x1;
     if (c < K && j < p) split_bf16(v[(int64_t)c * p + j], x1, x2);
     B[e] = x1;
-    B[e + (int64_t)16 * PB] = x2;
+    B[e + n] = x2;
   }
 }
 
@@ -469,6 +487,368 @@ __global__ void tc_split_kernel(const float *__restrict__ X, int64_t ldx, int64_
   }
 }
 
+// ---------------------------------------------------------------- wide K
+// 16 < K <= 128 (C up to 129): the same two GEMMs with the stacked operand
+// [B1 ; B2] of 2 KP rows (KP = K rounded up to 16; MMA N = 2 KP <= 256 and
+// KP), double-buffered 2 x 2 KP TMEM columns, 2 stages.  The epilogues move
+// the accumulators out in 16-class chunks; the last segment of a GEMM1 row
+// block keeps the row's V in shared memory for the row algebra (ComputeU, or
+// the softmax probabilities when preparing h).
+template <int KP> struct WShape {
+  static constexpr int N1 = 2 * KP;
+  static constexpr uint32_t BB = (uint32_t)N1 * 128;
+  static constexpr uint32_t STAGE = 2 * kXB + BB;
+  static constexpr int S = 2;
+  static constexpr int VS = 129;                    // V row stride (conflict-free columns)
+  static constexpr uint32_t VB = (uint32_t)VS * KP * 4u;  // f32 V[c][row]
+  static constexpr size_t SMEM = (size_t)S * STAGE + VB + 1024;
+  static constexpr uint32_t TMEM = 4 * KP <= 64 ? 64 : 4 * KP <= 128 ? 128 : 4 * KP <= 256 ? 256 : 512;
+};
+
+template <int KP>
+__global__ void __launch_bounds__(kThreads, 1) tcw_gemm1_kernel(const __grid_constant__ Tc1Args a) {
+  pdl_trigger();
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  using W = WShape<KP>;
+  extern __shared__ uint8_t smraw[];
+  uint8_t *sm = align1024(smraw);
+  float *vsm = reinterpret_cast<float *>(sm + W::S * W::STAGE);
+  __shared__ BarT<W::S> b;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
+  if (i0 == i1) return;
+  if (tid == 0) SNX_TC_TL(0, 0);
+  setup(b, warp, W::TMEM);
+  const int nk = a.nk, K = a.K;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&a.xmap);
+      tma_prefetch_desc(&a.lmap);
+      tma_prefetch_desc(&a.bmap);
+      for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
+        const int s = (int)(it % W::S);
+        mbar_wait(&b.empty[s], (unsigned)(((it / W::S) & 1) ^ 1));
+        mbar_arrive_expect_tx(&b.full[s], W::STAGE);
+        uint8_t *st = sm + s * W::STAGE;
+        const int rb = (int)(i / nk), kt = (int)(i - (int64_t)rb * nk);
+        tma_load_2d(st, &a.xmap, kt * kKT, rb * 128, &b.full[s]);
+        tma_load_2d(st + kXB, &a.lmap, kt * kKT, rb * 128, &b.full[s]);
+        tma_load_2d(st + 2 * kXB, &a.bmap, kt * kKT, 0, &b.full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0)
+      mma_loop<false, 0, W::S, W::STAGE, W::N1>(
+          b, sm, i0, i1, [&](int64_t i) { return i % nk == 0; },
+          [&](int64_t i) { return (i + 1) % nk == 0; });
+    __syncwarp();
+  } else {
+    const int row = (warp & 3) * 32 + lane;
+    const int et = tid - 64;
+    int n = 0;
+    for (int64_t rb = i0 / nk; rb <= (i1 - 1) / nk; ++rb, ++n) {
+      const int buf = n & 1;
+      const int64_t r = rb * 128 + row;
+      const int c_lo = sk_owner(a.items, G, rb * nk);
+      const int nseg = sk_owner(a.items, G, (rb + 1) * nk - 1) - c_lo + 1;
+      double *zrow = a.zp + ((rb * a.maxseg + (cta - c_lo)) * K) * 128 + row;
+      mbar_wait(&b.accf[buf], (unsigned)((n >> 1) & 1));
+      umma::fence_after();
+      const uint32_t t = b.tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(buf * W::N1);
+#pragma unroll 1
+      for (int cc = 0; cc < KP; cc += 16) {
+        float hi[16], lo[16];
+        umma::tmem_ld16(t + cc, hi);
+        umma::tmem_ld16(t + KP + cc, lo);
+        if (r < a.nrows) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (cc + j < K) zrow[(cc + j) * 128] = (double)hi[j] + (double)lo[j];
+        }
+      }
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&b.acce[buf]);
+      epi_sync();
+      if (et == 0) {
+        const unsigned prev = atomic_add_acq_rel(&a.rb_count[rb], 1u);
+        b.flag = prev == (unsigned)(nseg - 1);
+        if (b.flag) a.rb_count[rb] = 0u;
+      }
+      epi_sync();
+      if (b.flag) {
+        // last segment of this row block: the row's V (fixed-order segment
+        // sums, 16 classes x kSegBatch segments of loads in flight) into smem
+        const double *z0 = a.zp + (rb * a.maxseg * K) * 128 + row;
+#pragma unroll 1
+        for (int cc = 0; cc < K; cc += 16) {
+          double acc[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+          for (int s0 = 0; s0 < nseg; s0 += kSegBatch) {
+            double v[kSegBatch][16];
+#pragma unroll
+            for (int q = 0; q < kSegBatch; ++q)
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                v[q][j] = (s0 + q < nseg && cc + j < K)
+                              ? __ldcg(z0 + ((int64_t)(s0 + q) * K + cc + j) * 128)
+                              : 0.0;
+#pragma unroll
+            for (int q = 0; q < kSegBatch; ++q)
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (s0 + q < nseg) acc[j] += v[q][j];
+          }
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (cc + j < K) vsm[(cc + j) * W::VS + row] = (float)acc[j];
+        }
+        epi_sync();  // every row's V is in smem
+        if (et == 0) SNX_TC_TL(0, 4);
+        // row algebra with lanes over classes (coalesced h loads / h stores,
+        // fixed-order butterfly row reductions), each warp 32 rows, loads of
+        // 4 rows in flight; compact code (the kernel is instruction-cache bound
+        // if this loop is unrolled)
+        const int wq = warp & 3;
+        constexpr int kR = 4, kC = KP / 32 + (KP % 32 ? 1 : 0);
+        if (a.prep) {
+#pragma unroll 1
+          for (int rq = wq * 32; rq < wq * 32 + 32; ++rq) {
+            const int64_t rr = rb * 128 + rq;
+            if (rr >= a.nrows) break;
+            // softmax.py:91-98 and :189-195: h = E / alpha
+            float z[kC];
+            double M = 0.0;
+#pragma unroll
+            for (int k = 0; k < kC; ++k) {
+              const int c = lane + 32 * k;
+              z[k] = c < K ? vsm[c * W::VS + rq] : 0.0f;
+              if (c < K) M = ((double)z[k] > M || isnan(z[k])) ? (double)z[k] : M;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const double t2 = __shfl_xor_sync(0xffffffffu, M, o);
+              M = (t2 > M || isnan(t2)) ? t2 : M;
+            }
+            double e[kC], se = 0.0;
+#pragma unroll
+            for (int k = 0; k < kC; ++k) {
+              e[k] = lane + 32 * k < K ? exp((double)z[k] - M) : 0.0;
+              se += e[k];
+            }
+            const double alpha = exp(-M) + warp_allsum(se);
+#pragma unroll
+            for (int k = 0; k < kC; ++k)
+              if (lane + 32 * k < K) a.hout[rr * K + lane + 32 * k] = (float)(e[k] / alpha);
+          }
+        } else {
+#pragma unroll 1
+          for (int r0 = wq * 32; r0 < wq * 32 + 32; r0 += kR) {
+            float hh[kR][kC];
+#pragma unroll
+            for (int q = 0; q < kR; ++q)
+#pragma unroll
+              for (int k = 0; k < kC; ++k) {
+                const int c = lane + 32 * k;
+                const int64_t rr = rb * 128 + r0 + q;
+                hh[q][k] = (c < K && rr < a.nrows) ? a.H[rr * K + c] : 0.0f;
+              }
+#pragma unroll 1
+            for (int q = 0; q < kR; ++q) {
+              // softmax.py:206-208: U = V*W - W*rowsum(V*W), back into smem
+              double vw[kC], sv = 0.0;
+#pragma unroll
+              for (int k = 0; k < kC; ++k) {
+                const int c = lane + 32 * k;
+                vw[k] = c < K ? (double)vsm[c * W::VS + r0 + q] * (double)hh[q][k] : 0.0;
+                sv += vw[k];
+              }
+              const double srow = warp_allsum(sv);
+#pragma unroll
+              for (int k = 0; k < kC; ++k)
+                if (lane + 32 * k < K)
+                  vsm[(lane + 32 * k) * W::VS + r0 + q] =
+                      (float)(vw[k] - (double)hh[q][k] * srow);
+            }
+          }
+        }
+        epi_sync();
+        if (et == 0) SNX_TC_TL(0, 5);
+        if (!a.prep) {
+          // [U1^T ; U2^T]: tasks (class, 8-row group), one 16-B store per term
+          const int64_t rbase = rb * 128;
+          const int nr = (int)min((int64_t)128, a.nrows - rbase);
+          for (int task = et; task < K * 16; task += 128) {
+            const int c = task >> 4, g8 = (task & 15) * 8;
+            if (g8 >= nr) continue;
+            union {
+              uint4 v;
+              __nv_bfloat16 h[8];
+            } p1, p2;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float u = g8 + q < nr ? vsm[c * W::VS + g8 + q] : 0.0f;
+              split_bf16f(u, p1.h[q], p2.h[q]);
+            }
+            // rows past nrows land in ut's padding (ldu is a multiple of 8)
+            *reinterpret_cast<uint4 *>(a.ut + (int64_t)c * a.ldu + rbase + g8) = p1.v;
+            *reinterpret_cast<uint4 *>(a.ut + (int64_t)(KP + c) * a.ldu + rbase + g8) = p2.v;
+          }
+        }
+        if (et == 0) SNX_TC_TL(0, 6);
+      }
+      epi_sync();
+      if (et == 0 && b.flag) SNX_TC_TL(0, 7);
+    }
+    if (et == 0) SNX_TC_TL(0, 3);
+  }
+  teardown(b, warp, W::TMEM);
+}
+
+template <int KP>
+__global__ void __launch_bounds__(kThreads, 1) tcw_gemm2_kernel(const __grid_constant__ Tc2Args a) {
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  using W = WShape<KP>;
+  extern __shared__ uint8_t smraw[];
+  uint8_t *sm = align1024(smraw);
+  __shared__ BarT<W::S> b;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
+  if (i0 == i1) return;
+  if (tid == 0) SNX_TC_TL(1, 0);
+  setup(b, warp, W::TMEM);
+  const int rch = a.rchunks, K = a.K;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tma_prefetch_desc(&a.xmap);
+      tma_prefetch_desc(&a.lmap);
+      tma_prefetch_desc(&a.umap);
+      for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
+        const int s = (int)(it % W::S);
+        mbar_wait(&b.empty[s], (unsigned)(((it / W::S) & 1) ^ 1));
+        mbar_arrive_expect_tx(&b.full[s], W::STAGE);
+        uint8_t *st = sm + s * W::STAGE;
+        const int tile = (int)(i / rch), rc = (int)(i - (int64_t)tile * rch);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          tma_load_2d(st + q * 8192, &a.xmap, tile * 128 + q * 64, rc * kKT, &b.full[s]);
+          tma_load_2d(st + kXB + q * 8192, &a.lmap, tile * 128 + q * 64, rc * kKT, &b.full[s]);
+        }
+        if (it == 0) pdl_wait();
+        tma_load_2d(st + 2 * kXB, &a.umap, rc * kKT, 0, &b.full[s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0)
+      mma_loop<true, 1, W::S, W::STAGE, W::N1>(
+          b, sm, i0, i1, [&](int64_t i) { return i % rch == 0; },
+          [&](int64_t i) { return (i + 1) % rch == 0; });
+    __syncwarp();
+  } else {
+    const int col = (warp & 3) * 32 + lane;
+    const int et = tid - 64;
+    int n = 0;
+    for (int64_t tile = i0 / rch; tile <= (i1 - 1) / rch; ++tile, ++n) {
+      const int buf = n & 1;
+      const int c_lo = sk_owner(a.items, G, tile * rch);
+      const int nseg = sk_owner(a.items, G, (tile + 1) * rch - 1) - c_lo + 1;
+      double *g = a.gp + ((tile * a.maxseg + (cta - c_lo)) * K) * 128 + col;
+      mbar_wait(&b.accf[buf], (unsigned)((n >> 1) & 1));
+      umma::fence_after();
+      const uint32_t t = b.tbase + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(buf * W::N1);
+#pragma unroll 1
+      for (int cc = 0; cc < KP; cc += 16) {
+        float hi[16], lo[16];
+        umma::tmem_ld16(t + cc, hi);
+        umma::tmem_ld16(t + KP + cc, lo);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (cc + j < K) g[(cc + j) * 128] = (double)hi[j] + (double)lo[j];
+      }
+      umma::fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&b.acce[buf]);
+      epi_sync();
+      if (et == 0) {
+        const unsigned prev = atomic_add_acq_rel(&a.tile_count[tile], 1u);
+        b.flag = prev == (unsigned)(nseg - 1);
+        if (b.flag) a.tile_count[tile] = 0u;
+      }
+      epi_sync();
+      if (b.flag) {
+        const int j = (int)tile * 128 + col;
+        double bo = 0.0, bb = 0.0;
+        if (j < a.p) {
+          const double *g0 = a.gp + (tile * a.maxseg * K) * 128 + col;
+#pragma unroll 1
+          for (int cc = 0; cc < K; cc += 16) {
+            double acc[16], vcs[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) {
+              acc[q] = 0.0;
+              vcs[q] = cc + q < K ? a.v[(int64_t)(cc + q) * a.p + j] : 0.0;
+            }
+            for (int s0 = 0; s0 < nseg; s0 += kSegBatch) {
+              double v[kSegBatch][16];
+#pragma unroll
+              for (int q = 0; q < kSegBatch; ++q)
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                  v[q][jj] = (s0 + q < nseg && cc + jj < K)
+                                 ? __ldcg(g0 + ((int64_t)(s0 + q) * K + cc + jj) * 128)
+                                 : 0.0;
+#pragma unroll
+              for (int q = 0; q < kSegBatch; ++q)
+#pragma unroll
+                for (int jj = 0; jj < 16; ++jj)
+                  if (s0 + q < nseg) acc[jj] += v[q][jj];
+            }
+#pragma unroll
+            for (int jj = 0; jj < 16; ++jj) {
+              const int c = cc + jj;
+              if (c < K) {
+                const double vc = vcs[jj];
+                const double o = __dadd_rn(__dmul_rn(a.scale, acc[jj]), __dmul_rn(a.lam, vc));
+                a.out[(int64_t)c * a.p + j] = o;
+                bo += vc * o;
+                bb += vc * vc;
+              }
+            }
+          }
+        }
+        if (a.dots != nullptr) {
+          bo = warp_allsum(bo);
+          bb = warp_allsum(bb);
+          if (lane == 0) b.red[warp & 3] = bo;
+          epi_sync();
+          double so = 0.0;
+          if (et == 0) so = ((b.red[0] + b.red[1]) + b.red[2]) + b.red[3];
+          epi_sync();
+          if (lane == 0) b.red[warp & 3] = bb;
+          epi_sync();
+          if (et == 0) {
+            a.dots[tile] = so;
+            a.dots[kDotBlocks + tile] = ((b.red[0] + b.red[1]) + b.red[2]) + b.red[3];
+          }
+          if (tile == 0)
+            for (int tt = a.col_tiles + et; tt < kDotBlocks; tt += 128) {
+              a.dots[tt] = 0.0;
+              a.dots[kDotBlocks + tt] = 0.0;
+            }
+        }
+      }
+      epi_sync();
+    }
+    if (et == 0) SNX_TC_TL(1, 3);
+  }
+  teardown(b, warp, W::TMEM);
+}
+
 // GEMM2 overlaps its prologue and first X tiles with GEMM1's tail through
 // programmatic dependent launch (SNX_TC_PDL=0 disables).
 bool tc_pdl() {
@@ -482,18 +862,18 @@ bool tc_pdl() {
 
 template <typename ArgT>
 int launch_tc(void (*kernel)(ArgT), int grid, const ArgT &args, cudaStream_t st,
-              size_t *configured, const char *what, bool pdl) {
-  if (kSmem > *configured) {
-    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmem) !=
+              size_t *configured, const char *what, bool pdl, size_t smem = kSmem) {
+  if (smem > *configured) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
         cudaSuccess)
       return check_launch(what);
-    *configured = kSmem;
+    *configured = smem;
   }
   carveout(kernel);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = kSmem;
+  cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -511,9 +891,37 @@ int run_tc(const Tc1Args &a1, int g1, const Tc2Args &a2, int g2, cudaStream_t st
   return launch_tc(tc_gemm2_kernel<K>, g2, a2, st, &c2, "tc_gemm2", tc_pdl());
 }
 
+// wide K: GEMM1 alone (prep) or GEMM1 + GEMM2 (apply)
+template <int KP>
+int run_tcw(const Tc1Args &a1, int g1, const Tc2Args *a2, int g2, cudaStream_t st) {
+  static size_t c1 = 0, c2 = 0;
+  if (launch_tc(tcw_gemm1_kernel<KP>, g1, a1, st, &c1, "tcw_gemm1", false, WShape<KP>::SMEM))
+    return 1;
+  if (a2 == nullptr) return 0;
+  return launch_tc(tcw_gemm2_kernel<KP>, g2, *a2, st, &c2, "tcw_gemm2", tc_pdl(),
+                   WShape<KP>::SMEM);
+}
+
+int dispatch_wide(int KP, const Tc1Args &a1, int g1, const Tc2Args *a2, int g2,
+                  cudaStream_t st) {
+  switch (KP) {
+    case 32: return run_tcw<32>(a1, g1, a2, g2, st);
+    case 48: return run_tcw<48>(a1, g1, a2, g2, st);
+    case 64: return run_tcw<64>(a1, g1, a2, g2, st);
+    case 80: return run_tcw<80>(a1, g1, a2, g2, st);
+    case 96: return run_tcw<96>(a1, g1, a2, g2, st);
+    case 112: return run_tcw<112>(a1, g1, a2, g2, st);
+    case 128: return run_tcw<128>(a1, g1, a2, g2, st);
+    default:
+      set_error("snx: no tensor-core kernel for KP=%d", KP);
+      return 1;
+  }
+}
+
 }  // namespace
 
 int64_t tc_ld(int32_t p) { return (p + 7) / 8 * 8; }  // bf16 rows: 16-B multiple
+int tc_kp(int32_t K) { return K <= 16 ? 16 : (K + 15) / 16 * 16; }  // padded classes
 
 TcGeometry tc_geometry(int64_t nrows, int32_t P) {
   TcGeometry t{};
@@ -537,10 +945,12 @@ static int tc_apply(const void *X1, const void *X2, int64_t ldb, int64_t nrows, 
                     double *out, double *dots, const double *skip, void *ws, size_t ws_bytes,
                     cudaStream_t st) {
   const int64_t PB = tc_ld(p);
-  if (K < 1 || K > 16 || p < 1 || nrows < 0) {
-    set_error("snx_hess_apply_tc: K=%d (need 1..16), p=%d, nrows=%lld", K, p, (long long)nrows);
+  if (K < 1 || K > 128 || p < 1 || nrows < 0) {
+    set_error("snx_hess_apply_tc: K=%d (need 1..128), p=%d, nrows=%lld", K, p,
+              (long long)nrows);
     return 1;
   }
+  const int KP = tc_kp(K);
   if (ldb < PB || ldb % 8 != 0) {
     set_error("snx_hess_apply_tc: ldb=%lld needs >= round_up(p, 8) and %% 8 == 0",
               (long long)ldb);
@@ -567,13 +977,13 @@ static int tc_apply(const void *X1, const void *X2, int64_t ldb, int64_t nrows, 
   __nv_bfloat16 *B = reinterpret_cast<__nv_bfloat16 *>(wsb + lay.tc_b);
   __nv_bfloat16 *UT = reinterpret_cast<__nv_bfloat16 *>(wsb + lay.tc_ut);
   const int64_t ldu = tc_ld((int32_t)nrows);
-  tc_prep_b_kernel<<<64, 256, 0, st>>>(v, K, p, (int)PB, B);
+  tc_prep_b_kernel<<<64, 256, 0, st>>>(v, K, p, (int)PB, KP, B);
   if (check_launch("tc_prep_b")) return 1;
 
   Tc1Args a1{};
   if (make_tmap_bf16(&a1.xmap, X1, PB, nrows, ldb, kKT, 128) ||
       make_tmap_bf16(&a1.lmap, X2, PB, nrows, ldb, kKT, 128) ||
-      make_tmap_bf16(&a1.bmap, B, PB, 32, PB, kKT, 32))
+      make_tmap_bf16(&a1.bmap, B, PB, 2 * KP, PB, kKT, 2 * KP))
     return 1;
   a1.nrows = nrows;
   a1.nk = t.nk;
@@ -589,7 +999,7 @@ static int tc_apply(const void *X1, const void *X2, int64_t ldb, int64_t nrows, 
   Tc2Args a2{};
   if (make_tmap_bf16(&a2.xmap, X1, PB, nrows, ldb, 64, kKT) ||
       make_tmap_bf16(&a2.lmap, X2, PB, nrows, ldb, 64, kKT) ||
-      make_tmap_bf16(&a2.umap, UT, nrows, 32, ldu, kKT, 32))
+      make_tmap_bf16(&a2.umap, UT, nrows, 2 * KP, ldu, kKT, 2 * KP))
     return 1;
   a2.nrows = nrows;
   a2.rchunks = t.rchunks;
@@ -605,6 +1015,9 @@ static int tc_apply(const void *X1, const void *X2, int64_t ldb, int64_t nrows, 
   a2.out = out;
   a2.dots = dots;
   a2.skip = skip;
+  a1.K = K;
+  a2.K = K;
+  if (KP > 16) return dispatch_wide(KP, a1, t.grid1, &a2, t.grid2, st);
 
   switch (K) {
 #define SNX_TC_CASE(KK) \
@@ -619,6 +1032,12 @@ static int tc_apply(const void *X1, const void *X2, int64_t ldb, int64_t nrows, 
   }
 }
 
+// HessianOperator init for 16 < K <= 128: X1 / X2 of the (gathered) sample,
+// then the wide GEMM1 against [W1 ; W2] with the softmax epilogue -> h.
+static int tc_prepare_wide(const float *Xs, int64_t ld, int64_t nrows, int32_t p, int32_t K,
+                           const double *w, float *H, void *X1, void *X2, int64_t ldb,
+                           void *ws, size_t ws_bytes, cudaStream_t st);
+
 }  // namespace snx
 
 using namespace snx;
@@ -626,7 +1045,7 @@ using namespace snx;
 extern "C" {
 
 #ifdef SNX_TIMELINE
-int snx_debug_tc_timeline(unsigned long long *host_out) {
+int snx_debug_tc_timeline(unsigned long long *host_out) {  // [2][160][8]
   return cudaMemcpyFromSymbol(host_out, g_tc_timeline, sizeof(g_tc_timeline)) == cudaSuccess ? 0
                                                                                              : 1;
 }
@@ -641,6 +1060,23 @@ int snx_hess_prepare_tc(const float *X, int64_t ldx, const int64_t *rows, int64_
   if (nrows > 0 && (X1_out == nullptr || X2_out == nullptr || ldb < tc_ld(p) || ldb % 8 != 0)) {
     set_error("snx_hess_prepare_tc: X1_out / X2_out need ldb >= round_up(p, 8), ldb %% 8 == 0");
     return 1;
+  }
+  if (K > 16) {  // the SIMT row pass stops at K = 16: h from the wide tensor-core GEMM1
+    if (K > 128 || w == nullptr || (nrows > 0 && H_out == nullptr)) {
+      set_error("snx_hess_prepare_tc: K=%d outside [1, 128] or NULL w/H_out", K);
+      return 1;
+    }
+    if (nrows == 0) return 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const float *Xs = X;
+    int64_t ld = ldx;
+    if (rows != nullptr) {
+      if (gather(SNX_F32, X, ldx, nullptr, rows, nrows, Xs_out, ld_out, nullptr, st)) return 1;
+      Xs = Xs_out;
+      ld = ld_out;
+    }
+    return tc_prepare_wide(Xs, ld, nrows, p, K, w, H_out, X1_out, X2_out, ldb, ws, ws_bytes,
+                           st);
   }
   if (snx_hess_prepare(SNX_F32, X, ldx, rows, nrows, p, K, w, Xs_out, ld_out, H_out, ws,
                        ws_bytes, stream))
@@ -669,3 +1105,46 @@ int snx_hess_apply_tc(const void *X1, const void *X2, int64_t ldb, int64_t nrows
 }
 
 }  // extern "C"
+
+namespace snx {
+
+static int tc_prepare_wide(const float *Xs, int64_t ld, int64_t nrows, int32_t p, int32_t K,
+                           const double *w, float *H, void *X1, void *X2, int64_t ldb,
+                           void *ws, size_t ws_bytes, cudaStream_t st) {
+  const int64_t PB = tc_ld(p);
+  const int KP = tc_kp(K);
+  const Workspace lay = workspace_layout(SNX_F32, nrows, p, K);
+  if (ws == nullptr || ws_bytes < lay.total) {
+    set_error("snx: workspace too small (%zu < %zu bytes)", ws_bytes, lay.total);
+    return 1;
+  }
+  const int64_t n = nrows * ldb;
+  const int blocks = (int)((n + 255) / 256 < 8 * sm_count() ? (n + 255) / 256 : 8 * sm_count());
+  tc_split_kernel<<<blocks, 256, 0, st>>>(Xs, ld, nrows, p, ldb,
+                                          static_cast<__nv_bfloat16 *>(X1),
+                                          static_cast<__nv_bfloat16 *>(X2));
+  if (check_launch("tc_split")) return 1;
+  char *wsb = static_cast<char *>(ws);
+  unsigned *counters = reinterpret_cast<unsigned *>(wsb + lay.counters);
+  __nv_bfloat16 *B = reinterpret_cast<__nv_bfloat16 *>(wsb + lay.tc_b);
+  tc_prep_b_kernel<<<64, 256, 0, st>>>(w, K, p, (int)PB, KP, B);
+  if (check_launch("tc_prep_b")) return 1;
+  const TcGeometry t = tc_geometry(nrows, padded(p));
+  Tc1Args a1{};
+  if (make_tmap_bf16(&a1.xmap, X1, PB, nrows, ldb, kKT, 128) ||
+      make_tmap_bf16(&a1.lmap, X2, PB, nrows, ldb, kKT, 128) ||
+      make_tmap_bf16(&a1.bmap, B, PB, 2 * KP, PB, kKT, 2 * KP))
+    return 1;
+  a1.nrows = nrows;
+  a1.nk = t.nk;
+  a1.items = t.items1;
+  a1.maxseg = t.maxseg1;
+  a1.zp = reinterpret_cast<double *>(wsb + lay.tc_zp);
+  a1.rb_count = counters + 16 + SNX_DOT_BLOCKS;
+  a1.K = K;
+  a1.prep = 1;
+  a1.hout = H;
+  return dispatch_wide(KP, a1, t.grid1, nullptr, 0, st);
+}
+
+}  // namespace snx

@@ -31,7 +31,7 @@ buf = (ctypes.c_ulonglong * (3 * 160 * 8))()
 lib = _lib.load()
 if ds.dtype == "f32":  # tensor-core kernels (snx_tc.cu)
     assert lib.snx_debug_tc_timeline(buf) == 0
-    t = np.frombuffer(buf, dtype=np.uint64)[:2 * 160 * 4].reshape(2, 160, 4).astype(np.int64)
+    t = np.frombuffer(buf, dtype=np.uint64)[:2 * 160 * 8].reshape(2, 160, 8).astype(np.int64)
 else:
     assert lib.snx_debug_timeline(buf) == 0
     t = np.frombuffer(buf, dtype=np.uint64).reshape(3, 160, 8).astype(np.int64)

@@ -36,9 +36,9 @@ print(f"cg graph: {e0.elapsed_time(e1) * 1e3:.1f} us, iterations {int(ws.slot(10
 lib = _lib.load()
 rows = []
 if dtype == "f32":
-    b = (ctypes.c_ulonglong * (2 * 160 * 4))()
+    b = (ctypes.c_ulonglong * (2 * 160 * 8))()
     assert lib.snx_debug_tc_timeline(b) == 0
-    t = np.frombuffer(b, dtype=np.uint64).reshape(2, 160, 4).astype(np.int64)
+    t = np.frombuffer(b, dtype=np.uint64).reshape(2, 160, 8).astype(np.int64)
     rows += [("tc_gemm1", t[0, :, 0], t[0, :, 3]), ("tc_gemm2", t[1, :, 0], t[1, :, 3])]
 else:
     b = (ctypes.c_ulonglong * (3 * 160 * 8))()
