@@ -231,6 +231,14 @@ def secondary(snx, torch, args):
         out["cifar10_f32_tensor_core"] = shape_rate(snx, torch, A, y, C, "f32")
         out["cifar10_f32_tensor_core"]["workload"] = (
             "cifar10-shape, f32 data, Hessian GEMMs on tcgen05 (bf16 two-term split), 1e-4 path")
+    # BASELINE config #5 per GPU: a 1M x 3072 f32 shard of the 8M x 3072, C = 100
+    # problem (row-sharded over 8 GPUs; one GPU here), wide tensor-core product
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import large_shard
+
+    res, _, _, _ = large_shard.measure(1_000_000, 10)
+    out["large_c100_shard_f32"] = res
+    torch.cuda.empty_cache()
     # BASELINE config #4: trust region (Steihaug-CG), ill-conditioned CIFAR shape, 10% S_H
     A, y = oracle.synthetic_problem(N, P, C, seed=0, normalize=False, ill_conditioned=True)
     prob = snx.SoftmaxProblem(snx.DeviceDataset.from_numpy(A, y, C), LAM)

@@ -16,66 +16,69 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1802_09113_b200 as snx  # noqa: E402
 from paper_1802_09113_b200 import cg as cgmod, softmax  # noqa: E402
 
-n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
-reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-p, C = 3072, 100
-K = C - 1
-g = torch.Generator(device="cuda").manual_seed(0)
-X = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float32).mul_(1.0 / math.sqrt(n))
-labels = torch.randint(0, C, (n,), generator=g, device="cuda", dtype=torch.int32)
-ds = snx.DeviceDataset(X, labels, C, p, dtype="f32")
-x = 0.05 * torch.randn(K * p, generator=g, device="cuda", dtype=torch.float64)
-v = torch.randn(K * p, generator=g, device="cuda", dtype=torch.float64)
-s_h = snx.draw_samples(snx.SampleConfig(1.0, 0.05), n, 0)[1]
-view = ds.take(s_h)
-m = view.n_rows
-st = torch.cuda.current_stream()
-e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-
-op = softmax.HessianOperator(view, x, 1e-3, scale=n / m)  # warm-up prepare
-torch.cuda.synchronize()
-e0.record(st)
-for _ in range(3):
-    op = softmax.HessianOperator(view, x, 1e-3, scale=n / m)
-e1.record(st)
-torch.cuda.synchronize()
-prep_ms = e0.elapsed_time(e1) / 3
-
-out = torch.empty_like(v)
-for _ in range(3):
-    op.apply_into(v, out)
-torch.cuda.synchronize()
-e0.record(st)
-for _ in range(reps):
-    op.apply_into(v, out)
-e1.record(st)
-torch.cuda.synchronize()
-hv_ms = e0.elapsed_time(e1) / reps
-
-for _ in range(2):
+def measure(n=1_000_000, reps=10, p=3072, C=100, seed=0):
+    """Prepare + Hessian product + 10-product CG on an n x p f32 shard (device data)."""
+    K = C - 1
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    X = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float32)
+    X.mul_(1.0 / math.sqrt(n))
+    labels = torch.randint(0, C, (n,), generator=g, device="cuda", dtype=torch.int32)
+    ds = snx.DeviceDataset(X, labels, C, p, dtype="f32")
+    x = 0.05 * torch.randn(K * p, generator=g, device="cuda", dtype=torch.float64)
+    v = torch.randn(K * p, generator=g, device="cuda", dtype=torch.float64)
+    view = ds.take(snx.draw_samples(snx.SampleConfig(1.0, 0.05), n, 0)[1])
+    m = view.n_rows
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    op = softmax.HessianOperator(view, x, 1e-3, scale=n / m)  # warm-up prepare
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(3):
+        op = softmax.HessianOperator(view, x, 1e-3, scale=n / m)
+    e1.record(st)
+    torch.cuda.synchronize()
+    prep_ms = e0.elapsed_time(e1) / 3
+    out = torch.empty_like(v)
+    for _ in range(3):
+        op.apply_into(v, out)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        op.apply_into(v, out)
+    e1.record(st)
+    torch.cuda.synchronize()
+    hv_ms = e0.elapsed_time(e1) / reps
+    for _ in range(2):
+        ws = cgmod.cg_graph_for(op, 10, 1e-4).run(v)
+    torch.cuda.synchronize()
+    e0.record(st)
     ws = cgmod.cg_graph_for(op, 10, 1e-4).run(v)
-torch.cuda.synchronize()
-e0.record(st)
-ws = cgmod.cg_graph_for(op, 10, 1e-4).run(v)
-e1.record(st)
-torch.cuda.synchronize()
-cg_ms = e0.elapsed_time(e1)
-iters = int(ws.slot(10)[3])
+    e1.record(st)
+    torch.cuda.synchronize()
+    cg_ms = e0.elapsed_time(e1)
+    iters = int(ws.slot(10)[3])
+    useful = 4.0 * m * p * K                 # 2 GEMMs x 2 m p K
+    KP = (K + 15) // 16 * 16
+    issued = 2.0 * 2 * m * p * (3 * KP)      # per GEMM: N = 2 KP plus N = KP, bf16
+    xbytes = 2 * 2 * m * p * 2               # X1 + X2 (bf16) read by each GEMM
+    res = {
+        "workload": f"{n}x{p} f32 shard, C={C}, 5% S_H (m={m}), tcgen05 bf16 two-term split",
+        "prepare_ms": prep_ms, "hess_apply_ms": hv_ms, "hv_per_s": 1e3 / hv_ms,
+        "cg_10_ms": cg_ms, "cg_iters": iters, "cg_hv_per_s": iters / (cg_ms / 1e3),
+        "useful_tflops": useful / (hv_ms / 1e3) / 1e12,
+        "issued_mma_tflops": issued / (hv_ms / 1e3) / 1e12,
+        "x_stream_tb_s": xbytes / (hv_ms / 1e3) / 1e12,
+    }
+    return res, op, v, out
 
-useful = 4.0 * m * p * K                 # 2 GEMMs x 2 m p K
-KP = (K + 15) // 16 * 16
-issued = 2.0 * 2 * m * p * (3 * KP)      # per GEMM: N = 2 KP plus N = KP, bf16
-xbytes = 2 * 2 * m * p * 2               # X1 + X2 (bf16) read by each GEMM
-print(json.dumps({
-    "workload": f"{n}x{p} f32 shard, C={C}, 5% S_H (m={m}), tcgen05 bf16 two-term split",
-    "prepare_ms": prep_ms, "hess_apply_ms": hv_ms, "hv_per_s": 1e3 / hv_ms,
-    "cg_10_ms": cg_ms, "cg_iters": iters, "cg_hv_per_s": iters / (cg_ms / 1e3),
-    "useful_tflops": useful / (hv_ms / 1e3) / 1e12,
-    "issued_mma_tflops": issued / (hv_ms / 1e3) / 1e12,
-    "x_stream_tb_s": xbytes / (hv_ms / 1e3) / 1e12,
-}))
 
-if os.environ.get("SNX_LIB", "").endswith("libsnx_tl.so"):
+if __name__ == "__main__":
+    n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
+    res, op, v, out = measure(n, reps)
+    print(json.dumps(res))
+
+if __name__ == "__main__" and os.environ.get("SNX_LIB", "").endswith("libsnx_tl.so"):
     import ctypes
 
     from paper_1802_09113_b200 import _lib
