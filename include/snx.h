@@ -117,6 +117,21 @@ int snx_hess_apply_tc(const void *X1, const void *X2, int64_t ldb, int64_t nrows
                       double *Hv_out, double *dots, const double *skip, void *ws,
                       size_t ws_bytes, void *stream);
 
+/* Wide classes (16 < K <= 128) on f32 data: the full-data passes of
+ * snx_objective / snx_objective_grad on the tensor cores, reading the bf16
+ * split of the rows (snx_tc_split: X1 = bf16(X), X2 = bf16(X - X1), [nrows][ldb]).
+ * Same outputs and conventions as the SNX_F32 calls above. */
+int snx_tc_split(const float *X, int64_t ldx, int64_t nrows, int32_t p, void *X1, void *X2,
+                 int64_t ldb, void *stream);
+int snx_objective_tc(const void *X1, const void *X2, int64_t ldb, int64_t nrows, int32_t p,
+                     int32_t K, const int32_t *labels, const double *w, const double *dir,
+                     double alpha, double *out, int64_t *correct_out, void *ws, size_t ws_bytes,
+                     void *stream);
+int snx_objective_grad_tc(const void *X1, const void *X2, int64_t ldb, int64_t nrows, int32_t p,
+                          int32_t K, const int32_t *labels, const double *w, double scale,
+                          double lam, double *out, double *G_out, void *ws, size_t ws_bytes,
+                          void *stream);
+
 /* Fixed-order dot product: out[0] = x . y (np.dot / np.linalg.norm**2).
  * out must hold 1 + SNX_DOT_BLOCKS doubles (out[1..] = block partials). */
 int snx_dot(const double *x, const double *y, int64_t d, double *out, void *stream);

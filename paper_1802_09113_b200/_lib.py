@@ -39,6 +39,11 @@ SIGNATURES = {
                                      _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_size, _c_p]),
     "snx_hess_apply_tc": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                    _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_tc_split": (_c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_i64, _c_p]),
+    "snx_objective_tc": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p,
+                                  _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_objective_grad_tc": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                       _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_dot": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "snx_dot_partials": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "snx_axpy": (_c_int, [_c_p, _c_p, _c_dbl, _c_i64, _c_p, _c_p]),

@@ -101,9 +101,19 @@ struct Tc1Args {
   unsigned *rb_count; // [row_blocks] arrivals (zero at rest)
   const double *skip;
   int K;              // classes (wide kernels; the K <= 16 kernels take it as a template)
-  int prep;           // wide GEMM1: 1 = write the probabilities h (HessianOperator init)
+  int mode;           // wide GEMM1 row algebra: kTcApply, kTcPrep, kTcObjective, kTcGradient
   float *hout;        // [nrows][K] (prep)
+  // objective / gradient (full-data passes, 16 < K)
+  const int32_t *labels;
+  double *loss_part;               // [row_blocks] fixed-order per-block losses
+  unsigned long long *corr_part;   // [row_blocks]
+  unsigned *done_rb;               // finished row blocks (zero at rest)
+  int64_t row_blocks;
+  double *loss_out;
+  long long *corr_out;             // nullable
 };
+
+enum { kTcApply = 0, kTcPrep = 1, kTcObjective = 2, kTcGradient = 3 };
 
 struct Tc2Args {
   CUtensorMap xmap;   // X1 [nrows][PB]: boxes 64 cols x 64 rows, 128-B swizzle
@@ -127,8 +137,9 @@ struct Tc2Args {
 template <int S> struct BarT {
   uint64_t full[S], empty[S], accf[2], acce[2];
   uint32_t tbase;
-  int flag;
+  int flag, flag2;
   double red[4];
+  unsigned long long cnt[4];
 };
 using Barriers = BarT<kS>;
 
@@ -458,13 +469,17 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm2_kernel(const __grid_cons
 // v[c*p + j] (Q1 in rows [0, KP), Q2 in rows [KP, 2 KP)); other rows and
 // columns >= p zero.
 __global__ void tc_prep_b_kernel(const double *__restrict__ v, int K, int p, int PB, int KP,
-                                 __nv_bfloat16 *__restrict__ B) {
+                                 __nv_bfloat16 *__restrict__ B,
+                                 const double *__restrict__ dir = nullptr, double alpha = 0.0) {
   const int64_t n = (int64_t)KP * PB;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int c = (int)(e / PB), j = (int)(e - (int64_t)c * PB);
     __nv_bfloat16 x1 = __float2bfloat16(0.0f), x2 = x1;
-    if (c < K && j < p) split_bf16(v[(int64_t)c * p + j], x1, x2);
+    if (c < K && j < p) {
+      const int64_t f = (int64_t)c * p + j;
+      split_bf16(dir != nullptr ? np_axpy(v[f], alpha, dir[f]) : v[f], x1, x2);  // w + a dir
+    }
     B[e] = x1;
     B[e + n] = x2;
   }
@@ -614,7 +629,7 @@ __global__ void __launch_bounds__(kThreads, 1) tcw_gemm1_kernel(const __grid_con
         // if this loop is unrolled)
         const int wq = warp & 3;
         constexpr int kR = 4, kC = KP / 32 + (KP % 32 ? 1 : 0);
-        if (a.prep) {
+        if (a.mode == kTcPrep) {
 #pragma unroll 1
           for (int rq = wq * 32; rq < wq * 32 + 32; ++rq) {
             const int64_t rr = rb * 128 + rq;
@@ -643,6 +658,105 @@ __global__ void __launch_bounds__(kThreads, 1) tcw_gemm1_kernel(const __grid_con
 #pragma unroll
             for (int k = 0; k < kC; ++k)
               if (lane + 32 * k < K) a.hout[rr * K + lane + 32 * k] = (float)(e[k] / alpha);
+          }
+        } else if (a.mode == kTcObjective || a.mode == kTcGradient) {
+          // softmax.py:91-98, :134 (row loss), :157-161 (residual R = E/alpha -
+          // onehot, back into smem) and :224-240 (prediction, first max wins)
+          double lw = 0.0;
+          unsigned long long cw = 0;
+#pragma unroll 1
+          for (int rq = wq * 32; rq < wq * 32 + 32; ++rq) {
+            const int64_t rr = rb * 128 + rq;
+            if (rr >= a.nrows) break;
+            const int y = a.labels[rr];
+            float z[kC];
+            double M = 0.0, zy = 0.0;
+#pragma unroll
+            for (int k = 0; k < kC; ++k) {
+              const int c = lane + 32 * k;
+              z[k] = c < K ? vsm[c * W::VS + rq] : 0.0f;
+              if (c < K) M = ((double)z[k] > M || isnan(z[k])) ? (double)z[k] : M;
+              if (c == y) zy = (double)z[k];
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+              const double t2 = __shfl_xor_sync(0xffffffffu, M, o);
+              M = (t2 > M || isnan(t2)) ? t2 : M;
+            }
+            zy = warp_allsum(zy);  // one non-zero term (0 for the reference class y = K)
+            double e[kC], se = 0.0;
+#pragma unroll
+            for (int k = 0; k < kC; ++k) {
+              e[k] = lane + 32 * k < K ? exp((double)z[k] - M) : 0.0;
+              se += e[k];
+            }
+            const double alpha = exp(-M) + warp_allsum(se);
+            lw += (M + log(alpha)) - zy;  // identical in every lane
+            if (a.mode == kTcGradient) {
+#pragma unroll
+              for (int k = 0; k < kC; ++k) {
+                const int c = lane + 32 * k;
+                if (c < K) vsm[c * W::VS + rq] = (float)(e[k] / alpha - (c == y ? 1.0 : 0.0));
+              }
+            } else if (a.corr_out != nullptr) {
+              // argmax over [E/alpha, e^-M/alpha], lowest index on ties
+              double bv = -1.0;
+              int bi = 0x7fffffff;
+#pragma unroll
+              for (int k = 0; k < kC; ++k) {
+                const int c = lane + 32 * k;
+                const double pc = e[k] / alpha;
+                if (c < K && (pc > bv || (pc == bv && c < bi))) {
+                  bv = pc;
+                  bi = c;
+                }
+              }
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) {
+                const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                if (ov > bv || (ov == bv && oi < bi)) {
+                  bv = ov;
+                  bi = oi;
+                }
+              }
+              if (exp(-M) / alpha > bv) bi = K;  // the reference class comes last
+              cw += bi == y ? 1ull : 0ull;
+            }
+          }
+          if (lane == 0) {
+            b.red[wq] = lw;
+            b.cnt[wq] = cw;
+          }
+          epi_sync();
+          if (et == 0) {
+            a.loss_part[rb] = ((b.red[0] + b.red[1]) + b.red[2]) + b.red[3];
+            a.corr_part[rb] = b.cnt[0] + b.cnt[1] + b.cnt[2] + b.cnt[3];
+            b.flag2 = atomic_add_acq_rel(a.done_rb, 1u) == (unsigned)(a.row_blocks - 1);
+          }
+          epi_sync();
+          if (b.flag2) {  // last row block: fixed-order total over the row blocks
+            double t = 0.0;
+            unsigned long long tc = 0;
+            for (int64_t i = et; i < a.row_blocks; i += 128) {
+              t += __ldcg(a.loss_part + i);
+              tc += __ldcg(a.corr_part + i);
+            }
+            t = warp_allsum(t);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) tc += __shfl_xor_sync(0xffffffffu, tc, o);
+            epi_sync();
+            if (lane == 0) {
+              b.red[wq] = t;
+              b.cnt[wq] = tc;
+            }
+            epi_sync();
+            if (et == 0) {
+              a.loss_out[0] = ((b.red[0] + b.red[1]) + b.red[2]) + b.red[3];
+              if (a.corr_out != nullptr)
+                a.corr_out[0] = (long long)(b.cnt[0] + b.cnt[1] + b.cnt[2] + b.cnt[3]);
+              *a.done_rb = 0u;
+            }
           }
         } else {
 #pragma unroll 1
@@ -677,8 +791,8 @@ __global__ void __launch_bounds__(kThreads, 1) tcw_gemm1_kernel(const __grid_con
         }
         epi_sync();
         if (et == 0) SNX_TC_TL(0, 5);
-        if (!a.prep) {
-          // [U1^T ; U2^T]: tasks (class, 8-row group), one 16-B store per term
+        if (a.mode == kTcApply || a.mode == kTcGradient) {
+          // [U1^T ; U2^T] (or [R1^T ; R2^T]): tasks (class, 8-row group), one 16-B store per term
           const int64_t rbase = rb * 128;
           const int nr = (int)min((int64_t)128, a.nrows - rbase);
           for (int task = et; task < K * 16; task += 128) {
@@ -1142,9 +1256,141 @@ static int tc_prepare_wide(const float *Xs, int64_t ld, int64_t nrows, int32_t p
   a1.zp = reinterpret_cast<double *>(wsb + lay.tc_zp);
   a1.rb_count = counters + 16 + SNX_DOT_BLOCKS;
   a1.K = K;
-  a1.prep = 1;
+  a1.mode = kTcPrep;
   a1.hout = H;
   return dispatch_wide(KP, a1, t.grid1, nullptr, 0, st);
 }
 
 }  // namespace snx
+
+namespace snx {
+
+// softmax.py:125-169 for 16 < K <= 128 on f32 data: the full-data pass over the
+// bf16 split X1 / X2 (snx_tc_split): GEMM1 against [W1 ; W2] with the loss /
+// prediction / residual row algebra, and for the gradient GEMM2 (X^T R) with
+// scale * (.) + lam * w.  out[0] = data loss, out[1] = ||w_eff||^2.
+static int tc_rowpass_wide(int mode, const void *X1, const void *X2, int64_t ldb, int64_t nrows,
+                           int32_t p, int32_t K, const int32_t *labels, const double *w,
+                           const double *dir, double alpha, double scale, double lam,
+                           double *out, long long *corr_out, double *G_out, void *ws,
+                           size_t ws_bytes, cudaStream_t st) {
+  if (K <= 16 || K > 128 || p < 1 || nrows < 0 || w == nullptr || out == nullptr ||
+      (nrows > 0 && (labels == nullptr || X1 == nullptr || X2 == nullptr))) {
+    set_error("snx_objective*_tc: needs 16 < K <= 128, p >= 1, labels, X1/X2, w, out");
+    return 1;
+  }
+  const int64_t PB = tc_ld(p);
+  if (ldb < PB || ldb % 8 != 0) {
+    set_error("snx_objective*_tc: ldb=%lld needs >= round_up(p, 8), %% 8 == 0", (long long)ldb);
+    return 1;
+  }
+  const int KP = tc_kp(K);
+  const int32_t P = padded(p);
+  const Workspace lay = workspace_layout(SNX_F32, nrows, p, K);
+  if (ws == nullptr || ws_bytes < lay.total) {
+    set_error("snx: workspace too small (%zu < %zu bytes)", ws_bytes, lay.total);
+    return 1;
+  }
+  char *wsb = static_cast<char *>(ws);
+  unsigned *counters = reinterpret_cast<unsigned *>(wsb + lay.counters);
+  double *dotp = reinterpret_cast<double *>(wsb + lay.dot_part);
+  if (launch_prep_weights(SNX_F32, w, dir, alpha, K, p, P, nullptr, dotp, counters + 15, out + 1,
+                          st))
+    return 1;
+  if (nrows == 0) {  // empty dataset: data terms vanish
+    if (cudaMemsetAsync(out, 0, sizeof(double), st) != cudaSuccess) return check_launch("memset");
+    if (corr_out && cudaMemsetAsync(corr_out, 0, sizeof(long long), st) != cudaSuccess)
+      return check_launch("memset");
+    if (mode == kTcGradient) return launch_lam_only(K, p, lam, w, G_out, nullptr, nullptr, st);
+    return 0;
+  }
+  __nv_bfloat16 *B = reinterpret_cast<__nv_bfloat16 *>(wsb + lay.tc_b);
+  __nv_bfloat16 *UT = reinterpret_cast<__nv_bfloat16 *>(wsb + lay.tc_ut);
+  const int64_t ldu = tc_ld((int32_t)nrows);
+  tc_prep_b_kernel<<<64, 256, 0, st>>>(w, K, p, (int)PB, KP, B, dir, alpha);
+  if (check_launch("tc_prep_b")) return 1;
+  const TcGeometry t = tc_geometry(nrows, P);
+  Tc1Args a1{};
+  if (make_tmap_bf16(&a1.xmap, X1, PB, nrows, ldb, kKT, 128) ||
+      make_tmap_bf16(&a1.lmap, X2, PB, nrows, ldb, kKT, 128) ||
+      make_tmap_bf16(&a1.bmap, B, PB, 2 * KP, PB, kKT, 2 * KP))
+    return 1;
+  a1.nrows = nrows;
+  a1.nk = t.nk;
+  a1.items = t.items1;
+  a1.maxseg = t.maxseg1;
+  a1.ut = UT;
+  a1.ldu = ldu;
+  a1.zp = reinterpret_cast<double *>(wsb + lay.tc_zp);
+  a1.rb_count = counters + 16 + SNX_DOT_BLOCKS;
+  a1.K = K;
+  a1.mode = mode;
+  a1.labels = labels;
+  a1.loss_part = reinterpret_cast<double *>(wsb + lay.loss_part);
+  a1.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
+  a1.done_rb = counters + 2;
+  a1.row_blocks = t.row_blocks;
+  a1.loss_out = out;
+  a1.corr_out = corr_out;
+  if (mode != kTcGradient) return dispatch_wide(KP, a1, t.grid1, nullptr, 0, st);
+  Tc2Args a2{};
+  if (make_tmap_bf16(&a2.xmap, X1, PB, nrows, ldb, 64, kKT) ||
+      make_tmap_bf16(&a2.lmap, X2, PB, nrows, ldb, 64, kKT) ||
+      make_tmap_bf16(&a2.umap, UT, nrows, 2 * KP, ldu, kKT, 2 * KP))
+    return 1;
+  a2.nrows = nrows;
+  a2.rchunks = t.rchunks;
+  a2.items = t.items2;
+  a2.maxseg = t.maxseg2;
+  a2.gp = reinterpret_cast<double *>(wsb + lay.tc_gp);
+  a2.tile_count = counters + 16;
+  a2.col_tiles = t.col_tiles;
+  a2.p = p;
+  a2.scale = scale;
+  a2.lam = lam;
+  a2.v = w;
+  a2.out = G_out;
+  a2.K = K;
+  return dispatch_wide(KP, a1, t.grid1, &a2, t.grid2, st);
+}
+
+}  // namespace snx
+
+extern "C" {
+
+int snx_tc_split(const float *X, int64_t ldx, int64_t nrows, int32_t p, void *X1, void *X2,
+                 int64_t ldb, void *stream) {
+  if (nrows == 0) return 0;
+  if (X == nullptr || X1 == nullptr || X2 == nullptr || ldb < tc_ld(p) || ldb % 8 != 0) {
+    set_error("snx_tc_split: NULL pointer or ldb < round_up(p, 8)");
+    return 1;
+  }
+  const int64_t n = nrows * ldb;
+  const int blocks = (int)((n + 255) / 256 < 8 * sm_count() ? (n + 255) / 256 : 8 * sm_count());
+  tc_split_kernel<<<blocks, 256, 0, (cudaStream_t)stream>>>(
+      X, ldx, nrows, p, ldb, static_cast<__nv_bfloat16 *>(X1), static_cast<__nv_bfloat16 *>(X2));
+  return check_launch("tc_split");
+}
+
+int snx_objective_tc(const void *X1, const void *X2, int64_t ldb, int64_t nrows, int32_t p,
+                     int32_t K, const int32_t *labels, const double *w, const double *dir,
+                     double alpha, double *out, int64_t *correct_out, void *ws, size_t ws_bytes,
+                     void *stream) {
+  return tc_rowpass_wide(kTcObjective, X1, X2, ldb, nrows, p, K, labels, w, dir, alpha, 1.0, 0.0,
+                         out, reinterpret_cast<long long *>(correct_out), nullptr, ws, ws_bytes,
+                         (cudaStream_t)stream);
+}
+
+int snx_objective_grad_tc(const void *X1, const void *X2, int64_t ldb, int64_t nrows, int32_t p,
+                          int32_t K, const int32_t *labels, const double *w, double scale,
+                          double lam, double *out, double *G_out, void *ws, size_t ws_bytes,
+                          void *stream) {
+  if (G_out == nullptr) {
+    set_error("snx_objective_grad_tc: NULL G_out");
+    return 1;
+  }
+  return tc_rowpass_wide(kTcGradient, X1, X2, ldb, nrows, p, K, labels, w, nullptr, 0.0, scale,
+                         lam, out, nullptr, G_out, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+}  // extern "C"

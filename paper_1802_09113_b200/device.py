@@ -144,6 +144,20 @@ class DeviceDataset:
             hb = self._hess[key] = HessBuffers(self, m, gathered)
         return hb
 
+    # ------------------------------------------------------------ tensor-core split
+    def tc_split(self):
+        """bf16 split X1 + X2 of the f32 rows (the wide-class objective / gradient
+        passes read it); made once and cached."""
+        split = getattr(self, "_tc_split", None)
+        if split is None:
+            ldb = int(_lib.load().snx_tc_ld(self.n_features))
+            xs = torch.empty((2, max(self.n_rows, 1), ldb), dtype=torch.bfloat16,
+                             device=self.X.device)
+            _lib.call("snx_tc_split", ptr(self.X), self.ld, self.n_rows, self.n_features,
+                      ptr(xs[0]), ptr(xs[1]), ldb, stream_handle())
+            split = self._tc_split = (xs, ldb)
+        return split
+
     # ------------------------------------------------------------ workspace
     def workspace(self, nrows):
         owner = getattr(self, "_ws_owner", None)

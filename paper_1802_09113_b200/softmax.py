@@ -75,11 +75,22 @@ def _ws(view):
     return ptr(ws), ws.numel()
 
 
+def _wide(view):
+    """f32 data with more than 16 free classes: the tensor-core passes."""
+    return view.code == _lib.F32 and view.K > 16
+
+
 def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
     """Device [data loss, ||w_eff||^2] (+ correct count) at w_eff = w + alpha*direction."""
     view = view.materialized()
     out = torch.empty(2, dtype=torch.float64, device=w.device)
     corr = torch.empty(1, dtype=torch.int64, device=w.device) if want_correct else None
+    if _wide(view):
+        xs, ldb = view.tc_split()
+        _lib.call("snx_objective_tc", ptr(xs[0]), ptr(xs[1]), ldb, view.n_rows,
+                  view.n_features, view.K, ptr(view.labels), ptr(w), ptr(direction),
+                  float(alpha), ptr(out), ptr(corr), *_ws(view), stream_handle())
+        return out, corr
     _lib.call("snx_objective", *_args(view), ptr(view.labels), ptr(w), ptr(direction),
               float(alpha), ptr(out), ptr(corr), *_ws(view), stream_handle())
     return out, corr
@@ -90,6 +101,12 @@ def gradient_parts(view, w, scale, lam):
     view = view.materialized()
     out = torch.empty(2, dtype=torch.float64, device=w.device)
     G = torch.empty_like(w)
+    if _wide(view):
+        xs, ldb = view.tc_split()
+        _lib.call("snx_objective_grad_tc", ptr(xs[0]), ptr(xs[1]), ldb, view.n_rows,
+                  view.n_features, view.K, ptr(view.labels), ptr(w), float(scale), float(lam),
+                  ptr(out), ptr(G), *_ws(view), stream_handle())
+        return G, out
     _lib.call("snx_objective_grad", *_args(view), ptr(view.labels), ptr(w), float(scale),
               float(lam), ptr(out), ptr(G), *_ws(view), stream_handle())
     return G, out

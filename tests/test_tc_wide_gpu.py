@@ -39,3 +39,42 @@ def test_wide_hessian_vs_oracle(n, p, C, frac):
     got = op.apply(v)
     assert rel_err(got, ref) <= TOL_TC, rel_err(got, ref)
     assert np.array_equal(op.apply(v), got)
+
+
+@pytest.mark.parametrize("n,p,C", [(3001, 130, 18), (2500, 257, 100), (0, 40, 33), (1, 9, 129)])
+def test_wide_objective_gradient_vs_oracle(n, p, C):
+    A, y = oracle.synthetic_problem(max(n, 1), p, C, seed=C + 1)
+    A, y = A[:n], y[:n]
+    rng = np.random.default_rng(C)
+    x = 0.3 * rng.standard_normal((C - 1) * p)
+    d = rng.standard_normal((C - 1) * p)
+    ds = snx.DeviceDataset.from_numpy(A, y, C, dtype="f32")
+    prob = snx.SoftmaxProblem(ds, 1e-3)
+    f = snx.objective(prob, x)
+    f_ref = oracle.loss(A, y, C, x, 1e-3)
+    assert abs(f - f_ref) <= TOL_TC * max(1.0, abs(f_ref))
+    assert rel_err(snx.gradient(prob, x), oracle.grad(A, y, C, x, 1e-3)) <= TOL_TC
+    # line-search trial point and accuracy through the same pass
+    w = torch.from_numpy(x).cuda()
+    out, corr = snx.softmax.objective_parts(ds, w, torch.from_numpy(d).cuda(), 0.25,
+                                            want_correct=True)
+    xt = x + 0.25 * d
+    assert abs(float(out[0]) - oracle.data_loss(A, y, C, xt)) <= TOL_TC * max(
+        1.0, abs(oracle.data_loss(A, y, C, xt)))
+    assert abs(float(out[1]) - float(xt @ xt)) <= 1e-12 * float(xt @ xt)
+    if n:
+        acc_ref = oracle.accuracy(A, y, C, xt)
+        assert abs(int(corr) / n - acc_ref) <= 2.0 / n
+
+
+def test_wide_newton_solve_matches_oracle():
+    n, p, C = 4000, 60, 40
+    A, y = oracle.synthetic_problem(n, p, C, seed=3)
+    cfg = snx.make_variant("subsampled-20", snx.NewtonConfig(max_outer_iters=5))
+    tr = snx.newton_solve(snx.SoftmaxProblem(snx.DeviceDataset.from_numpy(A, y, C, dtype="f32"),
+                                             1e-3), cfg)
+    ref = oracle.newton_solve(A, y, C, 1e-3, variant="subsampled-20", max_outer_iters=5)
+    ref_f = [r[1] for r in ref["records"]]
+    assert len(tr.records) == len(ref_f)
+    for a, b in zip(tr.records, ref_f):
+        assert abs(a.objective - b) <= 1e-4 * abs(b)
