@@ -236,7 +236,7 @@ def secondary(snx, torch, args):
     sys.path.insert(0, os.path.join(ROOT, "tools"))
     import large_shard
 
-    res, _, _, _ = large_shard.measure(1_000_000, 10)
+    res, _, _, _ = large_shard.measure(1_000_000, 10, solve_iters=5)
     out["large_c100_shard_f32"] = res
     torch.cuda.empty_cache()
     # BASELINE config #4: trust region (Steihaug-CG), ill-conditioned CIFAR shape, 10% S_H

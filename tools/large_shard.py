@@ -8,6 +8,7 @@ import json
 import math
 import os
 import sys
+import time
 
 import numpy as np
 import torch
@@ -16,7 +17,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1802_09113_b200 as snx  # noqa: E402
 from paper_1802_09113_b200 import cg as cgmod, softmax  # noqa: E402
 
-def measure(n=1_000_000, reps=10, p=3072, C=100, seed=0):
+def measure(n=1_000_000, reps=10, p=3072, C=100, seed=0, solve_iters=0):
     """Prepare + Hessian product + 10-product CG on an n x p f32 shard (device data)."""
     K = C - 1
     g = torch.Generator(device="cuda").manual_seed(seed)
@@ -61,7 +62,23 @@ def measure(n=1_000_000, reps=10, p=3072, C=100, seed=0):
     KP = (K + 15) // 16 * 16
     issued = 2.0 * 2 * m * p * (3 * KP)      # per GEMM: N = 2 KP plus N = KP, bf16
     xbytes = 2 * 2 * m * p * 2               # X1 + X2 (bf16) read by each GEMM
+    solve = None
+    if solve_iters:
+        prob = snx.SoftmaxProblem(ds, 1e-3)
+        cfg = snx.make_variant("subsampled-100", snx.NewtonConfig(max_outer_iters=solve_iters))
+        snx.newton_solve(prob, snx.make_variant("subsampled-100",
+                                                snx.NewtonConfig(max_outer_iters=1)))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr = snx.newton_solve(prob, cfg)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        solve = {"outer_iters": tr.iterations, "seconds": dt, "ms_per_iter": 1e3 * dt /
+                 max(tr.iterations, 1), "reason": tr.reason,
+                 "objective": [r.objective for r in tr.records],
+                 "cg_iters": [r.cg_iters for r in tr.records[1:]]}
     res = {
+        "newton_solve": solve,
         "workload": f"{n}x{p} f32 shard, C={C}, 5% S_H (m={m}), tcgen05 bf16 two-term split",
         "prepare_ms": prep_ms, "hess_apply_ms": hv_ms, "hv_per_s": 1e3 / hv_ms,
         "cg_10_ms": cg_ms, "cg_iters": iters, "cg_hv_per_s": iters / (cg_ms / 1e3),
@@ -75,7 +92,8 @@ def measure(n=1_000_000, reps=10, p=3072, C=100, seed=0):
 if __name__ == "__main__":
     n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
-    res, op, v, out = measure(n, reps)
+    solve_iters = int(sys.argv[3]) if len(sys.argv) > 3 else 0
+    res, op, v, out = measure(n, reps, solve_iters=solve_iters)
     print(json.dumps(res))
 
 if __name__ == "__main__" and os.environ.get("SNX_LIB", "").endswith("libsnx_tl.so"):
