@@ -231,6 +231,27 @@ def secondary(snx, torch, args):
         out["cifar10_f32_tensor_core"] = shape_rate(snx, torch, A, y, C, "f32")
         out["cifar10_f32_tensor_core"]["workload"] = (
             "cifar10-shape, f32 data, Hessian GEMMs on tcgen05 (bf16 two-term split), 1e-4 path")
+    # estimate_lipschitz (bench.py:116-138 of the reference): 200 power
+    # iterations of the full-data (50k x 3072) Hessian product at x = 0
+    A, y = make_problem()
+    ds = snx.DeviceDataset.from_numpy(A, y, C)
+    lprob = snx.SoftmaxProblem(ds, LAM)
+    snx.estimate_lipschitz(lprob, iters=3)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    L = snx.estimate_lipschitz(lprob, iters=200)
+    dt = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.estimate_lipschitz(A, y, C, iters=5)
+    cpu5 = time.perf_counter() - t0
+    full_bytes = 2 * N * P * 8  # X streamed twice per product (V = X Q, X^T U)
+    out["lipschitz_cifar10"] = {
+        "seconds": dt, "iters": 200, "L": L, "ms_per_iter": dt / 200 * 1e3,
+        "x_stream_gb_s": full_bytes / (dt / 200) / 1e9,
+        "cpu_port_seconds_extrapolated": cpu5 / 5 * 200, "cpu_cores": os.cpu_count(),
+        "workload": "cifar10-shape full-data Hessian power iteration at x=0, lam=0, fp64"}
+    del ds, lprob, A, y
+    torch.cuda.empty_cache()
     # BASELINE config #5 per GPU: a 1M x 3072 f32 shard of the 8M x 3072, C = 100
     # problem (row-sharded over 8 GPUs; one GPU here), wide tensor-core product
     sys.path.insert(0, os.path.join(ROOT, "tools"))

@@ -199,6 +199,28 @@ int snx_hess_apply_cg(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int
 /* Address of the "done" field of slot t (pass as snx_hess_apply's skip). */
 const double *snx_cg_done_flag(const double *state, int32_t t);
 
+/* Power iteration of the reference's estimate_lipschitz (bench.py:116-138),
+ * one step after w = H v was written (snx_hess_apply(v -> w, skip = state+2)):
+ *   rayleigh = v.w, ||w|| = sqrt(w.w); ||w|| == 0 -> estimate 0 and stop
+ *   (sticky flag state[2]); else v = w / ||w||.
+ * state: SNX_POWER_STATE doubles, zero-filled before the first step;
+ * state[0] = current estimate (v.w of the last step), state[1] = ||w||. */
+#define SNX_POWER_STATE (4 + 2 * SNX_DOT_BLOCKS)
+int snx_power_step(double *v, const double *w, int64_t d, double *state, void *stream);
+
+/* Column normalisation (normalize_columns, dataset.py:314-324):
+ *   norms[j] = sqrt(sum_i X[i][j]^2)  (fixed-order; norms nullable)
+ *   scale[j] = 1 / norms[j] if norms[j] > 0 else 1
+ * ws: snx_colnorm_workspace_bytes(p) bytes of scratch. */
+size_t snx_colnorm_workspace_bytes(int32_t p);
+int snx_column_norms(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                     double *norms, double *scale, void *ws, size_t ws_bytes, void *stream);
+
+/* Y[i][j] = X[i][j] * scale[j] for j < p, 0 for p <= j < ld (scale_columns,
+ * dataset.py:109-118); Y may alias X. */
+int snx_scale_columns(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                      int64_t ld, const double *scale, void *Y, int64_t ldy, void *stream);
+
 /* Copy+convert host-layout helpers (device to device). */
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
                   int64_t ldd, void *stream);

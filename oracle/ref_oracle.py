@@ -23,7 +23,7 @@ __all__ = [
     "weights_matrix", "row_terms", "data_loss", "loss", "data_grad", "grad",
     "hess_probs", "hess_apply", "class_probs", "predict", "accuracy",
     "cg", "armijo", "minimize", "newton_solve", "estimate_lipschitz",
-    "synthetic_problem",
+    "synthetic_problem", "column_norms", "normalize_columns", "train_test_split",
 ]
 
 ROW_BLOCK = 8192          # softmax.py:25 (BLOCK_ROWS)
@@ -341,6 +341,32 @@ def estimate_lipschitz(A, y, C, iters=200, seed=0):
             return 0.0
         v = w / nw
     return rq
+
+
+# ----------------------------------------------------------------- data preparation
+def column_norms(A):
+    """dataset.py:103-107 (dense): sqrt of the column sums of squares."""
+    return np.sqrt((np.asarray(A, dtype=np.float64) ** 2).sum(axis=0))
+
+
+def normalize_columns(A):
+    """dataset.py:314-324 + scale_columns :109-118: nonzero columns to unit norm."""
+    norms = column_norms(A)
+    scale = np.ones_like(norms)
+    nz = norms > 0
+    scale[nz] = 1.0 / norms[nz]
+    return np.asarray(A, dtype=np.float64) * scale
+
+
+def train_test_split(n, train_fraction, seed):
+    """dataset.py:327-342: (train, test) sorted row indices from the SPLIT stream."""
+    if not 0.0 < train_fraction < 1.0:
+        raise ValueError(f"train_fraction must be in (0, 1), got {train_fraction}")
+    if n < 2:
+        raise ValueError(f"need at least 2 rows to split, got {n}")
+    n_train = int(np.ceil(train_fraction * n))
+    perm = stream_rng(seed, 2).permutation(n)  # rng.py:19 SPLIT_STREAM
+    return np.sort(perm[:n_train]), np.sort(perm[n_train:])
 
 
 # ----------------------------------------------------------------- synthetic data

@@ -15,6 +15,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIBDIR = os.path.join(PKG, "_lib")
 LIBPATH = os.path.join(LIBDIR, "libsnx.so")
 INCLUDE = os.path.join(ROOT, "include")
+OBJDIR = os.path.join(ROOT, "build", "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
@@ -44,18 +45,38 @@ def up_to_date():
     return all(os.path.getmtime(f) <= t for f in _deps())
 
 
-def build(force=False, verbose=False):
-    """Compile every csrc/*.cu for sm_100a into _lib/libsnx.so."""
-    if not force and up_to_date():
-        return LIBPATH
-    os.makedirs(LIBDIR, exist_ok=True)
-    tmp = LIBPATH + ".tmp"
-    cmd = [_nvcc(), *ARCH, *FLAGS, "-I", INCLUDE, *sources(), "-o", tmp]
+def _run(cmd, verbose):
     if verbose:
         print(" ".join(cmd))
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(f"nvcc failed ({proc.returncode}):\n{proc.stdout}\n{proc.stderr}")
+
+
+def build(force=False, verbose=False):
+    """Compile every csrc/*.cu for sm_100a (one object per source, rebuilt when
+    it or a header changed; in parallel) and link _lib/libsnx.so."""
+    if not force and up_to_date():
+        return LIBPATH
+    from concurrent.futures import ThreadPoolExecutor
+
+    os.makedirs(OBJDIR, exist_ok=True)
+    headers = [f for f in _deps() if not f.endswith(".cu")]
+    newest_header = max(os.path.getmtime(f) for f in headers)
+    compile_flags = [f for f in FLAGS if f != "-shared"]
+    jobs, objs = [], []
+    for src in sources():
+        obj = os.path.join(OBJDIR, os.path.basename(src)[:-3] + ".o")
+        objs.append(obj)
+        if force or not os.path.exists(obj) or os.path.getmtime(obj) < max(
+                os.path.getmtime(src), newest_header):
+            jobs.append([_nvcc(), *ARCH, *compile_flags, "-I", INCLUDE, "-c", src, "-o", obj])
+    with ThreadPoolExecutor(max_workers=max(1, min(len(jobs), os.cpu_count() or 1))) as ex:
+        for f in [ex.submit(_run, cmd, verbose) for cmd in jobs]:
+            f.result()
+    os.makedirs(LIBDIR, exist_ok=True)
+    tmp = LIBPATH + ".tmp"
+    _run([_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp], verbose)
     os.replace(tmp, LIBPATH)
     return LIBPATH
 

@@ -14,6 +14,7 @@ F64 = 0
 F32 = 1
 DOT_BLOCKS = 256
 CG_SLOT = 8
+POWER_STATE = 4 + 2 * DOT_BLOCKS
 ABI_VERSION = 1
 
 _c_int, _c_i32, _c_i64 = ctypes.c_int, ctypes.c_int32, ctypes.c_int64
@@ -59,6 +60,12 @@ SIGNATURES = {
     "snx_cg_solve": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_dbl, _c_dbl,
                               _c_p, _c_dbl, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                               _c_p, _c_size, _c_p]),
+    "snx_power_step": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
+    "snx_colnorm_workspace_bytes": (_c_size, [_c_i32]),
+    "snx_column_norms": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_size,
+                                  _c_p]),
+    "snx_scale_columns": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i64, _c_p, _c_p,
+                                   _c_i64, _c_p]),
     "snx_pack_rows": (_c_int, [_c_int, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p]),
 }
 

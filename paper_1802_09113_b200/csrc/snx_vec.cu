@@ -327,6 +327,64 @@ __global__ void __launch_bounds__(kDotThreads)
   if (threadIdx.x == 0) SNX_VTL(1, 1);
 }
 
+// ------------------------------------------------- power iteration (bench.py:116-138)
+// state: [rayleigh, ||w||, zero_flag, pad] + kDotBlocks (v.w) + kDotBlocks (w.w) partials.
+// Step part 1: block partials of v.w and w.w (skipped once a zero w was seen, so
+// the partials of that iteration stay in place).
+__global__ void __launch_bounds__(kDotThreads)
+    power_part_kernel(const double *__restrict__ v, const double *__restrict__ w, int64_t d,
+                      double *state) {
+  if (state[2] != 0.0) return;
+  __shared__ double sh[kDotThreads / 32];
+  double vw = 0.0, ww = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    const double wi = w[i];
+    vw += v[i] * wi;
+    ww += wi * wi;
+  }
+  const double a = block_sum<kDotThreads>(vw, sh);
+  const double b = block_sum<kDotThreads>(ww, sh);
+  if (threadIdx.x == 0) {
+    state[4 + blockIdx.x] = a;
+    state[4 + kDotBlocks + blockIdx.x] = b;
+  }
+}
+
+// Step part 2: every block reduces the partials in the same fixed order;
+// rayleigh = v.w, ||w|| = sqrt(w.w) (np.linalg.norm); ||w|| == 0 -> the
+// estimate is 0 and the iteration stops (bench.py:133-135); else v = w / ||w||.
+__global__ void __launch_bounds__(kDotThreads)
+    power_scale_kernel(double *__restrict__ v, const double *__restrict__ w, int64_t d,
+                       double *state) {
+  __shared__ double s_vw, s_nw;
+  if (threadIdx.x < 32) {
+    const double vw = warp_sum_partials(state + 4);
+    const double ww = warp_sum_partials(state + 4 + kDotBlocks);
+    if (threadIdx.x == 0) {
+      s_vw = vw;
+      s_nw = sqrt(ww);
+    }
+  }
+  __syncthreads();
+  const double nw = s_nw;
+  if (nw == 0.0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      state[0] = 0.0;
+      state[1] = 0.0;
+      state[2] = 1.0;
+    }
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    state[0] = s_vw;
+    state[1] = nw;
+  }
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads)
+    v[i] = __ddiv_rn(w[i], nw);
+}
+
 template <typename T>
 __global__ void pack_rows_kernel(const double *__restrict__ src, int64_t nrows, int p,
                                  T *__restrict__ dst, int64_t ldd) {
@@ -420,6 +478,14 @@ int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
 
 const double *snx_cg_done_flag(const double *state, int32_t t) {
   return state + (size_t)t * SNX_CG_SLOT + kDone;
+}
+
+int snx_power_step(double *v, const double *w, int64_t d, double *state, void *stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  power_part_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(v, w, d, state);
+  if (check_launch("power_part")) return 1;
+  power_scale_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(v, w, d, state);
+  return check_launch("power_scale");
 }
 
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,

@@ -57,3 +57,8 @@ def cuda_ok():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return True
+
+
+@pytest.fixture(scope="session")
+def data_golden():
+    return load_golden("data_golden.npz")
