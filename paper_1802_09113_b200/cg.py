@@ -25,7 +25,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .device import cuda_device, ptr, stream_handle, vec_in, vec_out
+from .device import cuda_device, download, ptr, stream_handle, vec_in, vec_out
 from .errors import CurvatureError, DataError
 
 CURVATURE_EPS = 1e-32  # cg.py:16
@@ -161,15 +161,20 @@ def _foreign_loop(apply_H, T, ws):
 
 
 def report_from(ws, t_final, as_torch):
-    rs, best, done, iters, conv, thr, err, curv = ws.slot(t_final).tolist()
+    if as_torch:
+        st = ws.slot(t_final).tolist()
+        sol = ws.pb.clone()
+    else:  # one synchronisation for the scalars and the solution
+        st, sol = download(ws.slot(t_final), ws.pb)
+        st = st.tolist()
+    rs, best, done, iters, conv, thr, err, curv = st
     if err != 0.0:
         raise CurvatureError(
             f"non-positive curvature s^T H s = {curv:.3e} at CG iteration {int(iters)}; "
             "operator is not positive definite")
-    sol = ws.pb.clone()
     if int(iters) == 0 and conv != 0.0:
-        sol.zero_()  # cg.py:61-62 returns zeros for g == 0
-    return CgReport(vec_out(sol, as_torch), best, int(iters), bool(conv))
+        sol = torch.zeros_like(sol) if as_torch else np.zeros_like(sol)  # cg.py:61-62: zeros for g == 0
+    return CgReport(sol, best, int(iters), bool(conv))
 
 
 def cg_solve(apply_H, g, cfg):

@@ -131,7 +131,7 @@ class DeviceDataset:
             return self
         if len(idx) and (idx.min() < 0 or idx.max() >= n):
             raise DimensionError("row index out of range")
-        return DeviceView(self, torch.from_numpy(idx).to(self.X.device), len(idx))
+        return DeviceView(self, upload(idx, self.X.device), len(idx))
 
     def slice_rows(self, i0, i1):
         return self.take(np.arange(i0, i1))
@@ -257,6 +257,26 @@ def as_device(ds, dtype="f64"):
     return dev
 
 
+def upload(a, device=None):
+    """numpy -> device through a pinned staging buffer (torch's caching host
+    allocator); the copy is asynchronous on the current stream, so the host
+    goes on enqueueing work instead of waiting for the GPU to drain."""
+    h = torch.from_numpy(np.ascontiguousarray(a)).pin_memory()
+    return h.to(device or cuda_device(), non_blocking=True)
+
+
+def download(*ts):
+    """Device tensors -> numpy arrays: asynchronous copies into pinned buffers and
+    ONE stream synchronisation for all of them."""
+    outs = []
+    for t in ts:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in outs]
+
+
 def vec_in(x, d, what="weight vector"):
     """User vector -> (contiguous fp64 CUDA tensor of length d, caller_used_torch)."""
     if isinstance(x, torch.Tensor):
@@ -266,11 +286,11 @@ def vec_in(x, d, what="weight vector"):
     a = np.asarray(x, dtype=np.float64)
     if a.shape != (d,):
         raise DimensionError(f"expected {what} of length {d}, got {a.shape}")
-    return torch.from_numpy(np.ascontiguousarray(a)).to(cuda_device()), False
+    return upload(a), False
 
 
 def vec_out(t, as_torch):
-    return t if as_torch else t.cpu().numpy()
+    return t if as_torch else download(t)[0]
 
 
 def dot(x, y):

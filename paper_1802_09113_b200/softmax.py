@@ -156,7 +156,7 @@ class HessianOperator:
 
     def __init__(self, ds, x, lam, scale=1.0, block_rows=BLOCK_ROWS):
         view = _view(ds)
-        w, _ = vec_in(x, view.dim)
+        w, from_torch = vec_in(x, view.dim)
         self.view = view
         self.ds = ds
         self.lam = float(lam)
@@ -164,7 +164,7 @@ class HessianOperator:
         self.block_rows = block_rows
         self.p, self.C = view.n_features, view.n_classes
         self.dim = view.dim
-        self._w = w.clone()
+        self._w = w.clone() if from_torch else w  # numpy input: w is already a private copy
         self._bufs = view.base.hess_buffers(view.n_rows, view.rows is not None)
         self._prepare()
 
