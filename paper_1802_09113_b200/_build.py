@@ -81,9 +81,9 @@ def build(force=False, verbose=False):
     return LIBPATH
 
 
-def build_timeline(out):
+def build_timeline(out, extra=()):
     """Debug variant with per-CTA globaltimer stamps (tools/timeline.py)."""
-    cmd = [_nvcc(), *ARCH, *FLAGS, "-DSNX_TIMELINE", "-I", INCLUDE, *sources(), "-o", out]
+    cmd = [_nvcc(), *ARCH, *FLAGS, "-DSNX_TIMELINE", *extra, "-I", INCLUDE, *sources(), "-o", out]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(proc.stderr)

@@ -518,15 +518,27 @@ __device__ __forceinline__ void gemm1_body(const G1Args &a, unsigned char *smem,
     const unsigned char *st = smem + s * Sh::STAGE;
     const unsigned char *xa = st + box * Sh::BOX + lane * 128;
     const T *wp = reinterpret_cast<const T *>(st + Sh::NB * Sh::BOX) + warp * Sh::WC;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
+#ifndef SNX_DIAG_NOMATH  // diagnostic build: data movement only
+    // software-pipelined over the 4 16-B column chunks of this warp's strip:
+    // the operands of chunk q+1 load while chunk q's 6K FMAs issue (two warps
+    // per SM sub-partition cannot hide the shared-memory latency otherwise)
+    T xv[2][3][V], wv[2][K][V];
+    auto load_q = [&](int q, T (&x)[3][V], T (&w)[K][V]) {
       const int off = ((c0 + q) ^ sw) * 16;
-      T v0[V], v1[V], v2[V], w[K][V];
-      lds(reinterpret_cast<const T *>(xa + off), v0);
-      lds(reinterpret_cast<const T *>(xa + 32 * 128 + off), v1);
-      lds(reinterpret_cast<const T *>(xa + 64 * 128 + off), v2);
+      lds(reinterpret_cast<const T *>(xa + off), x[0]);
+      lds(reinterpret_cast<const T *>(xa + 32 * 128 + off), x[1]);
+      lds(reinterpret_cast<const T *>(xa + 64 * 128 + off), x[2]);
 #pragma unroll
       for (int c = 0; c < K; ++c) lds(wp + c * Sh::CHUNK + q * V, w[c]);  // broadcasts
+    };
+    load_q(0, xv[0], wv[0]);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (q < 3) load_q(q + 1, xv[(q + 1) & 1], wv[(q + 1) & 1]);
+      const T(&v0)[V] = xv[q & 1][0];
+      const T(&v1)[V] = xv[q & 1][1];
+      const T(&v2)[V] = xv[q & 1][2];
+      const T(&w)[K][V] = wv[q & 1];
       // column-outer order: consecutive FMAs hit different accumulators, the
       // same accumulator recurs only every 3K instructions
 #pragma unroll
@@ -538,6 +550,7 @@ __device__ __forceinline__ void gemm1_body(const G1Args &a, unsigned char *smem,
           acc2[c] = fma(v2[v], w[c][v], acc2[c]);
         }
     }
+#endif
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
     ++itc;
@@ -899,6 +912,37 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
     const int nr = (int)min((int64_t)kG2Rows, a.nrows - (int64_t)rc * kG2Rows);
     const T *xs = reinterpret_cast<const T *>(smem + s * Sh::STAGE);
     const T *us = reinterpret_cast<const T *>(smem + s * Sh::STAGE + Sh::XB);
+    if (nr == kG2Rows) {
+      // full chunk: rows warp + 8j, j < 4, software-pipelined (row j+1's
+      // operands load while row j's 2VK FMAs issue)
+      T xb[2][2][V], ub[2][KP];
+      auto load_r = [&](int r, T (&x)[2][V], T (&u)[KP]) {
+        lds(xs + r * TCOL + lane * LC, x[0]);
+        lds(xs + r * TCOL + lane * LC + V, x[1]);
+#pragma unroll
+        for (int k = 0; k < KP; k += V) {  // 128-bit broadcasts of the U row
+          T t4[V];
+          lds(us + r * KP + k, t4);
+#pragma unroll
+          for (int v = 0; v < V; ++v) u[k + v] = t4[v];
+        }
+      };
+      load_r(warp, xb[0], ub[0]);
+#pragma unroll
+      for (int j = 0; j < kG2Rows / kWarps; ++j) {
+        if (j + 1 < kG2Rows / kWarps) load_r(warp + kWarps * (j + 1), xb[(j + 1) & 1], ub[(j + 1) & 1]);
+        const T(&x)[2][V] = xb[j & 1];
+        const T(&u)[KP] = ub[j & 1];
+#pragma unroll
+        for (int c = 0; c < K; ++c) {
+#pragma unroll
+          for (int v = 0; v < V; ++v) {
+            acc[v][c] = fma(x[0][v], u[c], acc[v][c]);
+            acc[V + v][c] = fma(x[1][v], u[c], acc[V + v][c]);
+          }
+        }
+      }
+    } else
     for (int r = warp; r < nr; r += kWarps) {
       T x0[V], x1[V];
       lds(xs + r * TCOL + lane * LC, x0);
