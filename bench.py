@@ -216,6 +216,99 @@ def shape_rate(snx, torch, A, y, nC, dtype, steps=30, warmup=3, frac=F_H):
     return res
 
 
+def sparse_problem(n=11314, p=61188, nC=20, density=0.0023, seed=0):
+    import scipy.sparse as sp
+
+    rng = np.random.default_rng(seed)
+    A = sp.random(n, p, density=density, format="csr", random_state=seed,
+                  data_rvs=lambda k: rng.uniform(0.0, 1.0, k))
+    norms = np.sqrt(np.asarray(A.multiply(A).sum(axis=0)).ravel())
+    scale = np.where(norms > 0, 1.0 / np.where(norms > 0, norms, 1.0), 1.0)
+    A = sp.csr_array(A @ sp.diags(scale))
+    y = rng.integers(0, nC, n)
+    return A, y
+
+
+def sparse_rate(snx, torch, steps=30, warmup=3):
+    """Hv/s of the bench step on CSR data (fresh S_H gather + prepare + captured
+    CG), device-timed; the oracle port on scipy CSR (the reference's sparse
+    arithmetic) timed on the host for comparison."""
+    import oracle
+    from paper_1802_09113_b200 import cg as cgmod, softmax
+    from paper_1802_09113_b200.sparse import CsrDataset
+
+    A, y = sparse_problem()
+    n, p = A.shape
+    nC = 20
+    ds = CsrDataset.from_scipy(A, y, nC)
+    x = torch.from_numpy(0.01 * np.random.default_rng(7).standard_normal((nC - 1) * p)).cuda()
+    g, _ = softmax.gradient_parts(ds, x, 1.0, LAM)
+    views = [ds.take(snx.draw_samples(snx.SampleConfig(1.0, F_H), n, k)[1])
+             for k in range(warmup + steps)]
+    m = views[0].n_rows
+    iters = torch.zeros(warmup + steps, dtype=torch.float64, device="cuda")
+    keep = [None]
+
+    def step(k):
+        op = softmax.HessianOperator(views[k], x, LAM, scale=n / m)
+        keep[0] = op
+        ws = cgmod.cg_graph_for(op, T_CG, THETA).run(g)
+        iters[k:k + 1].copy_(ws.slot(T_CG)[3:4])
+
+    for k in range(warmup):
+        step(k)
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for k in range(warmup, warmup + steps):
+        step(k)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    hv = int(iters[warmup:].sum())
+    op, out_v = keep[0], torch.empty_like(g)
+    for _ in range(3):
+        op.apply_into(g, out_v)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(50):
+        op.apply_into(g, out_v)
+    e1.record(st)
+    torch.cuda.synchronize()
+    apply_us = e0.elapsed_time(e1) / 50 * 1e3
+    e0.record(st)
+    for _ in range(5):
+        softmax.gradient_parts(ds, x, 1.0, LAM)
+    e1.record(st)
+    torch.cuda.synchronize()
+    grad_us = e0.elapsed_time(e1) / 5 * 1e3
+    # CPU: the oracle port on scipy CSR, same step (bounded sample)
+    xh = x.cpu().numpy()
+    gh = g.cpu().numpy()
+    t0, cnt, steps_cpu = time.perf_counter(), 0, 0
+    while time.perf_counter() - t0 < 5.0 and steps_cpu < 50:
+        s_h = oracle.draw_samples(1.0, F_H, False, 0, n, 900 + steps_cpu)[1]
+        As, ys = A[s_h], y[s_h]
+        h = oracle.hess_probs(As, ys, nC, xh)
+        c = [0]
+
+        def opc(v):
+            c[0] += 1
+            return oracle.hess_apply(As, h, nC, v, n / len(s_h), LAM)
+
+        oracle.cg(opc, gh, THETA, T_CG)
+        cnt += c[0]
+        steps_cpu += 1
+    cpu_s = time.perf_counter() - t0
+    nnz_s = int(views[-1].base.sample_nnz(views[-1].idx))
+    return {"value": hv / (ms / 1e3), "unit": UNIT, "ms_per_step": ms / steps, "m": m,
+            "nnz": int(A.nnz), "sample_nnz": nnz_s, "hess_apply_us": apply_us,
+            "full_gradient_us": grad_us,
+            "cpu_port_hv_per_s": cnt / cpu_s, "cpu_cores": os.cpu_count(),
+            "workload": f"newsgroups20-shape CSR {n}x{p} C={nC}, nnz {A.nnz}, 5% S_H, fp64"}
+
+
 def secondary(snx, torch, args):
     """The other BASELINE.json shapes and the tensor-core f32 path (one GPU)."""
     import oracle
@@ -251,6 +344,10 @@ def secondary(snx, torch, args):
         "cpu_port_seconds_extrapolated": cpu5 / 5 * 200, "cpu_cores": os.cpu_count(),
         "workload": "cifar10-shape full-data Hessian power iteration at x=0, lam=0, fp64"}
     del ds, lprob, A, y
+    torch.cuda.empty_cache()
+    # CSR storage (the paper's Newsgroups20 / cuSPARSE path): 11314 x
+    # 61188, C = 20, ~1.6M nonzeros, columns normalised; fresh 5% S_H + CG per step
+    out["newsgroups20_sparse"] = sparse_rate(snx, torch)
     torch.cuda.empty_cache()
     # BASELINE config #5 per GPU: a 1M x 3072 f32 shard of the 8M x 3072, C = 100
     # problem (row-sharded over 8 GPUs; one GPU here), wide tensor-core product

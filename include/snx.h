@@ -221,6 +221,46 @@ int snx_column_norms(int dtype, const void *X, int64_t ldx, int64_t nrows, int32
 int snx_scale_columns(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
                       int64_t ld, const double *scale, void *Y, int64_t ldy, void *stream);
 
+/* ------------------------------------------------------------------ sparse
+ * CSR feature storage (the reference's sparse DesignMatrix, dataset.py:21-147;
+ * the paper's cuSPARSE path), fp64 only, K <= 32:
+ *   CSR  indptr[n+1] (int64), indices[nnz] (int32 column ids), data[nnz]
+ *   CSC  colptr[p+1] (int64), rowidx[nnz] (int32 row ids),    cdata[nnz]
+ * (the CSC copy is the transpose; X^T R contracts column by column in a fixed
+ * order, no atomics).  Same outputs and conventions as the dense calls;
+ * ws: snx_csr_workspace_bytes(n, p, K) bytes (n = rows of the FULL dataset
+ * for snx_csr_gather). */
+size_t snx_csr_workspace_bytes(int64_t nrows, int32_t p, int32_t K);
+int snx_csr_objective(const int64_t *indptr, const int32_t *indices, const double *data,
+                      int64_t nrows, int32_t p, int32_t K, const int32_t *labels, const double *w,
+                      const double *dir, double alpha, double *out, int64_t *correct_out,
+                      void *ws, size_t ws_bytes, void *stream);
+int snx_csr_objective_grad(const int64_t *indptr, const int32_t *indices, const double *data,
+                           const int64_t *colptr, const int32_t *rowidx, const double *cdata,
+                           int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
+                           const double *w, double scale, double lam, double *out, double *G_out,
+                           void *ws, size_t ws_bytes, void *stream);
+/* The row sample S (sorted int64, duplicates allowed: sampling with
+ * replacement) as its own CSR (s_indptr[m+1], entries in the order of the
+ * source rows) and CSC (s_colptr[p+1], rows renumbered to sample positions,
+ * a duplicated row weighted by its multiplicity); s_* capacities must hold
+ * sum_r nnz(row S[r]) entries (dataset.py:90-97 take / sampling.py:79-80). */
+int snx_csr_gather(const int64_t *indptr, const int32_t *indices, const double *data,
+                   const int64_t *colptr, const int32_t *rowidx, const double *cdata,
+                   int64_t nrows, int32_t p, const int64_t *rows, int64_t m, int64_t *s_indptr,
+                   int32_t *s_indices, double *s_data, int64_t *s_colptr, int32_t *s_rowidx,
+                   double *s_cdata, void *ws, size_t ws_bytes, void *stream);
+/* softmax.py:181-195 on a (gathered) CSR sample: H_out[r*K + c] = h(a_r, x_c). */
+int snx_csr_hess_prepare(const int64_t *indptr, const int32_t *indices, const double *data,
+                         int64_t nrows, int32_t p, int32_t K, const double *w, double *H_out,
+                         void *ws, size_t ws_bytes, void *stream);
+/* softmax.py:197-210 on the CSR + CSC of the sample; dots / skip as snx_hess_apply. */
+int snx_csr_hess_apply(const int64_t *indptr, const int32_t *indices, const double *data,
+                       const int64_t *colptr, const int32_t *rowidx, const double *cdata,
+                       int64_t nrows, int32_t p, int32_t K, const double *H, const double *v,
+                       double scale, double lam, double *Hv_out, double *dots, const double *skip,
+                       void *ws, size_t ws_bytes, void *stream);
+
 /* Copy+convert host-layout helpers (device to device). */
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
                   int64_t ldd, void *stream);

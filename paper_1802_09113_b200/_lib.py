@@ -66,6 +66,19 @@ SIGNATURES = {
                                   _c_p]),
     "snx_scale_columns": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i64, _c_p, _c_p,
                                    _c_i64, _c_p]),
+    "snx_csr_workspace_bytes": (_c_size, [_c_i64, _c_i32, _c_i32]),
+    "snx_csr_objective": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p,
+                                   _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_csr_objective_grad": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i32,
+                                        _c_i32, _c_p, _c_p, _c_dbl, _c_dbl, _c_p, _c_p, _c_p,
+                                        _c_size, _c_p]),
+    "snx_csr_gather": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i32, _c_p, _c_i64,
+                                _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_csr_hess_prepare": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p,
+                                      _c_size, _c_p]),
+    "snx_csr_hess_apply": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i32, _c_i32,
+                                    _c_p, _c_p, _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_size,
+                                    _c_p]),
     "snx_pack_rows": (_c_int, [_c_int, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p]),
 }
 

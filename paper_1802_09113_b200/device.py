@@ -242,13 +242,18 @@ _CACHE = {}
 
 
 def as_device(ds, dtype="f64"):
-    if isinstance(ds, (DeviceDataset, DeviceView)):
+    if isinstance(ds, (DeviceDataset, DeviceView)) or getattr(ds, "is_sparse", False) is True:
         return ds
     key = (id(ds), dtype)
     hit = _CACHE.get(key)
     if hit is not None and hit[0]() is ds:
         return hit[1]
-    dev = DeviceDataset.from_dataset(ds, dtype=dtype)
+    if getattr(getattr(ds, "features", None), "is_sparse", False):  # reference CSR storage
+        from .sparse import CsrDataset
+
+        dev = CsrDataset.from_dataset(ds)
+    else:
+        dev = DeviceDataset.from_dataset(ds, dtype=dtype)
     try:
         ref = weakref.ref(ds, lambda _r, k=key: _CACHE.pop(k, None))
     except TypeError:  # not weak-referenceable: keep a strong reference

@@ -21,7 +21,7 @@ import os
 import numpy as np
 import torch
 
-from . import _lib
+from . import _lib, sparse
 from .device import DeviceDataset, DeviceView, as_device, ptr, stream_handle, vec_in, vec_out
 from .errors import DataError, DimensionError
 
@@ -82,6 +82,8 @@ def _wide(view):
 
 def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
     """Device [data loss, ||w_eff||^2] (+ correct count) at w_eff = w + alpha*direction."""
+    if getattr(view, "is_sparse", False):
+        return sparse.objective_parts(view, w, direction, alpha, want_correct)
     view = view.materialized()
     out = torch.empty(2, dtype=torch.float64, device=w.device)
     corr = torch.empty(1, dtype=torch.int64, device=w.device) if want_correct else None
@@ -98,6 +100,8 @@ def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
 
 def gradient_parts(view, w, scale, lam):
     """Device (G = scale * data_gradient + lam * w, [data loss, ||w||^2])."""
+    if getattr(view, "is_sparse", False):
+        return sparse.gradient_parts(view, w, scale, lam)
     view = view.materialized()
     out = torch.empty(2, dtype=torch.float64, device=w.device)
     G = torch.empty_like(w)
@@ -171,7 +175,9 @@ class HessianOperator:
     def _prepare(self):
         """Materialise this operator's sample and probabilities in the shared buffers."""
         view, base, hb = self.view, self.view.base, self._bufs
-        if hb.xs_tc is not None:  # f32: tensor-core product (csrc/snx_tc.cu)
+        if getattr(base, "is_sparse", False):  # CSR data (csrc/snx_csr.cu)
+            sparse.hess_prepare(self)
+        elif hb.xs_tc is not None:  # f32: tensor-core product (csrc/snx_tc.cu)
             _lib.call("snx_hess_prepare_tc", ptr(base.X), base.ld, ptr(view.rows), view.n_rows,
                       view.n_features, view.K, ptr(self._w), ptr(hb.xs), base.ld, ptr(hb.h),
                       ptr(hb.xs_tc[0]), ptr(hb.xs_tc[1]), hb.ldb, *_ws(view), stream_handle())
@@ -192,6 +198,8 @@ class HessianOperator:
         if self._bufs.owner is not self:
             self._prepare()
         base, hb = self.view.base, self._bufs
+        if getattr(base, "is_sparse", False):
+            return sparse.hess_apply(self, v, out, dots, skip)
         if hb.xs_tc is not None:
             _lib.call("snx_hess_apply_tc", ptr(hb.xs_tc[0]), ptr(hb.xs_tc[1]), hb.ldb,
                       self.view.n_rows, self.p, self.view.K, ptr(hb.h), ptr(v), self.scale,
@@ -210,7 +218,8 @@ class HessianOperator:
         solve) -- the tile finalizers' two waits for every other tile cost more
         than the two ~1 us kernel boundaries they remove."""
         hb, view = self._bufs, self.view
-        if hb.xs_tc is not None or os.environ.get("SNX_CG_FUSED", "0") != "1":
+        if (hb.xs_tc is not None or getattr(view.base, "is_sparse", False)
+                or os.environ.get("SNX_CG_FUSED", "0") != "1"):
             return False
         if hb.owner is not self:
             self._prepare()
@@ -230,7 +239,7 @@ class HessianOperator:
         grid barriers per iteration cost ~2.2 us each, more than the ~1 us
         kernel boundaries of the captured per-iteration graph."""
         hb, view = self._bufs, self.view
-        if (hb.xs_tc is not None or view.n_rows == 0
+        if (hb.xs_tc is not None or view.n_rows == 0 or getattr(view.base, "is_sparse", False)
                 or os.environ.get("SNX_CG_PERSISTENT", "0") != "1"):
             return False
         if hb.owner is not self:

@@ -62,3 +62,19 @@ def cuda_ok():
 @pytest.fixture(scope="session")
 def data_golden():
     return load_golden("data_golden.npz")
+
+
+@pytest.fixture(scope="session")
+def sparse_golden():
+    return load_golden("sparse_golden.npz")
+
+
+def sparse_cases(g):
+    import scipy.sparse as sp
+
+    i = 0
+    while f"s{i}_shape" in g:
+        n, p, C = (int(t) for t in g[f"s{i}_shape"])
+        A = sp.csr_array((g[f"s{i}_data"], g[f"s{i}_indices"], g[f"s{i}_indptr"]), shape=(n, p))
+        yield i, A, C, {k[len(f"s{i}_"):]: v for k, v in g.items() if k.startswith(f"s{i}_")}
+        i += 1
