@@ -98,7 +98,7 @@ template <typename T, int K> struct G1Shape {
   static constexpr size_t SMEM = S * STAGE + RED + 2 * S * 8 + 64;
 };
 
-// GEMM2 shape: an item is (1-KB column tile) x (32 rows); lanes own 2 x 16 B of
+// GEMM2 shape: an item is (1-KB column tile) x (32 rows); lanes own 2 x 16 B (one per tile half) of
 // consecutive columns; U rows are padded to a 16-B multiple (KP) so each row
 // is a few 128-bit smem broadcasts.
 template <typename T, int K> struct G2Shape {
@@ -860,12 +860,15 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
       // flush the segment partial of the tile just finished: warp pairs
       // (w, w+4), then the 4 pair sums in order
       const int ftile = (i == i1 && rc != 0) ? tile : tile - 1;
-      double *mine = red + (size_t)(warp & 3) * K * TCOL + lane * LC;
+      // lane columns: acc[v] is column V*lane + v (v < V) of the tile's first
+      // half and 32V + V*lane + v - V of its second half (conflict-free loads)
+      double *mine = red + (size_t)(warp & 3) * K * TCOL;
+      auto col_of = [&](int v) { return v < V ? V * lane + v : 32 * V + V * lane + (v - V); };
       if (warp >= 4) {
 #pragma unroll
         for (int c = 0; c < K; ++c)
 #pragma unroll
-          for (int v = 0; v < LC; ++v) mine[c * TCOL + v] = (double)acc[v][c];
+          for (int v = 0; v < LC; ++v) mine[c * TCOL + col_of(v)] = (double)acc[v][c];
       }
       consumer_sync(kConsumers);
       if (warp < 4) {
@@ -873,7 +876,7 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
         for (int c = 0; c < K; ++c)
 #pragma unroll
           for (int v = 0; v < LC; ++v)
-            mine[c * TCOL + v] = (double)acc[v][c] + mine[c * TCOL + v];
+            mine[c * TCOL + col_of(v)] = (double)acc[v][c] + mine[c * TCOL + col_of(v)];
       }
 #pragma unroll
       for (int v = 0; v < LC; ++v)
@@ -917,8 +920,8 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
       // operands load while row j's 2VK FMAs issue)
       T xb[2][2][V], ub[2][KP];
       auto load_r = [&](int r, T (&x)[2][V], T (&u)[KP]) {
-        lds(xs + r * TCOL + lane * LC, x[0]);
-        lds(xs + r * TCOL + lane * LC + V, x[1]);
+        lds(xs + r * TCOL + lane * V, x[0]);
+        lds(xs + r * TCOL + 32 * V + lane * V, x[1]);
 #pragma unroll
         for (int k = 0; k < KP; k += V) {  // 128-bit broadcasts of the U row
           T t4[V];
@@ -945,8 +948,8 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
     } else
     for (int r = warp; r < nr; r += kWarps) {
       T x0[V], x1[V];
-      lds(xs + r * TCOL + lane * LC, x0);
-      lds(xs + r * TCOL + lane * LC + V, x1);
+      lds(xs + r * TCOL + lane * V, x0);
+      lds(xs + r * TCOL + 32 * V + lane * V, x1);
       T u[KP];
 #pragma unroll
       for (int k = 0; k < KP; k += V) {  // 128-bit broadcasts of the U row
