@@ -516,23 +516,43 @@ def run_ours(args):
            "h2d_bytes_per_step": 2 * ds.dim * 8 + m * 8,
            "d2h_bytes_per_step": ds.dim * 8 + 8 * 8}
 
-    # ---- time-to-tolerance of one full Newton solve (device resident)
+    # ---- time-to-tolerance of Newton solves (device resident, reference timed region:
+    # newton.py:72-104 incl. objective / accuracy passes).  On this synthetic problem
+    # the 5%-Hessian method (BASELINE config) reaches eps = 1e-2 |grad F(0)| (it
+    # stalls before 1e-3); full Newton reaches 1e-6 in a few iterations.
     solve = None
     if not args.skip_solve:
         from paper_1802_09113_b200.device import dot
 
         gz = softmax.gradient_parts(ds, torch.zeros_like(x), 1.0, LAM)[0]
         g0 = math.sqrt(float(dot(gz, gz)))
-        ncfg = snx.make_variant("subsampled-100", snx.NewtonConfig(
-            epsilon=1e-6 * g0, max_outer_iters=100))
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        tr = snx.newton_solve(prob, ncfg, x0=torch.zeros_like(x))
-        torch.cuda.synchronize()
-        solve = {"time_to_tol_s": time.perf_counter() - t0, "outer_iters": tr.iterations,
-                 "reason": tr.reason, "final_objective": tr.final_objective,
-                 "cg_iters": [r.cg_iters for r in tr.records[1:]],
-                 "epsilon": 1e-6 * g0}
+        solve = {}
+        for name, variant, rel, cap in (("subsampled_100", "subsampled-100", 1e-2, 400),
+                                        ("full_newton", "full", 1e-6, 50)):
+            ncfg = snx.make_variant(variant, snx.NewtonConfig(epsilon=rel * g0,
+                                                              max_outer_iters=cap))
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            tr = snx.newton_solve(prob, ncfg, x0=torch.zeros_like(x))
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            solve[name] = {"time_to_tol_s": dt, "outer_iters": tr.iterations,
+                           "ms_per_outer_iter": 1e3 * dt / max(tr.iterations, 1),
+                           "reason": tr.reason, "final_objective": tr.final_objective,
+                           "epsilon": rel * g0, "epsilon_rel_to_grad0": rel,
+                           "cg_iters_total": int(sum(r.cg_iters for r in tr.records[1:]))}
+        if rank == 0 and world == 1 and not args.skip_cpu:
+            # the oracle port's Newton iteration on the same problem (2 iterations,
+            # extrapolated to the GPU's iteration count)
+            import oracle
+
+            t0 = time.perf_counter()
+            oracle.newton_solve(A, y, C, LAM, "subsampled-100", max_outer_iters=2)
+            per_it = (time.perf_counter() - t0) / 2
+            solve["cpu_port_s_per_outer_iter"] = per_it
+            solve["cpu_port_time_to_tol_s_extrapolated"] = (
+                per_it * solve["subsampled_100"]["outer_iters"])
+            solve["cpu_cores"] = os.cpu_count()
 
     cpu = cpu_baseline(A, y, x_host) if (rank == 0 and world == 1 and not args.skip_cpu) \
         else None

@@ -261,6 +261,17 @@ int snx_csr_hess_apply(const int64_t *indptr, const int32_t *indices, const doub
                        double scale, double lam, double *Hv_out, double *dots, const double *skip,
                        void *ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------------ ingest
+ * LIBSVM / svmlight text (dataset.py:242-293 load_libsvm), HOST memory:
+ * snx_libsvm_scan parses `path` (whitespace tokens, blank lines skipped,
+ * "<label> <idx>:<val> ..." with 1-based idx) and returns the sizes;
+ * snx_libsvm_fetch copies the parse out (raw float labels[nrows], CSR
+ * indptr[nrows+1], 0-based indices[nnz], data[nnz]).  Returns 2 on a parse
+ * error ("line N: ..." in snx_last_error), 1 on an I/O error. */
+int snx_libsvm_scan(const char *path, int64_t *nrows, int64_t *nnz, int64_t *max_index);
+int snx_libsvm_fetch(const char *path, double *labels, int64_t *indptr, int32_t *indices,
+                     double *data);
+
 /* Copy+convert host-layout helpers (device to device). */
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
                   int64_t ldd, void *stream);

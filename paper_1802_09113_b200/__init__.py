@@ -9,6 +9,7 @@ include/snx.h) called through ctypes.  torch only owns device memory.
 from .cg import CgConfig, CgReport, cg_solve
 from .data import column_norms, normalize_columns, train_test_split
 from .device import DeviceDataset, DeviceView, as_device
+from .io import load_csv, load_libsvm
 from .errors import (CurvatureError, DataError, DimensionError, LineSearchError, ParseError,
                      SubnewtonError)
 from .linesearch import LineSearchConfig, line_search
@@ -34,5 +35,5 @@ __all__ = [
     "matrix_as_weights", "objective", "weights_as_matrix", "zero_weights", "RunRecord",
     "SolveTrace", "TrustRegionConfig", "steihaug_cg", "trust_region_solve",
     "estimate_lipschitz", "column_norms", "normalize_columns", "train_test_split",
-    "read_trace_csv", "write_trace_csv",
+    "read_trace_csv", "write_trace_csv", "load_libsvm", "load_csv",
 ]

@@ -79,6 +79,8 @@ SIGNATURES = {
     "snx_csr_hess_apply": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i32, _c_i32,
                                     _c_p, _c_p, _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_size,
                                     _c_p]),
+    "snx_libsvm_scan": (_c_int, [ctypes.c_char_p, _c_p, _c_p, _c_p]),
+    "snx_libsvm_fetch": (_c_int, [ctypes.c_char_p, _c_p, _c_p, _c_p, _c_p]),
     "snx_pack_rows": (_c_int, [_c_int, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p]),
 }
 

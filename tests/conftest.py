@@ -78,3 +78,17 @@ def sparse_cases(g):
         A = sp.csr_array((g[f"s{i}_data"], g[f"s{i}_indices"], g[f"s{i}_indptr"]), shape=(n, p))
         yield i, A, C, {k[len(f"s{i}_"):]: v for k, v in g.items() if k.startswith(f"s{i}_")}
         i += 1
+
+
+@pytest.fixture(scope="session")
+def libsvm_golden():
+    return load_golden("libsvm_golden.npz")
+
+
+def libsvm_cases(g):
+    names = sorted({k[:-len("_args")] for k in g if k.endswith("_args")})
+    for name in names:
+        C, nf = (int(t) for t in g[name + "_args"])
+        yield name, os.path.join(GOLDEN, "libsvm", name + ".svm"), C, (None if nf < 0 else nf), \
+            str(g[name + "_storage"]), {k[len(name) + 1:]: v for k, v in g.items()
+                                         if k.startswith(name + "_")}

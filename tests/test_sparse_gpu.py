@@ -104,3 +104,21 @@ def test_sparse_reference_object_duck_typed():
     f = snx.objective(snx.SoftmaxProblem(ds, 0.0), x)
     assert isinstance(snx.as_device(ds), CsrDataset)
     assert abs(f - oracle.loss(A.toarray(), ds.labels, 4, x, 0.0)) <= 1e-12 * abs(f)
+
+
+def test_load_libsvm_to_device(libsvm_golden):
+    """load_libsvm straight to HBM: CSR or dense as the reference picks, and the
+    objective / gradient on it equal the oracle's on the reference's parse."""
+    from conftest import libsvm_cases
+
+    for name, path, C, nf, storage, g in libsvm_cases(libsvm_golden):
+        if str(g["error"]):
+            continue
+        ds = snx.load_libsvm(path, C, n_features=nf, storage=storage)
+        assert getattr(ds, "is_sparse", False) == bool(g["is_sparse"]), name
+        X, y = g["X"], g["y"]
+        x = 0.1 * np.random.default_rng(1).standard_normal((C - 1) * X.shape[1])
+        prob = snx.SoftmaxProblem(ds, 1e-3)
+        ref = oracle.loss(X, y, C, x, 1e-3)
+        assert abs(snx.objective(prob, x) - ref) <= 1e-10 * abs(ref), name
+        assert rel_err(snx.gradient(prob, x), oracle.grad(X, y, C, x, 1e-3)) <= 1e-10, name
