@@ -80,6 +80,14 @@ int snx_objective_grad(int dtype, const void *X, int64_t ldx, int64_t nrows, int
                        double lam, double *out, double *G_out, void *ws, size_t ws_bytes,
                        void *stream);
 
+/* snx_objective_grad plus the accuracy count of snx_objective (correct_out,
+ * nullable) in the same pass: the Newton loop evaluates its first line-search
+ * trial F(x + p) together with the gradient at x + p (newton.py:92-99). */
+int snx_objective_grad_acc(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                           int32_t K, const int32_t *labels, const double *w, double scale,
+                           double lam, double *out, int64_t *correct_out, double *G_out, void *ws,
+                           size_t ws_bytes, void *stream);
+
 /* softmax.py:181-195 (HessianOperator.__init__) on the sample rows S_H:
  * when rows != NULL the sample is first gathered into Xs_out (ld_out), else
  * X itself is the sample (the f = 1 identity, dataset.py:94-96).

@@ -31,6 +31,8 @@ SIGNATURES = {
                                _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_objective_grad": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                     _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_objective_grad_acc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                        _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_hess_prepare": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p,
                                   _c_p, _c_i64, _c_p, _c_p, _c_size, _c_p]),
     "snx_hess_apply": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,

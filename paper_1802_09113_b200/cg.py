@@ -160,8 +160,13 @@ def _foreign_loop(apply_H, T, ws):
     return last
 
 
-def report_from(ws, t_final, as_torch):
-    if as_torch:
+def report_from(ws, t_final, as_torch, slot_values=None):
+    """CgReport of a finished device solve; slot_values: the final slot already
+    read by the caller (no extra synchronisation; the solution is ws.pb)."""
+    if slot_values is not None:
+        st = list(slot_values)
+        sol = ws.pb
+    elif as_torch:
         st = ws.slot(t_final).tolist()
         sol = ws.pb.clone()
     else:  # one synchronisation for the scalars and the solution

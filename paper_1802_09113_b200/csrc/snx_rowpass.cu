@@ -255,7 +255,8 @@ __device__ __forceinline__ void row_epilogue(const G1Args &a, int64_t r, const d
     T *R = static_cast<T *>(a.rowout) + r * a.ustride;
 #pragma unroll
     for (int c = 0; c < K; ++c) R[c] = (T)(E[c] / alpha - (c == y ? 1.0 : 0.0));
-  } else if (a.corr_out != nullptr) {
+  }
+  if (a.corr_out != nullptr) {
     // softmax.py:224-240: argmax over [E/alpha, e^-M/alpha], first max wins
     int best = 0;
     double bv = E[0] / alpha;
@@ -1960,6 +1961,19 @@ int snx_objective_grad(int dtype, const void *X, int64_t ldx, int64_t nrows, int
   return rowpass(kGradient, dtype, X, ldx, nrows, p, K, labels, w, nullptr, 0.0, nullptr,
                  nullptr, scale, lam, w, out, nullptr, G_out, nullptr, nullptr, ws, ws_bytes,
                  (cudaStream_t)stream);
+}
+
+int snx_objective_grad_acc(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                           int32_t K, const int32_t *labels, const double *w, double scale,
+                           double lam, double *out, int64_t *correct_out, double *G_out, void *ws,
+                           size_t ws_bytes, void *stream) {
+  if (out == nullptr || w == nullptr || G_out == nullptr || (nrows > 0 && labels == nullptr)) {
+    set_error("snx_objective_grad_acc: NULL out/w/G_out/labels");
+    return 1;
+  }
+  return rowpass(kGradient, dtype, X, ldx, nrows, p, K, labels, w, nullptr, 0.0, nullptr,
+                 nullptr, scale, lam, w, out, reinterpret_cast<long long *>(correct_out), G_out,
+                 nullptr, nullptr, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows, int64_t nrows,

@@ -25,7 +25,7 @@ import torch
 
 from . import softmax
 from .cg import CgConfig, cg_graph_for, cg_solve, report_from
-from .device import as_device, axpy, cuda_device, dot, vec_in, vec_out
+from .device import as_device, axpy, cuda_device, dot, download, vec_in, vec_out
 from .errors import DataError, LineSearchError
 from .linesearch import LineSearchConfig, line_search
 from .sampling import SampleConfig, SubsampledOracle
@@ -115,13 +115,19 @@ def minimize(objective_fn, oracle_factory, x0, cfg, metrics=None, solver_name="n
 
 
 class _Trial:
-    """F(x + a p) and the correct count at that point, one fused device pass."""
+    """F(x + a p) and the correct count at that point, one fused device pass;
+    the first trial (a = alpha0) may be pre-evaluated (speculative pipeline)."""
 
-    def __init__(self, view, lam, x, p):
+    def __init__(self, view, lam, x, p, first=None):
         self.view, self.lam, self.x, self.p = view, lam, x, p
         self.seen = {}
+        if first is not None:
+            self.seen[first[0]] = first[1:]
 
     def __call__(self, a):
+        hit = self.seen.get(a)
+        if hit is not None:
+            return hit[0]
         out, corr = softmax.objective_parts(self.view, self.x, self.p, a, want_correct=True)
         loss, wsq = out.tolist()
         f = loss + 0.5 * self.lam * wsq
@@ -135,6 +141,17 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     x0 defaults to zeros.  Rows log the full objective, train accuracy and,
     with a test set, test accuracy.  x0 may be numpy (x_final is numpy) or a
     CUDA tensor (x_final stays on the device).
+
+    Each outer iteration is enqueued as one speculative pipeline with a single
+    host synchronisation: gradient, ||g||^2, the Hessian sample and the captured
+    CG solve, the slope p.g and the first Armijo trial at x + alpha0 p are all
+    launched before the host reads ||g||, the slope, F(x + alpha0 p) and the CG
+    report together.  With a full gradient sample the first trial is the fused
+    objective + gradient + accuracy pass at x + alpha0 p, so when the Armijo test
+    accepts alpha0 (the usual case) the next iteration's gradient is already
+    computed (bit-identical to recomputing it: same kernel, same point).  The
+    decisions and the trace are the reference's (newton.py:80-104); work done
+    past a stop (||g|| < eps, a failed line search) is discarded.
     """
     ds = as_device(prob.dataset)
     if ds.n_rows == 0:
@@ -147,6 +164,7 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     test = as_device(test_set) if test_set is not None else None
     dev_prob = softmax.SoftmaxProblem(ds, prob.lam)
     lam = prob.lam
+    a0 = cfg.ls.alpha0
 
     def test_acc(w):
         return (float(softmax.correct_count(test, w)) / test.n_rows) if test is not None \
@@ -158,24 +176,56 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     f_cur = loss + 0.5 * lam * wsq
     records = [RunRecord(solver_name, 0, 0.0, f_cur, int(corr) / n, test_acc(x), 0.0, 0)]
     reason = "max-iters"
+    g_next = None  # gradient at x carried from the accepted fused trial
+    oracle_next = None
     for k in range(cfg.max_outer_iters):
-        oracle = SubsampledOracle(dev_prob, cfg.samples, k)
-        g, _ = oracle.gradient_device(x)
-        if math.sqrt(float(dot(g, g))) < cfg.epsilon:
-            reason = "gradient-converged"
-            break
+        oracle = oracle_next if oracle_next is not None else SubsampledOracle(dev_prob,
+                                                                              cfg.samples, k)
+        g = g_next if g_next is not None else oracle.gradient_device(x)[0]
+        g_next = None
+        gg = dot(g, g)
         hess = oracle.hessian_operator(x)
         cgws = cg_graph_for(hess, cfg.cg.max_iters, cfg.cg.theta).run(g)
-        report = report_from(cgws, cfg.cg.max_iters, True)
-        p = report.solution
-        slope = float(dot(p, g))
-        trial = _Trial(ds, lam, x, p)
+        p = cgws.pb.clone()
+        slope_t = dot(p, g)
+        x_try = axpy(x, a0, p)
+        # fused first trial: objective + accuracy (+ gradient when S_g is the full set)
+        fused = None
+        if oracle.gradient_is_full:
+            fused = softmax.gradient_and_correct(ds, x_try, 1.0, lam)
+        if fused is not None:
+            g_try, out_t, corr_t = fused
+        else:
+            g_try = None
+            out_t, corr_t = softmax.objective_parts(ds, x_try, want_correct=True)
+        # the next iteration's samples depend only on k: draw them (host numpy) and
+        # upload the index sets while this iteration's kernels run
+        oracle_next = SubsampledOracle(dev_prob, cfg.samples, k + 1) \
+            if k + 1 < cfg.max_outer_iters else None
+        # the one synchronisation of the iteration (pinned async reads)
+        h_gg, h_slope, h_out, h_corr, h_slot = download(gg, slope_t, out_t, corr_t,
+                                                        cgws.slot(cfg.cg.max_iters))
+        vals = [float(h_gg), float(h_slope), float(h_out[0]), float(h_out[1]),
+                int(h_corr[0])] + h_slot.tolist()
+        if math.sqrt(vals[0]) < cfg.epsilon:
+            reason = "gradient-converged"
+            break
+        report = report_from(cgws, cfg.cg.max_iters, True, slot_values=vals[5:])
+        if int(report.iterations) == 0 and report.converged:
+            p.zero_()  # cg.py:61-62
+        slope = vals[1]
+        f_try = vals[2] + 0.5 * lam * vals[3]
+        trial = _Trial(ds, lam, x, p, first=(a0, f_try, int(vals[4])))
         try:
             alpha, _ = line_search(trial, f_cur, slope, cfg.ls)
         except LineSearchError:
             reason = "line-search-failure"
             break
-        x = axpy(x, alpha, p)
+        if alpha == a0:
+            x = x_try  # the same numpy-rounded x + a0 p (snx_axpy)
+            g_next = g_try
+        else:
+            x = axpy(x, alpha, p)
         f_cur, ncorr = trial.seen[alpha]
         records.append(RunRecord(solver_name, k + 1, time.perf_counter() - t0, f_cur,
                                  ncorr / n, test_acc(x), alpha, report.iterations))

@@ -116,6 +116,23 @@ def gradient_parts(view, w, scale, lam):
     return G, out
 
 
+def gradient_and_correct(view, w, scale, lam):
+    """One pass: (G, [data loss, ||w||^2], correct count) -- snx_objective_grad_acc.
+    None where that fused pass is not built (CSR / wide-class data): the caller
+    evaluates the objective and the gradient separately."""
+    if getattr(view, "is_sparse", False):
+        return None
+    view = view.materialized()
+    if _wide(view):
+        return None
+    out = torch.empty(2, dtype=torch.float64, device=w.device)
+    corr = torch.empty(1, dtype=torch.int64, device=w.device)
+    G = torch.empty_like(w)
+    _lib.call("snx_objective_grad_acc", *_args(view), ptr(view.labels), ptr(w), float(scale),
+              float(lam), ptr(out), ptr(corr), ptr(G), *_ws(view), stream_handle())
+    return G, out, corr
+
+
 def data_objective(ds, x):
     """softmax.py:125-135: sum_i (maxPart_i + logPart_i - linearPart_i)."""
     view = _view(ds)
