@@ -270,6 +270,18 @@ def upload(a, device=None):
     return h.to(device or cuda_device(), non_blocking=True)
 
 
+def download(*ts):
+    """Device tensors -> numpy arrays: asynchronous copies into pinned buffers and
+    ONE stream synchronisation for all of them."""
+    outs = []
+    for t in ts:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t, non_blocking=True)
+        outs.append(h)
+    torch.cuda.current_stream().synchronize()
+    return [h.numpy() for h in outs]
+
+
 def vec_in(x, d, what="weight vector"):
     """User vector -> (contiguous fp64 CUDA tensor of length d, caller_used_torch)."""
     if isinstance(x, torch.Tensor):
