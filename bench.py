@@ -571,7 +571,11 @@ def run_ours(args):
                        "n": N, "p": P, "C": C, "hessian_fraction": F_H, "lam": LAM,
                        "theta": THETA, "cg_max_iters": T_CG, "parallelism": f"rows sharded over {world} GPU(s), NCCL all-reduce per Hv",
                        "l2": "inputs > L2: 1.23 GB X in HBM, fresh S_H gathered every step"},
-            "hv_applied": hv_count, "gpu_launches": args.steps * (4 + 2 + 6 * T_CG),
+            "hv_applied": hv_count, "gpu_launches": args.steps * (
+                # per step: gather + GEMM1 (h prepare), cg_init x2, T x (GEMM1, GEMM2,
+                # cg_step1, cg_step2) [+ snx_finish_hv per product when sharded];
+                # matches profiles/r01_launches.csv (44 per step at N = 1)
+                2 + 2 + T_CG * (4 + (1 if world > 1 else 0))),
             "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
             "cpu_baseline": cpu, "newton_solve": solve, "other_shapes": shapes,
         }

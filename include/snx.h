@@ -280,6 +280,20 @@ int snx_libsvm_scan(const char *path, int64_t *nrows, int64_t *nnz, int64_t *max
 int snx_libsvm_fetch(const char *path, double *labels, int64_t *indptr, int32_t *indices,
                      double *data);
 
+/* Steihaug-CG of the sub-sampled trust-region Newton variant (BASELINE config
+ * #4; no reference counterpart -- oracle/trust_region.py steihaug_cg, N&W
+ * Alg. 7.2), device resident.  state: (max_iters + 2) * SNX_CG_SLOT +
+ * 4 * SNX_DOT_BLOCKS doubles; slot j = [rr, done, boundary, iters, model m,
+ * tol]; snx_tr_init sets z = 0, r = g, d = -g and slot 0.  Iteration j:
+ * snx_hess_apply(d -> Hd, dots = [d.Hd | d.d], skip = snx_cg_done_flag-style
+ * &state[j * SNX_CG_SLOT + 1]) then snx_tr_update(j, ...) (radius: device
+ * scalar).  The step is z; slot max_iters holds m(z), iterations, boundary. */
+int snx_tr_init(const double *g, int64_t d, double theta, int32_t max_iters, double *z,
+                double *r, double *dvec, double *state, void *stream);
+int snx_tr_update(int32_t j, int32_t max_iters, int64_t d, const double *radius,
+                  const double *Hd, const double *dots, double *z, double *r, double *dvec,
+                  double *znew, double *state, void *stream);
+
 /* Copy+convert host-layout helpers (device to device). */
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
                   int64_t ldd, void *stream);

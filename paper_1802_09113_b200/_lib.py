@@ -83,6 +83,9 @@ SIGNATURES = {
                                     _c_p]),
     "snx_libsvm_scan": (_c_int, [ctypes.c_char_p, _c_p, _c_p, _c_p]),
     "snx_libsvm_fetch": (_c_int, [ctypes.c_char_p, _c_p, _c_p, _c_p, _c_p]),
+    "snx_tr_init": (_c_int, [_c_p, _c_i64, _c_dbl, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p]),
+    "snx_tr_update": (_c_int, [_c_i32, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
+                               _c_p, _c_p]),
     "snx_pack_rows": (_c_int, [_c_int, _c_p, _c_i64, _c_i32, _c_p, _c_i64, _c_p]),
 }
 

@@ -385,6 +385,179 @@ __global__ void __launch_bounds__(kDotThreads)
     v[i] = __ddiv_rn(w[i], nw);
 }
 
+// ------------------------------------------------ Steihaug-CG (trust region)
+// N&W Alg. 7.2 as in oracle/trust_region.py steihaug_cg, device resident.  state:
+// (T + 2) slots of SNX_CG_SLOT doubles, slot j = the scalars entering iteration
+// j: [rr, done, boundary, iters, m, tol, -, -], then 4 x kDotBlocks partials
+// (z.d | z.z | znew.znew | r.r).  Every kernel of iteration j reads slot j and
+// writes slot j + 1 only (no block reads a field another block of the same
+// launch writes); every block reduces the partials in the same fixed order.
+enum { kTrRs = 0, kTrDone = 1, kTrBnd = 2, kTrIters = 3, kTrM = 4, kTrTol = 5 };
+
+__device__ __forceinline__ double *tr_scratch(double *state, int T) {
+  return state + (T + 2) * SNX_CG_SLOT;
+}
+
+__global__ void __launch_bounds__(kDotThreads)
+    tr_init_kernel(const double *__restrict__ g, int64_t d, int T, double *z, double *r,
+                   double *dv, double *state) {
+  __shared__ double sh[kDotThreads / 32];
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    const double gi = g[i];
+    z[i] = 0.0;
+    r[i] = gi;   // r0 = g
+    dv[i] = -gi; // d0 = -r0
+    acc += gi * gi;
+  }
+  const double b = block_sum<kDotThreads>(acc, sh);
+  if (threadIdx.x == 0) tr_scratch(state, T)[3 * kDotBlocks + blockIdx.x] = b;
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < (T + 2) * SNX_CG_SLOT; i += kDotThreads) state[i] = 0.0;
+}
+
+__global__ void tr_init_final_kernel(double theta, int T, double *state) {
+  const double gg = warp_sum_partials(tr_scratch(state, T) + 3 * kDotBlocks);
+  if (threadIdx.x == 0) {
+    double *s0 = slot(state, 0);
+    const double gn = sqrt(gg);  // np.linalg.norm(g)
+    s0[kTrRs] = gg;
+    s0[kTrTol] = theta * gn;
+    s0[kTrDone] = gn == 0.0 ? 1.0 : 0.0;  // zero step, 0 iterations
+  }
+}
+
+// Iteration j, part 1: alpha = rr / dHd; znew = z + alpha d; partials of z.d,
+// z.z, znew.znew (the boundary root and the |z_{j+1}| >= radius test).
+__global__ void __launch_bounds__(kDotThreads)
+    tr_step1_kernel(int j, int T, int64_t d, const double *__restrict__ dots,
+                    const double *__restrict__ z, const double *__restrict__ dv,
+                    double *__restrict__ znew, double *state) {
+  const double *st = slot(state, j);
+  if (st[kTrDone] != 0.0) return;
+  __shared__ double sh[kDotThreads / 32];
+  __shared__ double s_a;
+  if (threadIdx.x < 32) {
+    const double dhd = warp_sum_partials(dots);
+    if (threadIdx.x == 0) s_a = st[kTrRs] / dhd;
+  }
+  __syncthreads();
+  const double a = s_a;
+  double zd = 0.0, zz = 0.0, nn = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    const double zi = z[i], di = dv[i];
+    const double zn = np_axpy(zi, a, di);  // z + a * d
+    znew[i] = zn;
+    zd += zi * di;
+    zz += zi * zi;
+    nn += zn * zn;
+  }
+  double *sc = tr_scratch(state, T);
+  const double b0 = block_sum<kDotThreads>(zd, sh);
+  const double b1 = block_sum<kDotThreads>(zz, sh);
+  const double b2 = block_sum<kDotThreads>(nn, sh);
+  if (threadIdx.x == 0) {
+    sc[blockIdx.x] = b0;
+    sc[kDotBlocks + blockIdx.x] = b1;
+    sc[2 * kDotBlocks + blockIdx.x] = b2;
+  }
+}
+
+// Iteration j, part 2: negative curvature or |znew| >= radius -> the boundary
+// step z + tau d (done); else z = znew, r += alpha Hd, partials of r.r.
+__global__ void __launch_bounds__(kDotThreads)
+    tr_step2_kernel(int j, int T, int64_t d, const double *__restrict__ radius,
+                    const double *__restrict__ Hd, const double *__restrict__ dots,
+                    double *z, double *r, const double *__restrict__ dv,
+                    const double *__restrict__ znew, double *state) {
+  const double *st = slot(state, j);
+  if (st[kTrDone] != 0.0) return;
+  __shared__ double sh[kDotThreads / 32];
+  __shared__ double s_v[6];
+  if (threadIdx.x < 32) {
+    const double *sc = tr_scratch(state, T);
+    const double dhd = warp_sum_partials(dots);
+    const double dd = warp_sum_partials(dots + kDotBlocks);
+    const double zd = warp_sum_partials(sc);
+    const double zz = warp_sum_partials(sc + kDotBlocks);
+    const double nn = warp_sum_partials(sc + 2 * kDotBlocks);
+    if (threadIdx.x == 0) {
+      const double rr = st[kTrRs], rad = *radius;
+      const bool bnd = dhd <= 0.0 || sqrt(nn) >= rad;
+      double step;
+      if (bnd) {  // _to_boundary(z, d, radius)
+        const double disc = zd * zd + dd * (rad * rad - zz);
+        step = (-zd + sqrt(fmax(disc, 0.0))) / dd;
+      } else {
+        step = rr / dhd;
+      }
+      s_v[0] = bnd ? 1.0 : 0.0;
+      s_v[1] = step;
+      s_v[2] = st[kTrM] + (-step * rr + 0.5 * step * step * dhd);
+    }
+  }
+  __syncthreads();
+  const bool bnd = s_v[0] != 0.0;
+  const double step = s_v[1];
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    double *nx = slot(state, j + 1);
+    nx[kTrRs] = st[kTrRs];
+    nx[kTrTol] = st[kTrTol];
+    nx[kTrM] = s_v[2];
+    nx[kTrBnd] = bnd ? 1.0 : 0.0;
+    nx[kTrIters] = j + 1;
+    nx[kTrDone] = bnd ? 1.0 : 0.0;
+  }
+  double acc = 0.0;
+  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+       i += (int64_t)kDotBlocks * kDotThreads) {
+    if (bnd) {
+      z[i] = np_axpy(z[i], step, dv[i]);
+    } else {
+      z[i] = znew[i];
+      const double ri = np_axpy(r[i], step, Hd[i]);  // r + a * Hd
+      r[i] = ri;
+      acc += ri * ri;
+    }
+  }
+  if (bnd) return;
+  const double b = block_sum<kDotThreads>(acc, sh);
+  if (threadIdx.x == 0) tr_scratch(state, T)[3 * kDotBlocks + blockIdx.x] = b;
+}
+
+// Iteration j, part 3: |r| <= tol -> done; else d = -r + (rr_next / rr) d.
+__global__ void __launch_bounds__(kDotThreads)
+    tr_step3_kernel(int j, int T, int64_t d, const double *__restrict__ r, double *dv,
+                    double *state) {
+  const double *st = slot(state, j);
+  double *nx = slot(state, j + 1);
+  if (st[kTrDone] != 0.0) {  // finished earlier: carry the scalars forward
+    if (blockIdx.x == 0 && threadIdx.x < SNX_CG_SLOT) nx[threadIdx.x] = st[threadIdx.x];
+    return;
+  }
+  if (nx[kTrBnd] != 0.0) return;  // boundary step taken in part 2
+  __shared__ double s_rr;
+  if (threadIdx.x < 32) {
+    const double rr = warp_sum_partials(tr_scratch(state, T) + 3 * kDotBlocks);
+    if (threadIdx.x == 0) s_rr = rr;
+  }
+  __syncthreads();
+  const double rrn = s_rr;
+  const bool conv = sqrt(rrn) <= st[kTrTol];
+  if (!conv) {
+    const double beta = rrn / st[kTrRs];
+    for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
+         i += (int64_t)kDotBlocks * kDotThreads)
+      dv[i] = __dadd_rn(-r[i], __dmul_rn(beta, dv[i]));
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    nx[kTrRs] = conv ? st[kTrRs] : rrn;
+    nx[kTrDone] = (conv || j + 1 >= T) ? 1.0 : 0.0;
+  }
+}
+
 template <typename T>
 __global__ void pack_rows_kernel(const double *__restrict__ src, int64_t nrows, int p,
                                  T *__restrict__ dst, int64_t ldd) {
@@ -486,6 +659,37 @@ int snx_power_step(double *v, const double *w, int64_t d, double *state, void *s
   if (check_launch("power_part")) return 1;
   power_scale_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(v, w, d, state);
   return check_launch("power_scale");
+}
+
+int snx_tr_init(const double *g, int64_t d, double theta, int32_t max_iters, double *z,
+                double *r, double *dvec, double *state, void *stream) {
+  if (max_iters < 1) {
+    set_error("snx_tr_init: max_iters must be >= 1");
+    return 1;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  tr_init_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(g, d, max_iters, z, r, dvec, state);
+  if (check_launch("tr_init")) return 1;
+  tr_init_final_kernel<<<1, 32, 0, st>>>(theta, max_iters, state);
+  return check_launch("tr_init_final");
+}
+
+int snx_tr_update(int32_t j, int32_t max_iters, int64_t d, const double *radius,
+                  const double *Hd, const double *dots, double *z, double *r, double *dvec,
+                  double *znew, double *state, void *stream) {
+  if (j < 0 || j >= max_iters) {
+    set_error("snx_tr_update: iteration %d outside [0, %d)", j, max_iters);
+    return 1;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  tr_step1_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(j, max_iters, d, dots, z, dvec, znew,
+                                                      state);
+  if (check_launch("tr_step1")) return 1;
+  tr_step2_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(j, max_iters, d, radius, Hd, dots, z, r,
+                                                      dvec, znew, state);
+  if (check_launch("tr_step2")) return 1;
+  tr_step3_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(j, max_iters, d, r, dvec, state);
+  return check_launch("tr_step3");
 }
 
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
