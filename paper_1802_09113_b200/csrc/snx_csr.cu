@@ -345,7 +345,8 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int64_t *__restrict__ 
   const int64_t per = (n + 1023) / 1024;
   const int64_t b0 = t * per, b1 = min(n, b0 + per);
   int64_t s = 0;
-  for (int64_t i = b0; i < b1; ++i) s += in[i];
+#pragma unroll 8
+  for (int64_t i = b0; i < b1; ++i) s += __ldg(in + i);
   sh[t] = s;
   __syncthreads();
   for (int o = 1; o < 1024; o <<= 1) {  // Hillis-Steele inclusive scan of the chunk sums
@@ -355,8 +356,9 @@ __global__ void __launch_bounds__(1024) scan_kernel(const int64_t *__restrict__ 
     __syncthreads();
   }
   int64_t run = sh[t] - s;
+#pragma unroll 8
   for (int64_t i = b0; i < b1; ++i) {
-    const int64_t v = in[i];
+    const int64_t v = __ldg(in + i);
     out[i] = run;
     run += v;
   }
