@@ -28,10 +28,11 @@ import torch.distributed as dist
 
 from . import _lib, softmax
 from .cg import CgWorkspace, enqueue_cg, report_from
-from .device import DeviceDataset, as_device, axpy, dot, ptr, stream_handle, vec_in, vec_out
+from .device import (DeviceDataset, as_device, axpy, dot, download, ptr, stream_handle, vec_in,
+                     vec_out)
 from .errors import DataError, LineSearchError
 from .linesearch import line_search
-from .sampling import draw_samples
+from .sampling import draw_samples, sample_size
 from .trace import RunRecord, SolveTrace
 
 
@@ -89,14 +90,34 @@ class ShardedProblem:
     def row1(self):
         return self.row0 + self.local.n_rows
 
-    def objective_and_correct(self, w, direction=None, alpha=0.0):
-        """Global (F(w_eff), #correct) with one all-reduce of two scalars."""
+    def objective_parts_device(self, w, direction=None, alpha=0.0):
+        """Device [global data loss, global #correct] (one all-reduce of two
+        scalars) and the local [loss, ||w_eff||^2] (the norm is replicated)."""
         out, corr = softmax.objective_parts(self.local, w, direction, alpha, want_correct=True)
         buf = torch.stack([out[0], corr[0].to(torch.float64)])
         all_reduce_(buf, self.group)
-        loss, ncorr = buf.tolist()
-        wsq = float(out[1])  # weights are replicated: identical on every rank
+        return buf, out
+
+    def objective_and_correct(self, w, direction=None, alpha=0.0):
+        """Global (F(w_eff), #correct) with one all-reduce of two scalars."""
+        buf, out = self.objective_parts_device(w, direction, alpha)
+        (loss, ncorr), (_, wsq) = buf.tolist(), out.tolist()
         return loss + 0.5 * self.lam * wsq, int(round(ncorr))
+
+    def gradient_and_objective_device(self, w):
+        """Fused pass at w over the full data: (global gradient + lam w, global
+        [loss, #correct], local [loss, ||w||^2]); None where the fused pass is
+        not built (CSR / wide classes)."""
+        fused = softmax.gradient_and_correct(self.local, w, 1.0, 0.0)
+        if fused is None:
+            return None
+        G, out, corr = fused
+        all_reduce_(G, self.group)
+        _lib.call("snx_finish_hv", ptr(w), self.lam, G.numel(), ptr(G), None, None,
+                  stream_handle())
+        buf = torch.stack([out[0], corr[0].to(torch.float64)])
+        all_reduce_(buf, self.group)
+        return G, buf, out
 
 
 class ShardedHessian:
@@ -159,39 +180,66 @@ class ShardedOracle:
 
 
 def newton_solve_sharded(sp, cfg, x0=None, solver_name="newton"):
-    """newton.py:115-140 on a row-sharded problem; every rank returns the same trace."""
+    """newton.py:115-140 on a row-sharded problem; every rank returns the same trace.
+
+    One host synchronisation per outer iteration, as newton.newton_solve: the
+    gradient (all-reduced), CG (one all-reduce per product), the slope and the
+    first Armijo trial (fused with the gradient at the trial point when S_g is
+    the full set) are enqueued before the host reads the scalars."""
     d = sp.dim
     x, as_t = vec_in(np.zeros(d) if x0 is None else x0, d, "initial point")
     x = x.clone()
     n = sp.n_global
+    a0 = cfg.ls.alpha0
+    full_g = (not cfg.samples.with_replacement
+              and sample_size(cfg.samples.gradient_fraction, n) == n)
     cgws = CgWorkspace(d, cfg.cg.max_iters, x.device)
     t0 = time.perf_counter()
     f_cur, corr = sp.objective_and_correct(x)
     records = [RunRecord(solver_name, 0, 0.0, f_cur, corr / n, math.nan, 0.0, 0)]
     reason = "max-iters"
+    g_next = None
     for k in range(cfg.max_outer_iters):
         oracle = ShardedOracle(sp, cfg.samples, k)
-        g = oracle.gradient_device(x)
-        if math.sqrt(float(dot(g, g))) < cfg.epsilon:
-            reason = "gradient-converged"
-            break
+        g = g_next if g_next is not None else oracle.gradient_device(x)
+        g_next = None
+        gg = dot(g, g)
         hess = oracle.hessian_operator(x)
         enqueue_cg(hess, g, cfg.cg.theta, cfg.cg.max_iters, cgws)
-        report = report_from(cgws, cfg.cg.max_iters, True)
-        p = report.solution
-        slope = float(dot(p, g))
-        seen = {}
+        p = cgws.pb.clone()
+        slope_t = dot(p, g)
+        x_try = axpy(x, a0, p)
+        fused = sp.gradient_and_objective_device(x_try) if full_g else None
+        if fused is not None:
+            g_try, buf, out = fused
+        else:
+            g_try = None
+            buf, out = sp.objective_parts_device(x_try)
+        h_gg, h_slope, h_buf, h_out, h_slot = download(gg, slope_t, buf, out,
+                                                       cgws.slot(cfg.cg.max_iters))
+        if math.sqrt(float(h_gg)) < cfg.epsilon:
+            reason = "gradient-converged"
+            break
+        report = report_from(cgws, cfg.cg.max_iters, True, slot_values=h_slot.tolist())
+        if report.iterations == 0 and report.converged:
+            p.zero_()  # cg.py:61-62
+        seen = {a0: (float(h_buf[0]) + 0.5 * sp.lam * float(h_out[1]), int(round(h_buf[1])))}
 
         def trial(a):
-            seen[a] = sp.objective_and_correct(x, p, a)
+            if a not in seen:
+                seen[a] = sp.objective_and_correct(x, p, a)
             return seen[a][0]
 
         try:
-            alpha, _ = line_search(trial, f_cur, slope, cfg.ls)
+            alpha, _ = line_search(trial, f_cur, float(h_slope), cfg.ls)
         except LineSearchError:
             reason = "line-search-failure"
             break
-        x = axpy(x, alpha, p)
+        if alpha == a0:
+            x = x_try
+            g_next = g_try
+        else:
+            x = axpy(x, alpha, p)
         f_cur, corr = seen[alpha]
         records.append(RunRecord(solver_name, k + 1, time.perf_counter() - t0, f_cur, corr / n,
                                  math.nan, alpha, report.iterations))

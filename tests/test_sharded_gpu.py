@@ -67,3 +67,18 @@ def test_two_shards_sum_to_full():
     h = oracle.hess_probs(A[s_h], y[s_h], C, x)
     assert rel_err(hv, oracle.hess_apply(A[s_h], h, C, v, n / len(s_h), lam)) <= 1e-10
     assert abs(loss_sum - oracle.data_loss(A, y, C, x)) <= 1e-10 * abs(loss_sum)
+
+
+def test_world1_sharded_full_gradient_pipeline():
+    """subsampled-100 (full S_g): the fused trial/gradient pass is reused."""
+    A, y = oracle.synthetic_problem(3000, 48, 10, seed=23)
+    cfg = snx.make_variant("subsampled-100", snx.NewtonConfig(max_outer_iters=6))
+    ds = snx.DeviceDataset.from_numpy(A, y, 10)
+    ref = snx.newton_solve(snx.SoftmaxProblem(ds, 1e-3), cfg)
+    got = sd.newton_solve_sharded(sd.ShardedProblem.from_global(A, y, 10, 1e-3), cfg)
+    assert got.reason == ref.reason
+    assert rel_err(got.x_final, ref.x_final) <= 1e-12
+    for a, b in zip(got.records, ref.records):
+        assert abs(a.objective - b.objective) <= 1e-13 * abs(b.objective)
+        assert a.cg_iters == b.cg_iters and a.step_size == b.step_size
+        assert a.train_acc == b.train_acc
