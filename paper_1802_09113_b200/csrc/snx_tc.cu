@@ -509,15 +509,27 @@ __global__ void tc_split_kernel(const float *__restrict__ X, int64_t ldx, int64_
 // the accumulators out in 16-class chunks; the last segment of a GEMM1 row
 // block keeps the row's V in shared memory for the row algebra (ComputeU, or
 // the softmax probabilities when preparing h).
-template <int KP> struct WShape {
+constexpr size_t kSmemMax = 227 * 1024;  // opt-in dynamic shared memory per CTA
+
+template <int KP> struct WShape {  // GEMM1: pipeline stages + the V buffer of the row algebra
   static constexpr int N1 = 2 * KP;
   static constexpr uint32_t BB = (uint32_t)N1 * 128;
   static constexpr uint32_t STAGE = 2 * kXB + BB;
-  static constexpr int S = 2;
   static constexpr int VS = 129;                    // V row stride (conflict-free columns)
   static constexpr uint32_t VB = (uint32_t)VS * KP * 4u;  // f32 V[c][row]
+  static constexpr int SF = (int)((kSmemMax - VB - 1024) / STAGE);  // stages that fit
+  static constexpr int S = SF < 2 ? 2 : (SF > 4 ? 4 : SF);
   static constexpr size_t SMEM = (size_t)S * STAGE + VB + 1024;
   static constexpr uint32_t TMEM = 4 * KP <= 64 ? 64 : 4 * KP <= 128 ? 128 : 4 * KP <= 256 ? 256 : 512;
+};
+
+template <int KP> struct W2Shape {  // GEMM2: no V buffer, so deeper pipelines fit
+  static constexpr int N1 = 2 * KP;
+  static constexpr uint32_t STAGE = WShape<KP>::STAGE;
+  static constexpr int SF = (int)((kSmemMax - 1024) / STAGE);
+  static constexpr int S = SF < 2 ? 2 : (SF > 6 ? 6 : SF);
+  static constexpr size_t SMEM = (size_t)S * STAGE + 1024;
+  static constexpr uint32_t TMEM = WShape<KP>::TMEM;
 };
 
 template <int KP>
@@ -825,7 +837,7 @@ __global__ void __launch_bounds__(kThreads, 1) tcw_gemm1_kernel(const __grid_con
 template <int KP>
 __global__ void __launch_bounds__(kThreads, 1) tcw_gemm2_kernel(const __grid_constant__ Tc2Args a) {
   if (a.skip != nullptr && *a.skip != 0.0) return;
-  using W = WShape<KP>;
+  using W = W2Shape<KP>;
   extern __shared__ uint8_t smraw[];
   uint8_t *sm = align1024(smraw);
   __shared__ BarT<W::S> b;
@@ -1013,7 +1025,7 @@ int run_tcw(const Tc1Args &a1, int g1, const Tc2Args *a2, int g2, cudaStream_t s
     return 1;
   if (a2 == nullptr) return 0;
   return launch_tc(tcw_gemm2_kernel<KP>, g2, *a2, st, &c2, "tcw_gemm2", tc_pdl(),
-                   WShape<KP>::SMEM);
+                   W2Shape<KP>::SMEM);
 }
 
 int dispatch_wide(int KP, const Tc1Args &a1, int g1, const Tc2Args *a2, int g2,
