@@ -88,6 +88,16 @@ int snx_objective_grad_acc(int dtype, const void *X, int64_t ldx, int64_t nrows,
                            double lam, double *out, int64_t *correct_out, double *G_out, void *ws,
                            size_t ws_bytes, void *stream);
 
+/* softmax.py:224-240 class_probabilities / predict and :107-122 row_stats in
+ * one row pass (each output nullable):
+ *   probs_out[r*(K+1) + c] = E_rc / alpha_r (c < K), [K] = e^-M_r / alpha_r
+ *   pred_out[r]  = argmax over the K+1 probabilities, first max wins
+ *   stats_out[r*3 + 0..2] = (M_r, sum_c E_rc, linear part z_{r,y_r})  (labels needed) */
+int snx_class_probabilities(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                            int32_t K, const int32_t *labels, const double *w, double *probs_out,
+                            int32_t *pred_out, double *stats_out, void *ws, size_t ws_bytes,
+                            void *stream);
+
 /* softmax.py:181-195 (HessianOperator.__init__) on the sample rows S_H:
  * when rows != NULL the sample is first gathered into Xs_out (ld_out), else
  * X itself is the sample (the f = 1 identity, dataset.py:94-96).
@@ -248,6 +258,11 @@ int snx_csr_objective_grad(const int64_t *indptr, const int32_t *indices, const 
                            int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
                            const double *w, double scale, double lam, double *out, double *G_out,
                            void *ws, size_t ws_bytes, void *stream);
+int snx_csr_class_probabilities(const int64_t *indptr, const int32_t *indices,
+                                const double *data, int64_t nrows, int32_t p, int32_t K,
+                                const int32_t *labels, const double *w, double *probs_out,
+                                int32_t *pred_out, double *stats_out, void *ws, size_t ws_bytes,
+                                void *stream);
 /* The row sample S (sorted int64, duplicates allowed: sampling with
  * replacement) as its own CSR (s_indptr[m+1], entries in the order of the
  * source rows) and CSC (s_colptr[p+1], rows renumbered to sample positions,

@@ -17,9 +17,10 @@ from .lipschitz import estimate_lipschitz
 from .newton import VARIANT_FRACTIONS, NewtonConfig, make_variant, minimize, newton_solve
 from .rng import stream_rng
 from .sampling import SampleConfig, SubsampledOracle, draw_samples, sample_size
-from .softmax import (BLOCK_ROWS, HessianOperator, SoftmaxProblem, accuracy, data_gradient,
-                      data_objective, gradient, hess_vec, matrix_as_weights, objective,
-                      weights_as_matrix, zero_weights)
+from .softmax import (BLOCK_ROWS, HessianOperator, RowStats, SoftmaxProblem, accuracy,
+                      class_probabilities, data_gradient, data_objective, gradient, hess_vec,
+                      matrix_as_weights, objective, predict, row_stats, weights_as_matrix,
+                      zero_weights)
 from .trace import RunRecord, SolveTrace, read_trace_csv, write_trace_csv
 from .trust_region import TrustRegionConfig, steihaug_cg, trust_region_solve
 
@@ -35,5 +36,6 @@ __all__ = [
     "matrix_as_weights", "objective", "weights_as_matrix", "zero_weights", "RunRecord",
     "SolveTrace", "TrustRegionConfig", "steihaug_cg", "trust_region_solve",
     "estimate_lipschitz", "column_norms", "normalize_columns", "train_test_split",
-    "read_trace_csv", "write_trace_csv", "load_libsvm", "load_csv",
+    "read_trace_csv", "write_trace_csv", "load_libsvm", "load_csv", "RowStats", "row_stats",
+    "class_probabilities", "predict",
 ]

@@ -33,6 +33,10 @@ SIGNATURES = {
                                     _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_objective_grad_acc": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                         _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_class_probabilities": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                         _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
+    "snx_csr_class_probabilities": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                             _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_hess_prepare": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p,
                                   _c_p, _c_i64, _c_p, _c_p, _c_size, _c_p]),
     "snx_hess_apply": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,

@@ -30,7 +30,7 @@ constexpr int kCsrThreads = 256;
 constexpr int kCsrWarps = kCsrThreads / 32;
 constexpr int kRowBlocks = 148 * 4;  // fixed grid of the rows pass (loss partials)
 
-enum CsrMode { kObj = 0, kGrad = 1, kPrep = 2, kApply = 3 };
+enum CsrMode { kObj = 0, kGrad = 1, kPrep = 2, kApply = 3, kProbs = 4 };
 
 __host__ __device__ constexpr size_t al256(size_t x) { return (x + 255) / 256 * 256; }
 
@@ -123,7 +123,8 @@ __global__ void __launch_bounds__(kCsrThreads)
                     int64_t nrows, const double *__restrict__ wt, const int32_t *__restrict__ labels,
                     const double *__restrict__ H, double *__restrict__ rowout,
                     double *__restrict__ loss_part, unsigned long long *__restrict__ corr_part,
-                    const double *skip) {
+                    const double *skip, int32_t *__restrict__ pred_out = nullptr,
+                    double *__restrict__ stats_out = nullptr) {
   if (skip != nullptr && *skip != 0.0) return;
   __shared__ double shl[kCsrWarps];
   __shared__ unsigned long long shc[kCsrWarps];
@@ -176,6 +177,40 @@ __global__ void __launch_bounds__(kCsrThreads)
         if (lane == c) rowout[r * K + c] = E[c] / alpha;
       continue;
     }
+    if (mode == kProbs) {  // softmax.py:224-240 and row_stats :107-122
+      if (rowout != nullptr) {
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+          if (lane == c) rowout[r * (K + 1) + c] = E[c] / alpha;
+        if (lane == 31) rowout[r * (K + 1) + K] = exp(-M) / alpha;
+      }
+      if (lane == 0 && stats_out != nullptr) {
+        const int yy = labels[r];
+        double lin = 0.0;
+#pragma unroll
+        for (int c = 0; c < K; ++c)
+          if (c == yy) lin = z[c];
+        stats_out[r * 3 + 0] = M;
+        stats_out[r * 3 + 1] = se;
+        stats_out[r * 3 + 2] = lin;
+      }
+      if (lane == 0 && pred_out != nullptr) {
+        int best = 0;
+        double bv = E[0] / alpha;
+        bool nan_hit = isnan(bv);
+#pragma unroll
+        for (int c = 1; c <= K; ++c) {
+          const double pc = (c < K ? E[c] : exp(-M)) / alpha;
+          if (!nan_hit && (isnan(pc) || pc > bv)) {
+            best = c;
+            bv = pc;
+            nan_hit = isnan(pc);
+          }
+        }
+        pred_out[r] = best;
+      }
+      continue;
+    }
     const int y = labels[r];
     double lin = 0.0;
 #pragma unroll
@@ -203,7 +238,7 @@ __global__ void __launch_bounds__(kCsrThreads)
       cacc += (best == y) ? 1ull : 0ull;
     }
   }
-  if (mode == kPrep || mode == kApply || loss_part == nullptr) return;
+  if (mode == kPrep || mode == kApply || mode == kProbs || loss_part == nullptr) return;
   if (lane == 0) {
     shl[warp] = lacc;
     shc[warp] = cacc;
@@ -504,6 +539,27 @@ int snx_csr_objective(const int64_t *indptr, const int32_t *indices, const doubl
   csr_final_kernel<<<1, 32, 0, st>>>(W.loss_part, W.corr_part, W.wsq_part, out,
                                      reinterpret_cast<long long *>(correct_out));
   return check_launch("csr_final");
+}
+
+int snx_csr_class_probabilities(const int64_t *indptr, const int32_t *indices,
+                                const double *data, int64_t nrows, int32_t p, int32_t K,
+                                const int32_t *labels, const double *w, double *probs_out,
+                                int32_t *pred_out, double *stats_out, void *ws, size_t ws_bytes,
+                                void *stream) {
+  if (check_ws("snx_csr_class_probabilities", nrows, p, K, ws_bytes)) return 1;
+  cudaStream_t st = (cudaStream_t)stream;
+  CsrWs W;
+  csr_ws_layout(nrows, p, K, static_cast<char *>(ws), &W);
+  return dispatch_k(K, [&](auto kk) {
+    constexpr int KK = decltype(kk)::value;
+    csr_prep_w_kernel<KK><<<kDotBlocks, kCsrThreads, 0, st>>>(w, nullptr, 0.0, p, W.wt, nullptr,
+                                                             nullptr);
+    if (check_launch("csr_prep_w")) return 1;
+    csr_rows_kernel<KK><<<kRowBlocks, kCsrThreads, 0, st>>>(
+        kProbs, indptr, indices, data, nrows, W.wt, labels, nullptr, probs_out, nullptr, nullptr,
+        nullptr, pred_out, stats_out);
+    return check_launch("csr_rows(probabilities)");
+  });
 }
 
 int snx_csr_objective_grad(const int64_t *indptr, const int32_t *indices, const double *data,

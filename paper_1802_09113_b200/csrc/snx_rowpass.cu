@@ -40,7 +40,7 @@
 
 namespace snx {
 
-enum Mode { kObjective = 0, kGradient = 1, kHessPrep = 2, kHessApply = 3 };
+enum Mode { kObjective = 0, kGradient = 1, kHessPrep = 2, kHessApply = 3, kProbs = 4 };
 
 constexpr int kWarps = 8;                    // consumer warps
 constexpr int kConsumers = kWarps * 32;      // consumer threads
@@ -206,6 +206,8 @@ struct G1Args {
   long long *corr_out;
   const double *skip;
   unsigned *u_ready;   // persistent CG kernel: publish U rows of a row block (epoch)
+  int32_t *pred_out;   // kProbs: most probable class per row (nullable)
+  double *stats_out;   // kProbs: [M, sum E, linear] per row (nullable)
 };
 
 // Per-row softmax algebra on the summed logits z (softmax.py:85-99 and the
@@ -244,6 +246,41 @@ __device__ __forceinline__ void row_epilogue(const G1Args &a, int64_t r, const d
     T *h = static_cast<T *>(a.rowout) + r * a.ustride;
 #pragma unroll
     for (int c = 0; c < K; ++c) h[c] = (T)(E[c] / alpha);
+    return;
+  }
+  if (a.mode == kProbs) {
+    // softmax.py:224-235 class_probabilities (reference class last), :238-240
+    // predict (first max wins), :107-122 row_stats (max, sum of E, linear part)
+    if (a.rowout != nullptr) {
+      double *pr = static_cast<double *>(a.rowout) + r * (K + 1);
+#pragma unroll
+      for (int c = 0; c < K; ++c) pr[c] = E[c] / alpha;
+      pr[K] = exp(-M) / alpha;
+    }
+    if (a.stats_out != nullptr) {
+      double lin = 0.0;
+#pragma unroll
+      for (int c = 0; c < K; ++c)
+        if (c == y) lin = z[c];
+      a.stats_out[r * 3 + 0] = M;
+      a.stats_out[r * 3 + 1] = se;
+      a.stats_out[r * 3 + 2] = lin;
+    }
+    if (a.pred_out != nullptr) {
+      int best = 0;
+      double bv = E[0] / alpha;
+      bool nan_hit = isnan(bv);
+#pragma unroll
+      for (int c = 1; c <= K; ++c) {
+        const double pc = (c < K ? E[c] : exp(-M)) / alpha;
+        if (!nan_hit && (isnan(pc) || pc > bv)) {
+          best = c;
+          bv = pc;
+          nan_hit = isnan(pc);
+        }
+      }
+      a.pred_out[r] = best;
+    }
     return;
   }
   double lin = 0.0;
@@ -320,7 +357,7 @@ __device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, 
       const T *h = static_cast<const T *>(a.H) + r * K;
 #pragma unroll
       for (int c = 0; c < K; ++c) hw[c] = (double)h[c];
-    } else if (a.mode != kHessPrep) {
+    } else if (a.mode != kHessPrep && a.labels != nullptr) {
       y = a.labels[r];
     }
   }
@@ -1659,12 +1696,17 @@ struct CgFuse {  // snx_hess_apply_cg: the CG iteration fused into GEMM2's tail
   int t, T;
 };
 
+struct ProbsOut {
+  int32_t *pred;
+  double *stats;
+};
+
 static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
                    int32_t K, const int32_t *labels, const double *w, const double *dir,
                    double alpha, const void *H, void *rowout, double scale, double lam,
                    const double *base, double *out, long long *corr_out, double *vec_out,
                    double *dots, const double *skip, void *ws, size_t ws_bytes,
-                   cudaStream_t st, const CgFuse *cg = nullptr) {
+                   cudaStream_t st, const CgFuse *cg = nullptr, const ProbsOut *po = nullptr) {
   if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
   const int32_t P = padded(p);
   const Geometry g = geometry(dtype, nrows, P, K);
@@ -1701,7 +1743,7 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   }
 
   const size_t tb = dtype_bytes(dtype);
-  void *rowbuf = rowout ? rowout : (void *)(wsb + lay.rowbuf);
+  void *rowbuf = (rowout || mode == kProbs) ? rowout : (void *)(wsb + lay.rowbuf);
   double *zp = reinterpret_cast<double *>(wsb + lay.zp);
   G1Args a{};
   if (make_map(&a.xmap, dtype, X, P, nrows, ldx, (uint32_t)(128 / tb), kRB, true)) return 1;
@@ -1724,6 +1766,8 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   a.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
   a.loss_out = out;
   a.corr_out = corr_out;
+  a.pred_out = po ? po->pred : nullptr;
+  a.stats_out = po ? po->stats : nullptr;
   int rc = 1;
   if (dtype == SNX_F64) {
     SNX_K_SWITCH(K, (rc = launch_gemm1<double, KK>(a, g.grid1, st)));
@@ -1961,6 +2005,20 @@ int snx_objective_grad(int dtype, const void *X, int64_t ldx, int64_t nrows, int
   return rowpass(kGradient, dtype, X, ldx, nrows, p, K, labels, w, nullptr, 0.0, nullptr,
                  nullptr, scale, lam, w, out, nullptr, G_out, nullptr, nullptr, ws, ws_bytes,
                  (cudaStream_t)stream);
+}
+
+int snx_class_probabilities(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
+                            int32_t K, const int32_t *labels, const double *w, double *probs_out,
+                            int32_t *pred_out, double *stats_out, void *ws, size_t ws_bytes,
+                            void *stream) {
+  if (w == nullptr || (nrows > 0 && stats_out != nullptr && labels == nullptr)) {
+    set_error("snx_class_probabilities: NULL w (or labels with stats_out)");
+    return 1;
+  }
+  const ProbsOut po{pred_out, stats_out};
+  return rowpass(kProbs, dtype, X, ldx, nrows, p, K, labels, w, nullptr, 0.0, nullptr,
+                 probs_out, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ws,
+                 ws_bytes, (cudaStream_t)stream, nullptr, &po);
 }
 
 int snx_objective_grad_acc(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,

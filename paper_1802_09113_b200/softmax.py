@@ -286,6 +286,62 @@ def hess_vec(prob, x, v):
     return HessianOperator(prob.dataset, x, prob.lam).apply(v)
 
 
+@dataclass
+class RowStats:
+    """Per-row pieces of the stabilised loss (softmax.py:43-56): max_part M_i,
+    sum_exp_part sum_c exp(z_ic - M_i), linear_part z_{i,b_i} (0 for the
+    reference class).  numpy arrays when the weights came as numpy."""
+
+    max_part: object
+    sum_exp_part: object
+    linear_part: object
+
+
+def _probs_pass(ds, x, probs=False, pred=False, stats=False):
+    """One device row pass (snx_class_probabilities / its CSR twin)."""
+    view = _view(ds).materialized()
+    w, as_t = vec_in(x, view.dim)
+    n, C = view.n_rows, view.n_classes
+    dev = w.device
+    P = torch.empty((n, C), dtype=torch.float64, device=dev) if probs else None
+    Y = torch.empty(n, dtype=torch.int32, device=dev) if pred else None
+    S = torch.empty((n, 3), dtype=torch.float64, device=dev) if stats else None
+    if n:
+        if getattr(view, "is_sparse", False):
+            ws = view.workspace(n)
+            _lib.call("snx_csr_class_probabilities", ptr(view.indptr), ptr(view.indices),
+                      ptr(view.data), n, view.n_features, view.K, ptr(view.labels), ptr(w),
+                      ptr(P), ptr(Y), ptr(S), ptr(ws), ws.numel(), stream_handle())
+        elif _wide(view):
+            raise DataError(f"class probabilities are built for C <= 17 on f32 data "
+                            f"(C = {C}); use the fp64 dataset")
+        else:
+            _lib.call("snx_class_probabilities", *_args(view), ptr(view.labels), ptr(w), ptr(P),
+                      ptr(Y), ptr(S), *_ws(view), stream_handle())
+    return P, Y, S, as_t
+
+
+def class_probabilities(ds, x):
+    """softmax.py:224-235: n-by-C probabilities, reference class last."""
+    P, _, _, as_t = _probs_pass(ds, x, probs=True)
+    return vec_out(P, as_t)
+
+
+def predict(ds, x):
+    """softmax.py:238-240: most probable class per row, ties to the lowest index."""
+    _, Y, _, as_t = _probs_pass(ds, x, pred=True)
+    return Y.long() if as_t else vec_out(Y, False).astype(np.int64)
+
+
+def row_stats(ds, x):
+    """softmax.py:107-122: RowStats for every row of ds at weights x."""
+    _, _, S, as_t = _probs_pass(ds, x, stats=True)
+    if as_t:
+        return RowStats(S[:, 0], S[:, 1], S[:, 2])
+    h = vec_out(S, False)
+    return RowStats(h[:, 0].copy(), h[:, 1].copy(), h[:, 2].copy())
+
+
 def correct_count(ds, x):
     """Device count of rows whose most probable class equals the label."""
     view = _view(ds)
@@ -306,5 +362,5 @@ __all__ = [
     "BLOCK_ROWS", "SoftmaxProblem", "zero_weights", "weights_as_matrix", "matrix_as_weights",
     "data_objective", "objective", "data_gradient", "gradient", "HessianOperator", "hess_vec",
     "accuracy", "correct_count", "objective_parts", "gradient_parts", "DeviceDataset",
-    "DeviceView",
+    "DeviceView", "RowStats", "row_stats", "class_probabilities", "predict",
 ]
