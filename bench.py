@@ -392,6 +392,9 @@ def run_ours(args):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl")
+    # the row-sharded code path (NCCL all-reduce per product); SNX_BENCH_SHARDED=1
+    # runs it at world size 1 too (all-reduce = identity) to exercise it on one GPU
+    sharded = world > 1 or os.environ.get("SNX_BENCH_SHARDED") == "1"
 
     A, y = make_problem()
     x_host = 0.01 * np.random.default_rng(7).standard_normal((C - 1) * P)
@@ -400,7 +403,7 @@ def run_ours(args):
     total = args.warmup + args.steps
     samples = snx.SampleConfig(1.0, F_H)
     iters = torch.zeros(total, dtype=torch.float64, device=dev)
-    if world == 1:
+    if not sharded:
         ds = snx.DeviceDataset.from_numpy(A, y, C, dtype=args.dtype)
         prob = snx.SoftmaxProblem(ds, LAM)
         g, _ = softmax.gradient_parts(ds, x, 1.0, LAM)
@@ -472,7 +475,7 @@ def run_ours(args):
     op = ops[0]
     v = g.clone()
     out = torch.empty_like(v)
-    if world > 1:
+    if sharded:
         op = op.op  # the local product (the all-reduce is timed in `value`)
     reps = 50
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -500,14 +503,14 @@ def run_ours(args):
                 "note": "X_S rows re-read from L2 across CG iterations; bytes counted once"}
 
     # ---- e2e: the public numpy API, host buffers in and out
-    if world > 1:
+    if sharded:
         args.skip_solve = True
     g_host = g.cpu().numpy()
     cfg = snx.CgConfig(THETA, T_CG)
     e2e_steps = max(10, min(args.steps, 50))
 
     def e2e_step(k):
-        if world == 1:
+        if not sharded:
             orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, F_H), k)
         else:
             orc = sd.ShardedOracle(sp, snx.SampleConfig(1.0, F_H), k)
@@ -587,7 +590,7 @@ def run_ours(args):
                 # per step: gather + GEMM1 (h prepare), cg_init x2, T x (GEMM1, GEMM2,
                 # cg_step1, cg_step2) [+ snx_finish_hv per product when sharded];
                 # matches profiles/r01_launches.csv (44 per step at N = 1)
-                2 + 2 + T_CG * (4 + (1 if world > 1 else 0))),
+                2 + 2 + T_CG * (4 + (1 if sharded else 0))),
             "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
             "cpu_baseline": cpu, "newton_solve": solve, "other_shapes": shapes,
         }
