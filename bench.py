@@ -500,7 +500,15 @@ def run_ours(args):
                 "kernel": "snx_hess_apply (rowpass GEMM1+ComputeU, xtu GEMM2, finalize)",
                 "peak_kind": pk_kind, "ms_per_launch": hv_ms,
                 "flops_per_launch": 4 * m * P * (C - 1),
-                "note": "X_S rows re-read from L2 across CG iterations; bytes counted once"}
+                "note": "X_S rows re-read from L2 across CG iterations; bytes counted once",
+                # the same launch against the other ceilings it could hit (B200
+                # microbenchmarks in profiles/r01_microbench.txt): X_S read twice
+                # from L2 per product, and the FP64 FMA pipe
+                "alt_bounds": {
+                    "l2_read_gb_s": 2 * m * P * tb / (hv_ms / 1e3) / 1e9,
+                    "l2_read_peak_gb_s": 18037.0,
+                    "fp64_tflops": 4 * m * P * (C - 1) / (hv_ms / 1e3) / 1e12,
+                    "fp64_peak_tflops": 36.0}}
 
     # ---- e2e: the public numpy API, host buffers in and out
     if sharded:
