@@ -343,7 +343,7 @@ __device__ __forceinline__ void segment_sums(const double *base, int64_t seg_str
 // row runs the row algebra; loss / correct counts reduce per row block and,
 // by the CTA that finishes the last row block, over all row blocks (fixed order).
 template <typename T, int K>
-__device__ __noinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, double *zsum,
+__device__ __forceinline__ void block_epilogue(const G1Args &a, int64_t rb, int G, double *zsum,
                                             double *shd, unsigned long long *shu, int *flag,
                                             unsigned epoch) {
   const int tid = threadIdx.x;
@@ -434,7 +434,7 @@ __device__ __forceinline__ void gemm1_body(const G1Args &a, unsigned char *smem,
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;  // more CTAs than items (the host never launches that)
   const int64_t rb0 = i0 / a.nchunks;
-  __shared__ double shd[kWarps];
+  __shared__ double shd[2 * kWarps];
   __shared__ unsigned long long shu[kWarps];
   __shared__ int flag;
   __shared__ long long epi_rb;
@@ -660,8 +660,18 @@ __device__ __forceinline__ void tile_finalize(const G2Args &a, int tile, int G, 
   const int c_lo = sk_owner(a.items, G, (int64_t)tile * a.rchunks);
   const int nseg = sk_owner(a.items, G, (int64_t)(tile + 1) * a.rchunks - 1) - c_lo + 1;
   constexpr int kPer = (K * TCOL + kConsumers - 1) / kConsumers;
+  // the base values first: their loads overlap the segment loads (one L2
+  // round trip for both when nseg <= kBatch)
+  double bv[kPer];
+#pragma unroll
+  for (int q = 0; q < kPer; ++q) {
+    const int e = tid + q * kConsumers;
+    const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
+    bv[q] = (e < K * TCOL && j < a.p) ? __ldcg(a.base + (int64_t)c * a.p + j)  // may be written
+                                      : 0.0;                                  // by other CTAs
+  }
   double acc[kPer];
-  segment_sums<kPer, (kPer <= 4 ? 8 : 4)>(a.gp + (int64_t)tile * a.maxseg * K * TCOL,
+  segment_sums<kPer, (kPer <= 8 ? 8 : 4)>(a.gp + (int64_t)tile * a.maxseg * K * TCOL,
                                           (int64_t)K * TCOL, nseg, tid, kConsumers, K * TCOL,
                                           acc);
   double bo = 0.0, bb = 0.0;
@@ -670,21 +680,33 @@ __device__ __forceinline__ void tile_finalize(const G2Args &a, int tile, int G, 
     const int e = tid + q * kConsumers;
     const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
     if (e < K * TCOL && j < a.p) {
-      const int64_t i = (int64_t)c * a.p + j;
-      const double b = __ldcg(a.base + i);  // may be written by other CTAs (persistent CG)
+      const double b = bv[q];
       const double o = __dadd_rn(__dmul_rn(a.scale, acc[q]), __dmul_rn(a.lam, b));
-      a.out[i] = o;
+      a.out[(int64_t)c * a.p + j] = o;
       bo += b * o;
       bb += b * b;
     }
   }
   if (a.dots == nullptr) return;
-  const double so = consumer_sum(bo, shd);
-  const double sb = consumer_sum(bb, shd);
+  // both curvature partials in one fixed-order block reduction
+  bo = warp_allsum(bo);
+  bb = warp_allsum(bb);
+  if ((tid & 31) == 0) {
+    shd[tid >> 5] = bo;
+    shd[kWarps + (tid >> 5)] = bb;
+  }
+  consumer_sync(kConsumers);
   if (tid == 0) {
+    double so = 0.0, sb = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      so += shd[w];
+      sb += shd[kWarps + w];
+    }
     a.dots[tile] = so;
     a.dots[kDotBlocks + tile] = sb;
   }
+  consumer_sync(kConsumers);
   if (tile == 0)
     for (int t = a.col_tiles + tid; t < kDotBlocks; t += kConsumers) {
       a.dots[t] = 0.0;
@@ -852,7 +874,7 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
   if (i0 == i1) return;
   const int tile0 = (int)(i0 / a.rchunks);
   const int rc0 = (int)(i0 - (int64_t)tile0 * a.rchunks);
-  __shared__ double shd[kWarps];
+  __shared__ double shd[2 * kWarps];
   __shared__ int last_tile;
   __shared__ int fin_tiles[4], nfin;  // tiles this CTA finalized (fused CG tail)
   __shared__ double shx[8];
@@ -1187,7 +1209,7 @@ __global__ void __launch_bounds__(kThreads, 1) cg_solve_kernel(const __grid_cons
   double *red1 = reinterpret_cast<double *>(smem + Sh::RING);
   double *red2 = reinterpret_cast<double *>(smem + Sh::RED2);
   __shared__ uint64_t full1[S1], empty1[S1], full2[S2], empty2[S2];
-  __shared__ double shd[kWarps];
+  __shared__ double shd[2 * kWarps];
   __shared__ CgSlot cur;
   const int tid = threadIdx.x;
   const bool consumer = tid < kConsumers;
