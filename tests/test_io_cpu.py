@@ -7,7 +7,12 @@ import pytest
 
 import paper_1802_09113_b200 as snx
 from conftest import libsvm_cases
-from paper_1802_09113_b200 import io
+from paper_1802_09113_b200 import _build, io
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _built():
+    _build.build()  # the parser lives in libsnx (host code; no GPU needed)
 
 
 def test_libsvm_matches_reference(libsvm_golden):
