@@ -90,6 +90,9 @@ def enqueue_cg(op, g, theta, T, ws):
                   ptr(ws.p), ptr(ws.pb), ptr(ws.state), stream_handle())
 
 
+_EAGER = object()  # marker: graph capture failed, launch eagerly
+
+
 class CgGraph:
     """The whole device CG solve (init + T iterations, ~6T kernels) captured
     once as a CUDA graph for an operator's shared sample buffers; replayed
@@ -121,10 +124,17 @@ class CgGraph:
             # this capture would invalidate it
             gc.collect()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
-                self._enqueue()
-            self.graph = graph
-        self.graph.replay()
+            try:
+                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                    self._enqueue()
+                self.graph = graph
+            except RuntimeError:  # capture unsupported here: same kernels, eager launches
+                torch.cuda.synchronize()
+                self.graph = _EAGER
+        if self.graph is _EAGER:
+            self._enqueue()
+        else:
+            self.graph.replay()
         return self.ws
 
 

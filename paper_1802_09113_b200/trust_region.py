@@ -19,6 +19,7 @@ import numpy as np
 import torch
 
 from . import _lib, softmax
+from .cg import _EAGER
 from .device import (as_device, axpy, cuda_device, dot, download, ptr, stream_handle, vec_in,
                      vec_out)
 from .errors import DataError
@@ -107,10 +108,17 @@ class SteihaugGraph:
             torch.cuda.current_stream().wait_stream(side)
             gc.collect()
             graph = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(graph, capture_error_mode="thread_local"):
-                enqueue_steihaug(self.op, ws, self.theta)
-            self.graph = graph
-        self.graph.replay()
+            try:
+                with torch.cuda.graph(graph, capture_error_mode="thread_local"):
+                    enqueue_steihaug(self.op, ws, self.theta)
+                self.graph = graph
+            except RuntimeError:  # capture unsupported here: same kernels, eager launches
+                torch.cuda.synchronize()
+                self.graph = _EAGER
+        if self.graph is _EAGER:
+            enqueue_steihaug(self.op, ws, self.theta)
+        else:
+            self.graph.replay()
         return ws
 
 
