@@ -93,10 +93,25 @@ class ClockSampler:
 TRAFFIC = {"f64": 61.660672e6 + 0.47232e6 + 61.907456e6 + 0.493312e6}
 
 
-def make_problem(seed=0):
-    import oracle  # synthetic data generator only (the checker's data recipe)
+def synthetic_problem(n, p, nC, seed=0, normalize=True, ill_conditioned=False):
+    """Synthetic data per SURVEY.md 8(d): N(0,1) features (numpy default_rng), columns
+    scaled to unit norm (dataset.py:314-324) or, for the trust-region config, by
+    logspace(2, -4, p) (tests/test_acceptance.py:223-229); uniform labels.  The same
+    recipe as the tests' fixtures, kept here so the measured legs do not import
+    the oracle (which only the CPU-baseline legs run)."""
+    gen = np.random.default_rng(seed)
+    A = gen.standard_normal((n, p))
+    y = gen.integers(0, nC, size=n).astype(np.int64)
+    if ill_conditioned:
+        A *= np.logspace(2, -4, p)
+    elif normalize:
+        norms = np.sqrt((A ** 2).sum(axis=0))
+        A *= np.where(norms > 0, 1.0 / np.where(norms > 0, norms, 1.0), 1.0)
+    return np.ascontiguousarray(A), y
 
-    return oracle.synthetic_problem(N, P, C, seed=seed)
+
+def make_problem(seed=0):
+    return synthetic_problem(N, P, C, seed=seed)
 
 
 def cpu_baseline(A, y, x, steps_budget_s=10.0, max_steps=1000):
@@ -319,7 +334,7 @@ def secondary(snx, torch, args):
 
     out = {}
     for name, n, p, nC in (("mnist", 60000, 784, 10), ("covertype", 581012, 54, 7)):
-        A, y = oracle.synthetic_problem(n, p, nC, seed=0)
+        A, y = synthetic_problem(n, p, nC, seed=0)
         out[name] = shape_rate(snx, torch, A, y, nC, "f64")
         out[name]["workload"] = f"{name}-shape {n}x{p} C={nC}, 5% S_H, fp64"
         del A, y
@@ -362,7 +377,7 @@ def secondary(snx, torch, args):
     out["large_c100_shard_f32"] = res
     torch.cuda.empty_cache()
     # BASELINE config #4: trust region (Steihaug-CG), ill-conditioned CIFAR shape, 10% S_H
-    A, y = oracle.synthetic_problem(N, P, C, seed=0, normalize=False, ill_conditioned=True)
+    A, y = synthetic_problem(N, P, C, seed=0, normalize=False, ill_conditioned=True)
     prob = snx.SoftmaxProblem(snx.DeviceDataset.from_numpy(A, y, C), LAM)
     cfg = snx.TrustRegionConfig(max_outer_iters=20)
     snx.trust_region_solve(prob, snx.TrustRegionConfig(max_outer_iters=2))  # warm-up
