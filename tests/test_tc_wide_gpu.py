@@ -2,6 +2,8 @@
 C = 100 configuration of BASELINE.json): h (the wide GEMM1 with the softmax
 epilogue) and H v against the fp64 oracle, ragged shapes, reruns bitwise."""
 
+import math
+
 import numpy as np
 import pytest
 import torch
@@ -78,3 +80,32 @@ def test_wide_newton_solve_matches_oracle():
     assert len(tr.records) == len(ref_f)
     for a, b in zip(tr.records, ref_f):
         assert abs(a.objective - b) <= 1e-4 * abs(b)
+
+
+def test_config5_shard_properties_full_size():
+    """BASELINE config #5 at its per-GPU size (1M x 3072 f32 rows, C = 100, 5%
+    sample): too large for the oracle, so size-independent properties of the
+    sampled Hessian: symmetry u.Hv = v.Hu, linearity, positive curvature, and
+    bit-identical reruns (fixed-order reductions)."""
+    n, p, C = 1_000_000, 3072, 100
+    K = C - 1
+    g = torch.Generator(device="cuda").manual_seed(5)
+    X = torch.randn((n, p), generator=g, device="cuda", dtype=torch.float32) / math.sqrt(n)
+    lab = torch.randint(0, C, (n,), generator=g, device="cuda", dtype=torch.int32)
+    ds = snx.DeviceDataset(X, lab, C, p, dtype="f32")
+    x = 0.05 * torch.randn(K * p, generator=g, device="cuda", dtype=torch.float64)
+    u = torch.randn(K * p, generator=g, device="cuda", dtype=torch.float64)
+    v = torch.randn(K * p, generator=g, device="cuda", dtype=torch.float64)
+    orc = snx.SubsampledOracle(snx.SoftmaxProblem(ds, 1e-3), snx.SampleConfig(1.0, 0.05), 0)
+    op = orc.hessian_operator(x)
+    Hu, Hv = op.apply(u), op.apply(v)
+    uHv, vHu = float(u @ Hv), float(v @ Hu)
+    assert abs(uHv - vHu) <= 1e-4 * max(abs(uHv), 1e-30)
+    assert float(u @ Hu) > 0 and float(v @ Hv) > 0
+    w = 0.3 * u - 2.0 * v
+    Hw = op.apply(w)
+    lin = 0.3 * Hu - 2.0 * Hv
+    assert float(torch.linalg.vector_norm(Hw - lin) / torch.linalg.vector_norm(lin)) <= 1e-4
+    assert torch.equal(op.apply(u), Hu)
+    del X, ds, op
+    torch.cuda.empty_cache()
