@@ -208,6 +208,9 @@ struct G1Args {
   unsigned *u_ready;   // persistent CG kernel: publish U rows of a row block (epoch)
   int32_t *pred_out;   // kProbs: most probable class per row (nullable)
   double *stats_out;   // kProbs: [M, sum E, linear] per row (nullable)
+  int early_x;         // launched as a programmatic dependent: stage the first X
+                       // tiles before waiting for the previous kernel (X_S is
+                       // older than it; the weights and the skip flag are not)
 };
 
 // Per-row softmax algebra on the summed logits z (softmax.py:85-99 and the
@@ -446,28 +449,65 @@ __device__ __forceinline__ void gemm1_body(const G1Args &a, unsigned char *smem,
       tma_prefetch_desc(&a.xmap);
       tma_prefetch_desc(&a.wmap);
       constexpr unsigned kTx = (unsigned)(Sh::NB * Sh::BOX + Sh::WBYTES);
+      // early_x: the X boxes of the first S items go out before the wait for
+      // the previous kernel (fresh ring: the empty waits pass at once)
+      const int64_t npre = a.early_x ? min((int64_t)S, i1 - i0) : 0;
+      {
+        int64_t rb = rb0;
+        int ch = ch0;
+        for (int64_t j = 0; j < npre; ++j) {
+          const int s = (int)((itp + j) % S);
+          mbar_arrive_expect_tx(&full[s], kTx);
+          unsigned char *st = smem + s * Sh::STAGE;
+          const int col = ch * Sh::CHUNK, row = (int)(rb * kRB);
+#pragma unroll
+          for (int b = 0; b < Sh::NB; ++b)
+            tma_load_2d(st + b * Sh::BOX, &a.xmap, col + b * Sh::BOXC, row, &full[s]);
+          if (++ch == a.nchunks) {
+            ch = 0;
+            ++rb;
+          }
+        }
+      }
+      bool skipped = false;
+      if (a.early_x) {
+        pdl_wait();
+        skipped = a.skip != nullptr && *a.skip != 0.0;
+      }
       int64_t rb = rb0;
       int ch = ch0;
       for (int64_t i = i0; i < i1; ++i, ++itp) {
         const int s = (int)(itp % S);
-        mbar_wait(&empty[s], (unsigned)((itp / S) & 1) ^ 1u);
-        mbar_arrive_expect_tx(&full[s], kTx);
+        const bool pre = i - i0 < npre;
+        if (skipped && !pre) break;
+        if (!pre) {
+          mbar_wait(&empty[s], (unsigned)((itp / S) & 1) ^ 1u);
+          mbar_arrive_expect_tx(&full[s], kTx);
+        }
         unsigned char *st = smem + s * Sh::STAGE;
         const int col = ch * Sh::CHUNK, row = (int)(rb * kRB);
+        if (!pre) {
 #pragma unroll
-        for (int b = 0; b < Sh::NB; ++b)
-          tma_load_2d(st + b * Sh::BOX, &a.xmap, col + b * Sh::BOXC, row, &full[s]);
+          for (int b = 0; b < Sh::NB; ++b)
+            tma_load_2d(st + b * Sh::BOX, &a.xmap, col + b * Sh::BOXC, row, &full[s]);
+        }
         tma_load_2d(st + Sh::NB * Sh::BOX, &a.wmap, col, 0, &full[s]);
         if (++ch == a.nchunks) {
           ch = 0;
           ++rb;
         }
       }
+      if (skipped)  // no consumer will read them: let the staged copies land before exit
+        for (int64_t j = 0; j < npre; ++j) mbar_wait(&full[(int)(j % S)], 0u);
     }
     return;
   }
 
   // -------------------------------------------------- consumer warps
+  if (a.early_x) {  // everything below may depend on the previous kernel
+    pdl_wait();
+    if (a.skip != nullptr && *a.skip != 0.0) return;
+  }
   const int box = warp >> 1;
   const int c0 = (warp & 1) * 4;  // first 16-B chunk of this warp's strip
   const int sw = lane & 7;        // swizzle phase of rows lane, lane+32, lane+64
@@ -602,8 +642,10 @@ __device__ __forceinline__ void gemm1_body(const G1Args &a, unsigned char *smem,
 template <typename T, int K>
 __global__ void __launch_bounds__(kThreads, 1) gemm1_kernel(const __grid_constant__ G1Args a) {
   pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
-  pdl_wait();
-  if (a.skip != nullptr && *a.skip != 0.0) return;
+  if (!a.early_x) {
+    pdl_wait();
+    if (a.skip != nullptr && *a.skip != 0.0) return;
+  }
   using Sh = G1Shape<T, K>;
   constexpr int S = Sh::S;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -898,6 +940,13 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
         if (a.u_ready != nullptr) wait_flag_geq(a.u_ready + c0 / kRB, epoch);
         if (i == i0) pdl_wait();  // no-op unless launched as a programmatic dependent
         bulk_g2s(st + Sh::XB, U + c0 * KP, ub, &full[s]);
+        // the done flag of a captured CG loop is read only after the wait: the
+        // kernel that writes it (cg_step2 / the fused tail) may still be running
+        // when this grid starts (GEMM1 lets its dependents launch early)
+        if (i == i0 && a.skip != nullptr && *a.skip != 0.0) {
+          mbar_wait(&full[s], (unsigned)((itp / S) & 1));  // the staged copy lands first
+          break;
+        }
         if (++rc == a.rchunks) {
           rc = 0;
           ++tile;
@@ -908,6 +957,12 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
   }
 
   // -------------------------------------------------- consumer warps
+  pdl_wait();  // no-op unless launched as a programmatic dependent
+  if (a.skip != nullptr && *a.skip != 0.0) {
+    if (a.cg_state != nullptr && cta == 0 && tid < SNX_CG_SLOT)  // cg_step2 on a done slot
+      slot(a.cg_state, a.cg_t + 1)[tid] = slot(a.cg_state, a.cg_t)[tid];
+    return;
+  }
   T acc[LC][K];
 #pragma unroll
   for (int v = 0; v < LC; ++v)
@@ -1040,14 +1095,10 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
 template <typename T, int K>
 __global__ void __launch_bounds__(kThreads, 1) gemm2_kernel(const __grid_constant__ G2Args a) {
   pdl_trigger();  // all CTAs are resident (one per SM): safe to let the successor queue
-  // launched as a programmatic dependent of GEMM1: everything read here was
-  // complete before GEMM1 started, except the U rows -- the producer waits
-  // for GEMM1 (griddepcontrol.wait) right before its first U load
-  if (a.skip != nullptr && *a.skip != 0.0) {
-    if (a.cg_state != nullptr && blockIdx.x == 0 && threadIdx.x < SNX_CG_SLOT)  // cg_step2 on a done slot
-      slot(a.cg_state, a.cg_t + 1)[threadIdx.x] = slot(a.cg_state, a.cg_t)[threadIdx.x];
-    return;
-  }
+  // launched as a programmatic dependent of GEMM1: X_S is older than both, the
+  // U rows, the done flag and the CG state are not -- the producer waits
+  // (griddepcontrol.wait) right before its first U load, the consumers before
+  // anything else (gemm2_body)
   using Sh = G2Shape<T, K>;
   constexpr int S = Sh::S;
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -1636,11 +1687,22 @@ static int launch_persistent(KernelT kernel, int grid, size_t smem, size_t *conf
   return check_launch(what);
 }
 
+// SNX_G1_PDL=0: GEMM1 of the Hessian product waits for the previous kernel
+// before staging anything (A/B switch for the early X prefetch)
+static bool gemm1_early_x() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SNX_G1_PDL");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 template <typename T, int K>
 static int launch_gemm1(const G1Args &a, int grid, cudaStream_t st) {
   static size_t configured = 0;
   return launch_persistent(gemm1_kernel<T, K>, grid, G1Shape<T, K>::SMEM, &configured, st, a,
-                           "gemm1");
+                           "gemm1", a.early_x != 0);
 }
 
 template <typename T, int K>
@@ -1788,6 +1850,9 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   a.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
   a.loss_out = out;
   a.corr_out = corr_out;
+  // the CG loop's product: X_S is older than the kernel before (cg_step2), the
+  // weights s and the skip flag are its outputs -> stage X early (PDL)
+  a.early_x = (mode == kHessApply && !convert && gemm1_early_x()) ? 1 : 0;
   a.pred_out = po ? po->pred : nullptr;
   a.stats_out = po ? po->stats : nullptr;
   int rc = 1;

@@ -281,7 +281,10 @@ __global__ void __launch_bounds__(kDotThreads)
 __global__ void __launch_bounds__(kDotThreads)
     cg_step2_kernel(int t, int max_iters, int64_t d, const double *__restrict__ r, double *s,
                     const double *__restrict__ p, double *pb, double *state) {
-  pdl_wait();  // successor launches when this grid exits (implicit trigger)
+  // the next product's GEMM1 (a programmatic dependent) may stage its X tiles
+  // while this runs; it waits for this grid before reading s or the done flag
+  pdl_trigger();
+  pdl_wait();
   if (threadIdx.x == 0) SNX_VTL(1, 0);
   const double *st = slot(state, t);
   double *nx = slot(state, t + 1);
