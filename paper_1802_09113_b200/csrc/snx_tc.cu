@@ -111,6 +111,8 @@ struct Tc1Args {
   int64_t row_blocks;
   double *loss_out;
   long long *corr_out;             // nullable
+  int early_x;  // narrow GEMM1 launched as a programmatic dependent of tc_prep_b:
+                // stage the X1 / X2 tiles of the first items before the wait
 };
 
 enum { kTcApply = 0, kTcPrep = 1, kTcObjective = 2, kTcGradient = 3 };
@@ -144,7 +146,7 @@ template <int S> struct BarT {
 using Barriers = BarT<kS>;
 
 template <int S>
-__device__ __forceinline__ void setup(BarT<S> &b, int warp, uint32_t tmem_cols = kTmemCols) {
+__device__ __forceinline__ void setup_barriers(BarT<S> &b) {
   if (threadIdx.x == 0) {
 #pragma unroll
     for (int s = 0; s < S; ++s) {
@@ -158,10 +160,20 @@ __device__ __forceinline__ void setup(BarT<S> &b, int warp, uint32_t tmem_cols =
     }
     mbar_fence_init();
   }
+}
+
+template <int S>
+__device__ __forceinline__ void setup_tmem(BarT<S> &b, int warp, uint32_t tmem_cols) {
   if (warp == 1) umma::tmem_alloc(&b.tbase, tmem_cols);
   umma::fence_before();
   __syncthreads();
   umma::fence_after();
+}
+
+template <int S>
+__device__ __forceinline__ void setup(BarT<S> &b, int warp, uint32_t tmem_cols = kTmemCols) {
+  setup_barriers(b);
+  setup_tmem(b, warp, tmem_cols);
 }
 
 template <int S>
@@ -266,7 +278,7 @@ __device__ __forceinline__ void mma_loop(BarT<S> &b, uint8_t *sm, int64_t i0, in
 template <int K>
 __global__ void __launch_bounds__(kThreads, 1) tc_gemm1_kernel(const __grid_constant__ Tc1Args a) {
   pdl_trigger();  // GEMM2 may become resident on SMs this grid leaves (see tc_gemm2)
-  if (a.skip != nullptr && *a.skip != 0.0) return;
+  if (!a.early_x && a.skip != nullptr && *a.skip != 0.0) return;
   extern __shared__ uint8_t smraw[];
   uint8_t *sm = align1024(smraw);
   __shared__ Barriers b;
@@ -275,8 +287,45 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm1_kernel(const __grid_cons
   const int64_t i0 = sk_begin(a.items, G, cta), i1 = sk_begin(a.items, G, cta + 1);
   if (i0 == i1) return;
   if (tid == 0) SNX_TC_TL(0, 0);
-  setup(b, warp);
   const int nk = a.nk;
+  int64_t npre = 0;
+  if (a.early_x) {
+    // the sample split X1 / X2 is older than tc_prep_b; B (v's split) and the
+    // done flag are its outputs: stage the X tiles of the first kS items, then
+    // wait for it, all before the TMEM allocation (a skipped product exits clean)
+    setup_barriers(b);
+    __syncthreads();
+    npre = min((int64_t)kS, i1 - i0);
+    if (tid == 0) {
+      tma_prefetch_desc(&a.xmap);
+      tma_prefetch_desc(&a.lmap);
+      for (int64_t j = 0; j < npre; ++j) {
+        const int64_t i = i0 + j;
+        const int s = (int)(j % kS);
+        mbar_arrive_expect_tx(&b.full[s], kStage);
+        uint8_t *st = sm + s * kStage;
+        const int rb = (int)(i / nk), kt = (int)(i - (int64_t)rb * nk);
+        tma_load_2d(st, &a.xmap, kt * kKT, rb * 128, &b.full[s]);
+        tma_load_2d(st + kXB, &a.lmap, kt * kKT, rb * 128, &b.full[s]);
+      }
+    }
+    pdl_wait();
+    if (a.skip != nullptr && *a.skip != 0.0) {
+      if (tid == 0) {  // complete the staged transactions, let them land, exit
+        for (int64_t j = 0; j < npre; ++j) {
+          const int64_t i = i0 + j;
+          const int kt = (int)(i - (int64_t)(i / nk) * nk);
+          tma_load_2d(sm + (int)(j % kS) * kStage + 2 * kXB, &a.bmap, kt * kKT, 0,
+                      &b.full[(int)(j % kS)]);
+        }
+        for (int64_t j = 0; j < npre; ++j) mbar_wait(&b.full[(int)(j % kS)], 0u);
+      }
+      return;
+    }
+    setup_tmem(b, warp, kTmemCols);
+  } else {
+    setup(b, warp);
+  }
 
   if (warp == 0) {
     if (lane == 0) {
@@ -285,12 +334,14 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm1_kernel(const __grid_cons
       tma_prefetch_desc(&a.bmap);
       for (int64_t i = i0, it = 0; i < i1; ++i, ++it) {
         const int s = (int)(it % kS);
-        mbar_wait(&b.empty[s], (unsigned)(((it / kS) & 1) ^ 1));
-        mbar_arrive_expect_tx(&b.full[s], kStage);
         uint8_t *st = sm + s * kStage;
         const int rb = (int)(i / nk), kt = (int)(i - (int64_t)rb * nk);
-        tma_load_2d(st, &a.xmap, kt * kKT, rb * 128, &b.full[s]);
-        tma_load_2d(st + kXB, &a.lmap, kt * kKT, rb * 128, &b.full[s]);
+        if (it >= npre) {
+          mbar_wait(&b.empty[s], (unsigned)(((it / kS) & 1) ^ 1));
+          mbar_arrive_expect_tx(&b.full[s], kStage);
+          tma_load_2d(st, &a.xmap, kt * kKT, rb * 128, &b.full[s]);
+          tma_load_2d(st + kXB, &a.lmap, kt * kKT, rb * 128, &b.full[s]);
+        }
         tma_load_2d(st + 2 * kXB, &a.bmap, kt * kKT, 0, &b.full[s]);
       }
     }
@@ -471,6 +522,7 @@ __global__ void __launch_bounds__(kThreads, 1) tc_gemm2_kernel(const __grid_cons
 __global__ void tc_prep_b_kernel(const double *__restrict__ v, int K, int p, int PB, int KP,
                                  __nv_bfloat16 *__restrict__ B,
                                  const double *__restrict__ dir = nullptr, double alpha = 0.0) {
+  pdl_trigger();  // GEMM1 may stage its X tiles meanwhile (it waits before reading B)
   const int64_t n = (int64_t)KP * PB;
   for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -975,6 +1027,16 @@ __global__ void __launch_bounds__(kThreads, 1) tcw_gemm2_kernel(const __grid_con
   teardown(b, warp, W::TMEM);
 }
 
+// SNX_G1_PDL=0: the narrow GEMM1 waits for tc_prep_b before staging anything
+static bool tc_early_x() {
+  static int on = -1;
+  if (on < 0) {
+    const char *e = getenv("SNX_G1_PDL");
+    on = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
+}
+
 // GEMM2 overlaps its prologue and first X tiles with GEMM1's tail through
 // programmatic dependent launch (SNX_TC_PDL=0 disables).
 bool tc_pdl() {
@@ -1013,7 +1075,7 @@ int launch_tc(void (*kernel)(ArgT), int grid, const ArgT &args, cudaStream_t st,
 template <int K>
 int run_tc(const Tc1Args &a1, int g1, const Tc2Args &a2, int g2, cudaStream_t st) {
   static size_t c1 = 0, c2 = 0;
-  if (launch_tc(tc_gemm1_kernel<K>, g1, a1, st, &c1, "tc_gemm1", false)) return 1;
+  if (launch_tc(tc_gemm1_kernel<K>, g1, a1, st, &c1, "tc_gemm1", a1.early_x != 0)) return 1;
   return launch_tc(tc_gemm2_kernel<K>, g2, a2, st, &c2, "tc_gemm2", tc_pdl());
 }
 
@@ -1121,6 +1183,7 @@ static int tc_apply(const void *X1, const void *X2, int64_t ldb, int64_t nrows, 
   a1.zp = reinterpret_cast<double *>(wsb + lay.tc_zp);
   a1.rb_count = counters + 16 + SNX_DOT_BLOCKS;
   a1.skip = skip;
+  a1.early_x = (KP <= 16 && tc_early_x()) ? 1 : 0;  // narrow kernels only
 
   Tc2Args a2{};
   if (make_tmap_bf16(&a2.xmap, X1, PB, nrows, ldb, 64, kKT) ||
