@@ -10,6 +10,7 @@ from .cg import CgConfig, CgReport, cg_solve
 from .data import column_norms, normalize_columns, train_test_split
 from .device import DeviceDataset, DeviceView, as_device
 from .io import load_csv, load_libsvm
+from .sparse import CsrDataset
 from .errors import (CurvatureError, DataError, DimensionError, LineSearchError, ParseError,
                      SubnewtonError)
 from .linesearch import LineSearchConfig, line_search
@@ -37,5 +38,5 @@ __all__ = [
     "SolveTrace", "TrustRegionConfig", "steihaug_cg", "trust_region_solve",
     "estimate_lipschitz", "column_norms", "normalize_columns", "train_test_split",
     "read_trace_csv", "write_trace_csv", "load_libsvm", "load_csv", "RowStats", "row_stats",
-    "class_probabilities", "predict",
+    "class_probabilities", "predict", "CsrDataset",
 ]
