@@ -263,6 +263,17 @@ int snx_csr_class_probabilities(const int64_t *indptr, const int32_t *indices,
                                 const int32_t *labels, const double *w, double *probs_out,
                                 int32_t *pred_out, double *stats_out, void *ws, size_t ws_bytes,
                                 void *stream);
+/* normalize_columns on CSR storage (dataset.py:103-118, 314-324): norms[j] =
+ * sqrt(sum of the column's squared stored values) from the CSC copy (norms
+ * nullable), scale[j] = 1/norms[j] (1 for an empty column); then both copies
+ * scaled: data_out = data * scale[indices], cdata_out = cdata * scale[column]
+ * (col_scratch: nnz int32). */
+int snx_csr_column_norms(const int64_t *colptr, const double *cdata, int32_t p, double *norms,
+                         double *scale, void *stream);
+int snx_csr_scale_columns(const int32_t *indices, const double *data, const int64_t *colptr,
+                          const double *cdata, int64_t nnz, int32_t p, const double *scale,
+                          double *data_out, double *cdata_out, int32_t *col_scratch,
+                          void *stream);
 /* The row sample S (sorted int64, duplicates allowed: sampling with
  * replacement) as its own CSR (s_indptr[m+1], entries in the order of the
  * source rows) and CSC (s_colptr[p+1], rows renumbered to sample positions,

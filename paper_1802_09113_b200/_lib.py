@@ -78,6 +78,9 @@ SIGNATURES = {
     "snx_csr_objective_grad": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i32,
                                         _c_i32, _c_p, _c_p, _c_dbl, _c_dbl, _c_p, _c_p, _c_p,
                                         _c_size, _c_p]),
+    "snx_csr_column_norms": (_c_int, [_c_p, _c_p, _c_i32, _c_p, _c_p, _c_p]),
+    "snx_csr_scale_columns": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_i64, _c_i32, _c_p, _c_p, _c_p,
+                                       _c_p, _c_p]),
     "snx_csr_gather": (_c_int, [_c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_i32, _c_p, _c_i64,
                                 _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_csr_hess_prepare": (_c_int, [_c_p, _c_p, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p,

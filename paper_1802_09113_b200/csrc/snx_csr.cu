@@ -476,6 +476,45 @@ __global__ void __launch_bounds__(kCsrThreads)
   }
 }
 
+// ---------------------------------------------------------------- column scaling
+// normalize_columns on CSR storage (dataset.py:103-107 column_norms: sum of the
+// squared stored values per column; :109-118 scale_columns: data *= scale[col]).
+// Norms come from the CSC copy (one warp per column, lane-strided + butterfly:
+// fixed order); both copies are scaled.
+__global__ void __launch_bounds__(kCsrThreads)
+    csc_colnorm_kernel(const int64_t *__restrict__ colptr, const double *__restrict__ cdata,
+                       int p, double *__restrict__ norms, double *__restrict__ scale) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = blockIdx.x * kCsrWarps + warp; j < p; j += gridDim.x * kCsrWarps) {
+    double acc = 0.0;
+    for (int64_t t = colptr[j] + lane; t < colptr[j + 1]; t += 32) {
+      const double v = cdata[t];
+      acc += v * v;
+    }
+    acc = warp_allsum(acc);
+    if (lane == 0) {
+      const double nj = sqrt(acc);
+      if (norms) norms[j] = nj;
+      scale[j] = nj > 0.0 ? __ddiv_rn(1.0, nj) : 1.0;
+    }
+  }
+}
+
+__global__ void scale_entries_kernel(const int32_t *__restrict__ col_of, const double *__restrict__ in,
+                                     int64_t nnz, const double *__restrict__ scale,
+                                     double *__restrict__ out) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < nnz;
+       t += (int64_t)gridDim.x * blockDim.x)
+    out[t] = __dmul_rn(in[t], scale[col_of[t]]);
+}
+
+__global__ void csc_col_index_kernel(const int64_t *__restrict__ colptr, int p,
+                                     int32_t *__restrict__ col_of) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = blockIdx.x * kCsrWarps + warp; j < p; j += gridDim.x * kCsrWarps)
+    for (int64_t t = colptr[j] + lane; t < colptr[j + 1]; t += 32) col_of[t] = j;
+}
+
 template <typename Fn>
 int dispatch_k(int K, Fn &&fn) {
   switch (K) {
@@ -515,6 +554,28 @@ extern "C" {
 
 size_t snx_csr_workspace_bytes(int64_t nrows, int32_t p, int32_t K) {
   return csr_ws_layout(nrows, p, K, nullptr, nullptr);
+}
+
+int snx_csr_column_norms(const int64_t *colptr, const double *cdata, int32_t p, double *norms,
+                         double *scale, void *stream) {
+  if (p <= 0) return 0;
+  csc_colnorm_kernel<<<148 * 4, kCsrThreads, 0, (cudaStream_t)stream>>>(colptr, cdata, p, norms,
+                                                                       scale);
+  return check_launch("csc_colnorm");
+}
+
+int snx_csr_scale_columns(const int32_t *indices, const double *data, const int64_t *colptr,
+                          const double *cdata, int64_t nnz, int32_t p, const double *scale,
+                          double *data_out, double *cdata_out, int32_t *col_scratch,
+                          void *stream) {
+  if (nnz == 0) return 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  scale_entries_kernel<<<148 * 8, 256, 0, st>>>(indices, data, nnz, scale, data_out);
+  if (check_launch("scale_entries(csr)")) return 1;
+  csc_col_index_kernel<<<148 * 4, kCsrThreads, 0, st>>>(colptr, p, col_scratch);
+  if (check_launch("csc_col_index")) return 1;
+  scale_entries_kernel<<<148 * 8, 256, 0, st>>>(col_scratch, cdata, nnz, scale, cdata_out);
+  return check_launch("scale_entries(csc)");
 }
 
 int snx_csr_objective(const int64_t *indptr, const int32_t *indices, const double *data,

@@ -17,9 +17,20 @@ from .errors import DataError
 from .rng import SPLIT_STREAM, stream_rng
 
 
+def _csr_norms(base):
+    p = base.n_features
+    norms = torch.empty(max(p, 1), dtype=torch.float64, device=base.data.device)
+    scale = torch.empty_like(norms)
+    _lib.call("snx_csr_column_norms", ptr(base.colptr), ptr(base.cdata), p, ptr(norms),
+              ptr(scale), stream_handle())
+    return norms[:p], scale[:p]
+
+
 def column_norms(ds):
     """Device fp64 Euclidean norms of the p feature columns (dataset.py:103-107)."""
     view = as_device(ds)
+    if getattr(view, "is_sparse", False):
+        return _csr_norms(view.materialized())
     base = view.materialized() if isinstance(view, DeviceView) else view
     p = base.n_features
     norms = torch.empty(max(p, 1), dtype=torch.float64, device=base.X.device)
@@ -36,6 +47,19 @@ def normalize_columns(ds):
     are left untouched (dataset.py:314-324).  Returns a new DeviceDataset; the
     input is not modified (inputs are immutable)."""
     view = as_device(ds)
+    if getattr(view, "is_sparse", False):  # CSR: scale the stored values of both copies
+        from .sparse import CsrDataset
+
+        b = view.materialized()
+        _, scale = _csr_norms(b)
+        data, cdata = torch.empty_like(b.data), torch.empty_like(b.cdata)
+        scratch = torch.empty(max(b.nnz, 1), dtype=torch.int32, device=b.data.device)
+        _lib.call("snx_csr_scale_columns", ptr(b.indices), ptr(b.data), ptr(b.colptr),
+                  ptr(b.cdata), b.nnz, b.n_features, ptr(scale), ptr(data), ptr(cdata),
+                  ptr(scratch), stream_handle())
+        return CsrDataset(b.indptr.clone(), b.indices.clone(), data, b.colptr.clone(),
+                          b.rowidx.clone(), cdata, b.labels.clone(), b.n_classes, b.n_features,
+                          b.host_indptr.copy())
     base = view.materialized() if isinstance(view, DeviceView) else view
     _, scale = column_norms(base)
     Y = torch.empty_like(base.X)

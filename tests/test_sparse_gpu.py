@@ -122,3 +122,29 @@ def test_load_libsvm_to_device(libsvm_golden):
         ref = oracle.loss(X, y, C, x, 1e-3)
         assert abs(snx.objective(prob, x) - ref) <= 1e-10 * abs(ref), name
         assert rel_err(snx.gradient(prob, x), oracle.grad(X, y, C, x, 1e-3)) <= 1e-10, name
+
+
+def test_normalize_columns_csr():
+    """normalize_columns on CSR storage (dataset.py:103-118, 314-324): stored
+    values of both copies scaled, an empty column untouched."""
+    rng = np.random.default_rng(12)
+    A = sp.random(700, 90, density=0.05, format="csr", random_state=12,
+                  data_rvs=lambda k: rng.standard_normal(k) * 7.0)
+    A = A.tolil()
+    A[:, 3] = 0.0  # an empty column
+    A = sp.csr_array(A.tocsr())
+    A.eliminate_zeros()
+    y = rng.integers(0, 6, 700)
+    ds = CsrDataset.from_scipy(A, y, 6)
+    norms, _ = snx.column_norms(ds)
+    D = A.toarray()
+    assert rel_err(norms.cpu().numpy(), oracle.column_norms(D)) <= 1e-15
+    nd = snx.normalize_columns(ds)
+    assert isinstance(nd, CsrDataset)
+    Dn = oracle.normalize_columns(D)
+    got = sp.csr_array((nd.data.cpu().numpy(), nd.indices.cpu().numpy(), nd.indptr.cpu().numpy()),
+                       shape=(700, 90)).toarray()
+    assert rel_err(got, Dn) <= 1e-15
+    x = 0.2 * rng.standard_normal(5 * 90)
+    prob = snx.SoftmaxProblem(nd, 1e-3)
+    assert rel_err(snx.gradient(prob, x), oracle.grad(Dn, y, 6, x, 1e-3)) <= 1e-10  # CSC copy too
