@@ -81,7 +81,7 @@ def train_test_split(ds, train_fraction, seed):
     perm = stream_rng(seed, SPLIT_STREAM).permutation(n)
     train_idx = np.sort(perm[:n_train])
     test_idx = np.sort(perm[n_train:])
-    if isinstance(view, DeviceView):  # compose with the parent selection
+    if getattr(view, "rows", None) is not None and view.base is not view:  # a row view
         rows = view.rows.cpu().numpy()
         return view.base.take(rows[train_idx]), view.base.take(rows[test_idx])
     return view.take(train_idx), view.take(test_idx)

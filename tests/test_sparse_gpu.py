@@ -148,3 +148,30 @@ def test_normalize_columns_csr():
     x = 0.2 * rng.standard_normal(5 * 90)
     prob = snx.SoftmaxProblem(nd, 1e-3)
     assert rel_err(snx.gradient(prob, x), oracle.grad(Dn, y, 6, x, 1e-3)) <= 1e-10  # CSC copy too
+
+
+def test_trust_region_and_split_on_csr():
+    rng = np.random.default_rng(14)
+    A = sp.random(1200, 80, density=0.08, format="csr", random_state=14,
+                  data_rvs=lambda k: rng.standard_normal(k))
+    y = rng.integers(0, 4, 1200)
+    ds = CsrDataset.from_scipy(A, y, 4)
+    tr, te = snx.train_test_split(ds, 0.75, 3)
+    tri, tei = oracle.train_test_split(1200, 0.75, 3)
+    x = 0.1 * rng.standard_normal(3 * 80)
+    D = A.toarray()
+    assert abs(snx.objective(snx.SoftmaxProblem(tr, 0.0), x) -
+               oracle.loss(D[tri], y[tri], 4, x, 0.0)) <= 1e-10 * abs(oracle.loss(D[tri], y[tri], 4, x, 0.0))
+    sub_tr, _ = snx.train_test_split(tr, 0.5, 1)  # a split of a view composes the selections
+    a, _ = oracle.train_test_split(len(tri), 0.5, 1)
+    assert abs(snx.objective(snx.SoftmaxProblem(sub_tr, 0.0), x) -
+               oracle.loss(D[tri[a]], y[tri[a]], 4, x, 0.0)) <= 1e-10 * abs(
+                   oracle.loss(D[tri[a]], y[tri[a]], 4, x, 0.0))
+    cfg = oracle.TrustRegionConfig(max_outer_iters=6)
+    ref = oracle.trust_region_solve(D, y, 4, 1e-3, cfg, hessian_fraction=0.1)
+    got = snx.trust_region_solve(snx.SoftmaxProblem(ds, 1e-3),
+                                 snx.TrustRegionConfig(max_outer_iters=6))
+    assert len(got.records) == len(ref["records"])
+    for r, (k, f, acc, _, step, it, rad) in zip(got.records, ref["records"]):
+        assert r.iteration == k and r.cg_iters == it
+        assert abs(r.objective - f) <= 1e-9 * abs(f)
