@@ -90,7 +90,7 @@ class ClockSampler:
 
 # dram__bytes_read.sum + dram__bytes_write.sum of one Hessian product's two GEMM
 # kernels, from the committed ncu --set full capture (per launch, cold cache)
-TRAFFIC = {"f64": 61.660672e6 + 0.47232e6 + 61.907456e6 + 0.493312e6}
+TRAFFIC = {"f64": 61.913088e6 + 0.429568e6 + 61.913344e6 + 0.436992e6}
 
 
 def synthetic_problem(n, p, nC, seed=0, normalize=True, ill_conditioned=False):
