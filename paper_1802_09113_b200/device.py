@@ -282,6 +282,25 @@ def download(*ts):
     return [h.numpy() for h in outs]
 
 
+class AsyncRead:
+    """Device tensors -> numpy without a stream synchronisation: copies into
+    pinned buffers are enqueued now, `wait()` blocks on an event recorded after
+    them (work enqueued later keeps the GPU busy meanwhile)."""
+
+    def __init__(self, *ts):
+        self.bufs = []
+        for t in ts:
+            h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+            h.copy_(t, non_blocking=True)
+            self.bufs.append(h)
+        self.event = torch.cuda.Event()
+        self.event.record()
+
+    def wait(self):
+        self.event.synchronize()
+        return [h.numpy() for h in self.bufs]
+
+
 def vec_in(x, d, what="weight vector"):
     """User vector -> (contiguous fp64 CUDA tensor of length d, caller_used_torch)."""
     if isinstance(x, torch.Tensor):

@@ -25,7 +25,7 @@ import torch
 
 from . import softmax
 from .cg import CgConfig, cg_graph_for, cg_solve, report_from
-from .device import as_device, axpy, cuda_device, dot, download, vec_in, vec_out
+from .device import AsyncRead, as_device, axpy, cuda_device, dot, download, vec_in, vec_out
 from .errors import DataError, LineSearchError
 from .linesearch import LineSearchConfig, line_search
 from .sampling import SampleConfig, SubsampledOracle
@@ -142,16 +142,16 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     with a test set, test accuracy.  x0 may be numpy (x_final is numpy) or a
     CUDA tensor (x_final stays on the device).
 
-    Each outer iteration is enqueued as one speculative pipeline with a single
-    host synchronisation: gradient, ||g||^2, the Hessian sample and the captured
-    CG solve, the slope p.g and the first Armijo trial at x + alpha0 p are all
-    launched before the host reads ||g||, the slope, F(x + alpha0 p) and the CG
-    report together.  With a full gradient sample the first trial is the fused
-    objective + gradient + accuracy pass at x + alpha0 p, so when the Armijo test
-    accepts alpha0 (the usual case) the next iteration's gradient is already
-    computed (bit-identical to recomputing it: same kernel, same point).  The
-    decisions and the trace are the reference's (newton.py:80-104); work done
-    past a stop (||g|| < eps, a failed line search) is discarded.
+    Each outer iteration is enqueued as one pipeline read back with a single
+    wait: gradient, ||g||^2, the Hessian sample and the captured CG solve, the
+    slope p.g and the first Armijo trial at x + alpha0 p (with a full gradient
+    sample the fused objective + gradient + accuracy pass, so an accepted alpha0
+    already yields the next gradient -- bit-identical to recomputing it).  While
+    the host waits for iteration k's scalars, iteration k + 1 is already enqueued
+    speculatively from x + alpha0 p: the GPU never idles through the host's
+    Armijo / bookkeeping step.  When the line search picks another step (or the
+    loop stops) the speculative work is simply discarded.  The decisions and the
+    trace are the reference's (newton.py:80-104).
     """
     ds = as_device(prob.dataset)
     if ds.n_rows == 0:
@@ -165,10 +165,34 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     dev_prob = softmax.SoftmaxProblem(ds, prob.lam)
     lam = prob.lam
     a0 = cfg.ls.alpha0
+    T = cfg.cg.max_iters
 
     def test_acc(w):
         return (float(softmax.correct_count(test, w)) / test.n_rows) if test is not None \
             else math.nan
+
+    def launch(k, oracle, x, g):
+        """Enqueue iteration k at (x, g); nothing is read back yet."""
+        if g is None:
+            g = oracle.gradient_device(x)[0]
+        gg = dot(g, g)
+        hess = oracle.hessian_operator(x)
+        cgws = cg_graph_for(hess, T, cfg.cg.theta).run(g)
+        p = cgws.pb.clone()
+        slope_t = dot(p, g)
+        x_try = axpy(x, a0, p)
+        fused = softmax.gradient_and_correct(ds, x_try, 1.0, lam) \
+            if oracle.gradient_is_full else None
+        if fused is not None:
+            g_try, out_t, corr_t = fused
+        else:
+            g_try = None
+            out_t, corr_t = softmax.objective_parts(ds, x_try, want_correct=True)
+        reads = [gg, slope_t, out_t, corr_t, cgws.slot(T)]
+        if test is not None:
+            reads.append(softmax.correct_count(test, x_try))
+        return {"p": p, "x_try": x_try, "g_try": g_try, "read": AsyncRead(*reads),
+                "cgws": cgws}
 
     t0 = time.perf_counter()
     out, corr = softmax.objective_parts(ds, x, want_correct=True)
@@ -176,57 +200,40 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     f_cur = loss + 0.5 * lam * wsq
     records = [RunRecord(solver_name, 0, 0.0, f_cur, int(corr) / n, test_acc(x), 0.0, 0)]
     reason = "max-iters"
-    g_next = None  # gradient at x carried from the accepted fused trial
-    oracle_next = None
+    cur = launch(0, SubsampledOracle(dev_prob, cfg.samples, 0), x, None) \
+        if cfg.max_outer_iters > 0 else None
     for k in range(cfg.max_outer_iters):
-        oracle = oracle_next if oracle_next is not None else SubsampledOracle(dev_prob,
-                                                                              cfg.samples, k)
-        g = g_next if g_next is not None else oracle.gradient_device(x)[0]
-        g_next = None
-        gg = dot(g, g)
-        hess = oracle.hessian_operator(x)
-        cgws = cg_graph_for(hess, cfg.cg.max_iters, cfg.cg.theta).run(g)
-        p = cgws.pb.clone()
-        slope_t = dot(p, g)
-        x_try = axpy(x, a0, p)
-        # fused first trial: objective + accuracy (+ gradient when S_g is the full set)
-        fused = None
-        if oracle.gradient_is_full:
-            fused = softmax.gradient_and_correct(ds, x_try, 1.0, lam)
-        if fused is not None:
-            g_try, out_t, corr_t = fused
-        else:
-            g_try = None
-            out_t, corr_t = softmax.objective_parts(ds, x_try, want_correct=True)
-        # the next iteration's samples depend only on k: draw them (host numpy) and
-        # upload the index sets while this iteration's kernels run
-        oracle_next = SubsampledOracle(dev_prob, cfg.samples, k + 1) \
-            if k + 1 < cfg.max_outer_iters else None
-        # the one synchronisation of the iteration (pinned async reads)
-        h_gg, h_slope, h_out, h_corr, h_slot = download(gg, slope_t, out_t, corr_t,
-                                                        cgws.slot(cfg.cg.max_iters))
-        vals = [float(h_gg), float(h_slope), float(h_out[0]), float(h_out[1]),
-                int(h_corr[0])] + h_slot.tolist()
-        if math.sqrt(vals[0]) < cfg.epsilon:
+        # speculate: iteration k + 1 from x + alpha0 p, before reading iteration k
+        nxt = None
+        if k + 1 < cfg.max_outer_iters:
+            nxt = launch(k + 1, SubsampledOracle(dev_prob, cfg.samples, k + 1), cur["x_try"],
+                         cur["g_try"])
+        h = cur["read"].wait()
+        h_gg, h_slope, h_out, h_corr, h_slot = h[:5]
+        if math.sqrt(float(h_gg)) < cfg.epsilon:
             reason = "gradient-converged"
             break
-        report = report_from(cgws, cfg.cg.max_iters, True, slot_values=vals[5:])
+        report = report_from(cur["cgws"], T, True, slot_values=h_slot.tolist())
+        p = cur["p"]
         if int(report.iterations) == 0 and report.converged:
             p.zero_()  # cg.py:61-62
-        slope = vals[1]
-        f_try = vals[2] + 0.5 * lam * vals[3]
-        trial = _Trial(ds, lam, x, p, first=(a0, f_try, int(vals[4])))
+        f_try = float(h_out[0]) + 0.5 * lam * float(h_out[1])
+        trial = _Trial(ds, lam, x, p, first=(a0, f_try, int(h_corr[0])))
         try:
-            alpha, _ = line_search(trial, f_cur, slope, cfg.ls)
+            alpha, _ = line_search(trial, f_cur, float(h_slope), cfg.ls)
         except LineSearchError:
             reason = "line-search-failure"
             break
         if alpha == a0:
-            x = x_try  # the same numpy-rounded x + a0 p (snx_axpy)
-            g_next = g_try
+            x = cur["x_try"]  # the same numpy-rounded x + a0 p (snx_axpy)
+            te = float(h[5][0]) / test.n_rows if test is not None else math.nan
+            cur = nxt  # the speculation holds
         else:
             x = axpy(x, alpha, p)
+            te = test_acc(x)
+            cur = launch(k + 1, SubsampledOracle(dev_prob, cfg.samples, k + 1), x, None) \
+                if k + 1 < cfg.max_outer_iters else None
         f_cur, ncorr = trial.seen[alpha]
         records.append(RunRecord(solver_name, k + 1, time.perf_counter() - t0, f_cur,
-                                 ncorr / n, test_acc(x), alpha, report.iterations))
+                                 ncorr / n, te, alpha, report.iterations))
     return SolveTrace(records, vec_out(x, as_t), reason)
