@@ -534,6 +534,9 @@ __global__ void __launch_bounds__(kDotThreads)
 __global__ void __launch_bounds__(kDotThreads)
     tr_step3_kernel(int j, int T, int64_t d, const double *__restrict__ r, double *dv,
                     double *state) {
+  // the next product's GEMM1 (a programmatic dependent) may stage its X tiles
+  // now; it waits for this grid before reading d or the done flag
+  pdl_trigger();
   const double *st = slot(state, j);
   double *nx = slot(state, j + 1);
   if (st[kTrDone] != 0.0) {  // finished earlier: carry the scalars forward
