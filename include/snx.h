@@ -99,8 +99,10 @@ int snx_class_probabilities(int dtype, const void *X, int64_t ldx, int64_t nrows
                             void *stream);
 
 /* softmax.py:181-195 (HessianOperator.__init__) on the sample rows S_H:
- * when rows != NULL the sample is first gathered into Xs_out (ld_out), else
- * X itself is the sample (the f = 1 identity, dataset.py:94-96).
+ * when rows != NULL the sample is X[rows] (gathered into Xs_out (ld_out) when
+ * Xs_out != NULL; with Xs_out == NULL nothing is materialised and the product
+ * is snx_hess_apply_rows -- fp64 data, K <= 9 only), else X itself is the
+ * sample (the f = 1 identity, dataset.py:94-96).
  *   H_out[r*K + c] = h(a_r, x_c) = E_rc / alpha_r, stored in the X dtype. */
 int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows, int64_t nrows,
                      int32_t p, int32_t K, const double *w, void *Xs_out, int64_t ld_out,
@@ -115,6 +117,18 @@ int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
 int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
                    const void *H, const double *v, double scale, double lam, double *Hv_out,
                    double *dots, const double *skip, void *ws, size_t ws_bytes, void *stream);
+
+/* The gather-fused form of snx_hess_apply: the sample is rows[0..nrows) of X
+ * (sorted int64 indices, duplicates allowed), read in place -- no X_S copy.
+ * H comes from snx_hess_prepare(..., rows, ..., Xs_out = NULL, ...), which
+ * fuses the same gather.  fp64 data with K <= 9 (snx_rowpass_fused != 0):
+ * the one-pass cluster kernel (csrc/snx_cluster.cu) streams every sample row
+ * once per product. */
+int snx_rowpass_fused(int dtype, int32_t p, int32_t K);
+int snx_hess_apply_rows(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                        int64_t nrows, int32_t p, int32_t K, const void *H, const double *v,
+                        double scale, double lam, double *Hv_out, double *dots,
+                        const double *skip, void *ws, size_t ws_bytes, void *stream);
 
 /* Tensor-core variant of the two calls above for f32 data (the declared 1e-4
  * path; tcgen05 kind::f16 MMAs on a two-term bf16 split, see csrc/snx_tc.cu).

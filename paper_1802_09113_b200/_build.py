@@ -81,9 +81,10 @@ def build(force=False, verbose=False):
     return LIBPATH
 
 
-def build_timeline(out, extra=()):
-    """Debug variant with per-CTA globaltimer stamps (tools/timeline.py)."""
-    cmd = [_nvcc(), *ARCH, *FLAGS, "-DSNX_TIMELINE", *extra, "-I", INCLUDE, *sources(), "-o", out]
+def build_timeline(out, extra=("-DSNX_TIMELINE",)):
+    """Debug variant with per-CTA globaltimer stamps (tools/timeline.py with
+    -DSNX_TIMELINE, tools/cl_timeline.py with -DSNX_CL_TIMELINE)."""
+    cmd = [_nvcc(), *ARCH, *FLAGS, *extra, "-I", INCLUDE, *sources(), "-o", out]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(proc.stderr)

@@ -18,7 +18,6 @@ numpy and H s uploaded back.
 """
 
 import gc
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -76,15 +75,9 @@ class CgWorkspace:
 def enqueue_cg(op, g, theta, T, ws):
     """Enqueue init + T iterations with a device operator (op.apply_into)."""
     d = ws.d
-    solve = getattr(op, "cg_solve_into", None)
-    if solve is not None and solve(g, theta, T, ws):  # one persistent kernel
-        return
     _lib.call("snx_cg_init", ptr(g), d, float(theta), T, ptr(ws.r), ptr(ws.s), ptr(ws.p),
               ptr(ws.pb), ptr(ws.state), stream_handle())
-    fused = getattr(op, "apply_cg_into", None)
     for t in range(T):
-        if fused is not None and fused(t, T, ws):  # CG update inside the product's tail
-            continue
         op.apply_into(ws.s, ws.Hs, dots=ws.dots, skip=ws.done_ptr(t))
         _lib.call("snx_cg_update", t, T, d, ptr(ws.Hs), ptr(ws.dots), ptr(ws.r), ptr(ws.s),
                   ptr(ws.p), ptr(ws.pb), ptr(ws.state), stream_handle())
@@ -141,8 +134,7 @@ class CgGraph:
 def cg_graph_for(op, T, theta):
     """The CgGraph of op's shared buffers for (T, theta, scale, lam)."""
     hb = op._bufs
-    key = (T, float(theta), op.scale, op.lam, op.dim, os.environ.get("SNX_CG_PERSISTENT", "0"),
-           os.environ.get("SNX_CG_FUSED", "0"))
+    key = (T, float(theta), op.scale, op.lam, op.dim)
     cg = hb.graphs.get(key)
     if cg is None:
         cg = hb.graphs[key] = CgGraph(op, op.dim, T, theta, hb.h.device)

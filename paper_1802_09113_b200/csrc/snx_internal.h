@@ -88,6 +88,17 @@ inline void carveout(F *kernel) {
   prefer_max_smem(reinterpret_cast<const void *>(kernel));
 }
 
+// one-pass fp64 row pass on thread-block clusters (snx_cluster.cu)
+size_t rowpass_counter_bytes();  // the zero-at-rest counter block at workspace offset 0
+bool cluster_supported(int dtype, int32_t p, int32_t K);
+size_t cluster_ws_bytes(int dtype, int64_t nrows, int32_t p, int32_t K);
+int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+                    int32_t p, int32_t K, const int32_t *labels, const double *w,
+                    const double *h, double *hout, double scale, double lam,
+                    const double *base, double *out, double *loss_out, long long *corr_out,
+                    double *dots, const double *skip, int early, void *ws, size_t ws_bytes,
+                    cudaStream_t st);
+
 // vector kernels (snx_vec.cu)
 int launch_prep_weights(int dtype, const double *w, const double *dir, double alpha, int K,
                         int p, int P, void *Wt, double *wsq_partials, unsigned *counter,

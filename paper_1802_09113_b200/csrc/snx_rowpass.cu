@@ -1607,6 +1607,8 @@ static int make_map(CUtensorMap *m, int dtype, const void *base, uint64_t cols, 
                    swizzle ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
+size_t rowpass_counter_bytes() { return (size_t)kCounterWords * 4; }
+
 int sk_maxseg(int64_t items, int grid, int per_group) {
   const int64_t per = items / grid > 0 ? items / grid : 1;
   return (int)((per_group + per - 1) / per + 1);
@@ -1667,7 +1669,10 @@ Workspace workspace_layout(int dtype, int64_t nrows, int32_t p, int32_t K) {
     w.tc_zp = take((size_t)(t.row_blocks > 0 ? t.row_blocks : 1) * t.maxseg1 * 128 * K * 8);
     w.tc_gp = take((size_t)t.col_tiles * t.maxseg2 * K * 128 * 8);
   }
-  w.total = off;
+  // the one-pass cluster row pass (snx_cluster.cu) shares the counter block and
+  // carves its cluster partials out of the same buffer
+  const size_t cl = cluster_ws_bytes(dtype, nrows, p, K);
+  w.total = off > cl ? off : cl;
   return w;
 }
 
@@ -1798,6 +1803,19 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   char *wsb = static_cast<char *>(ws);
   unsigned *counters = reinterpret_cast<unsigned *>(wsb + lay.counters);
   double *dotp = reinterpret_cast<double *>(wsb + lay.dot_part);
+
+  // fp64, K <= 9: the one-pass cluster kernel (X streamed once per product)
+  if (nrows > 0 && cg == nullptr && (mode == kGradient || mode == kHessApply) &&
+      cluster_supported(dtype, p, K)) {
+    if (mode == kGradient && out != nullptr &&
+        launch_prep_weights(dtype, w, nullptr, 0.0, K, p, P, nullptr, dotp, counters + 15,
+                            out + 1, st))
+      return 1;
+    return cluster_rowpass(mode == kHessApply ? 1 : 2, static_cast<const double *>(X), ldx,
+                           nullptr, nrows, p, K, labels, w, static_cast<const double *>(H),
+                           nullptr, scale, lam, base, vec_out, out, corr_out, dots, skip,
+                           (mode == kHessApply && gemm1_early_x()) ? 1 : 0, ws, ws_bytes, st);
+  }
 
   // Weights in the X dtype, padded to P columns (and ||w_eff||^2 for the
   // objective's regulariser).
@@ -2129,6 +2147,17 @@ int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
     return 1;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  if (nrows > 0 && cluster_supported(dtype, p, K)) {
+    // one pass over X[rows]: the row gather is fused into the TMA loads; X_S is
+    // materialised only if the caller asks for it (Xs_out != NULL)
+    if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
+    if (rows != nullptr && Xs_out != nullptr &&
+        gather(dtype, X, ldx, nullptr, rows, nrows, Xs_out, ld_out, nullptr, st))
+      return 1;
+    return cluster_rowpass(0, static_cast<const double *>(X), ldx, rows, nrows, p, K, nullptr, w,
+                           nullptr, static_cast<double *>(H_out), 1.0, 0.0, nullptr, nullptr,
+                           nullptr, nullptr, nullptr, nullptr, 0, ws, ws_bytes, st);
+  }
   const void *Xs = X;
   int64_t lds = ldx;
   if (rows != nullptr) {  // materialise X_S = X[rows] (dataset.py:90-97)
@@ -2187,6 +2216,32 @@ int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_
   return rowpass(kHessApply, dtype, Xs, ldx, nrows, p, K, nullptr, v, nullptr, 0.0, H, nullptr,
                  scale, lam, v, nullptr, nullptr, Hv_out, dots, skip, ws, ws_bytes,
                  (cudaStream_t)stream);
+}
+
+int snx_rowpass_fused(int dtype, int32_t p, int32_t K) {
+  return cluster_supported(dtype, p, K) ? 1 : 0;
+}
+
+int snx_hess_apply_rows(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                        int64_t nrows, int32_t p, int32_t K, const void *H, const double *v,
+                        double scale, double lam, double *Hv_out, double *dots,
+                        const double *skip, void *ws, size_t ws_bytes, void *stream) {
+  if (v == nullptr || Hv_out == nullptr || (nrows > 0 && H == nullptr)) {
+    set_error("snx_hess_apply_rows: NULL v/Hv_out/H");
+    return 1;
+  }
+  if (rows == nullptr || nrows == 0)
+    return snx_hess_apply(dtype, X, ldx, nrows, p, K, H, v, scale, lam, Hv_out, dots, skip, ws,
+                          ws_bytes, stream);
+  if (!cluster_supported(dtype, p, K)) {
+    set_error("snx_hess_apply_rows: fp64 data with K <= 9 only (snx_rowpass_fused)");
+    return 1;
+  }
+  if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
+  return cluster_rowpass(1, static_cast<const double *>(X), ldx, rows, nrows, p, K, nullptr, v,
+                         static_cast<const double *>(H), nullptr, scale, lam, v, Hv_out, nullptr,
+                         nullptr, dots, skip, gemm1_early_x() ? 1 : 0, ws, ws_bytes,
+                         (cudaStream_t)stream);
 }
 
 }  // extern "C"

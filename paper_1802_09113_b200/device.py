@@ -171,18 +171,31 @@ class DeviceDataset:
 
 
 class HessBuffers:
-    """HBM buffers of one sampled Hessian (X_S rows and h probabilities).
+    """HBM buffers of one sampled Hessian (the sample's rows and h probabilities).
 
     Operators of the same dataset and sample size share them, so every outer
     iteration reuses the same addresses and the captured CUDA graph of the CG
     loop (cg.CgGraph) stays valid.  `owner` is the operator whose sample is
-    currently materialised; any other operator re-prepares before use."""
+    currently prepared; any other operator re-prepares before use.
+
+    fp64 data with K <= 9 (`fused`): the kernels read the sample in place
+    through its row indices (a fixed-address copy in `rows`), nothing else is
+    materialised.  Otherwise the rows are gathered into `xs` (and, for f32, the
+    bf16 split X1 + X2 the tensor-core product reads)."""
 
     def __init__(self, base, m, gathered):
         dev = base.X.device
         mm = max(m, 1)
-        self.xs = torch.empty((mm, base.ld), dtype=base.X.dtype, device=dev) if gathered \
-            else base.X
+        self.fused = base.code == _lib.F64 and bool(
+            _lib.load().snx_rowpass_fused(base.code, base.n_features, base.K))
+        self.rows = None
+        self.xs = None
+        if self.fused:
+            if gathered:
+                self.rows = torch.empty(mm, dtype=torch.int64, device=dev)
+        else:
+            self.xs = torch.empty((mm, base.ld), dtype=base.X.dtype, device=dev) if gathered \
+                else base.X
         self.h = torch.empty((mm, base.K), dtype=base.X.dtype, device=dev)
         # f32: bf16 split X1 + X2 of the sample rows for the tensor-core product
         self.xs_tc = None

@@ -16,8 +16,6 @@ contract) or CUDA torch tensors (results stay on the device).
 
 from dataclasses import dataclass
 
-import os
-
 import numpy as np
 import torch
 
@@ -190,10 +188,18 @@ class HessianOperator:
         self._prepare()
 
     def _prepare(self):
-        """Materialise this operator's sample and probabilities in the shared buffers."""
+        """Prepare this operator's sample and probabilities in the shared buffers."""
         view, base, hb = self.view, self.view.base, self._bufs
         if getattr(base, "is_sparse", False):  # CSR data (csrc/snx_csr.cu)
             sparse.hess_prepare(self)
+        elif hb.fused:  # fp64, K <= 9: gather fused into the one-pass kernel
+            rows = None
+            if view.rows is not None:
+                hb.rows[:view.n_rows].copy_(view.rows)  # fixed address: graph replays
+                rows = hb.rows
+            _lib.call("snx_hess_prepare", base.code, ptr(base.X), base.ld, ptr(rows),
+                      view.n_rows, view.n_features, view.K, ptr(self._w), None, base.ld,
+                      ptr(hb.h), *_ws(view), stream_handle())
         elif hb.xs_tc is not None:  # f32: tensor-core product (csrc/snx_tc.cu)
             _lib.call("snx_hess_prepare_tc", ptr(base.X), base.ld, ptr(view.rows), view.n_rows,
                       view.n_features, view.K, ptr(self._w), ptr(hb.xs), base.ld, ptr(hb.h),
@@ -217,7 +223,12 @@ class HessianOperator:
         base, hb = self.view.base, self._bufs
         if getattr(base, "is_sparse", False):
             return sparse.hess_apply(self, v, out, dots, skip)
-        if hb.xs_tc is not None:
+        if hb.fused:
+            rows = hb.rows if self.view.rows is not None else None
+            _lib.call("snx_hess_apply_rows", base.code, ptr(base.X), base.ld, ptr(rows),
+                      self.view.n_rows, self.p, self.view.K, ptr(hb.h), ptr(v), self.scale,
+                      self.lam, ptr(out), ptr(dots), skip, *_ws(self.view), stream_handle())
+        elif hb.xs_tc is not None:
             _lib.call("snx_hess_apply_tc", ptr(hb.xs_tc[0]), ptr(hb.xs_tc[1]), hb.ldb,
                       self.view.n_rows, self.p, self.view.K, ptr(hb.h), ptr(v), self.scale,
                       self.lam, ptr(out), ptr(dots), skip, *_ws(self.view), stream_handle())
@@ -226,47 +237,6 @@ class HessianOperator:
                       self.p, self.view.K, ptr(hb.h), ptr(v), self.scale, self.lam, ptr(out),
                       ptr(dots), skip, *_ws(self.view), stream_handle())
         return out
-
-    def apply_cg_into(self, t, T, ws):
-        """Hs = H s and CG iteration t fused (snx_hess_apply_cg, fp64 data) when
-        SNX_CG_FUSED=1; False -> the caller runs apply_into + snx_cg_update.
-
-        Opt-in: measured slower on B200 (455 vs 423 us per 10-product CIFAR
-        solve) -- the tile finalizers' two waits for every other tile cost more
-        than the two ~1 us kernel boundaries they remove."""
-        hb, view = self._bufs, self.view
-        if (hb.xs_tc is not None or getattr(view.base, "is_sparse", False)
-                or os.environ.get("SNX_CG_FUSED", "0") != "1"):
-            return False
-        if hb.owner is not self:
-            self._prepare()
-        base = view.base
-        _lib.call("snx_hess_apply_cg", base.code, ptr(hb.xs), base.ld, view.n_rows, self.p,
-                  view.K, ptr(hb.h), self.scale, self.lam, t, T, ptr(ws.r), ptr(ws.s),
-                  ptr(ws.p), ptr(ws.pb), ptr(ws.Hs), ptr(ws.dots), ptr(ws.state), *_ws(view),
-                  stream_handle())
-        return True
-
-    def cg_solve_into(self, g, theta, T, ws):
-        """Enqueue the whole CG solve as one persistent kernel (snx_cg_solve,
-        fp64 data) when SNX_CG_PERSISTENT=1; False -> the per-iteration path.
-
-        Opt-in: bit-identical to the per-iteration path, but measured slower
-        on B200 (484 vs 432 us per 10-product CIFAR solve): its three software
-        grid barriers per iteration cost ~2.2 us each, more than the ~1 us
-        kernel boundaries of the captured per-iteration graph."""
-        hb, view = self._bufs, self.view
-        if (hb.xs_tc is not None or view.n_rows == 0 or getattr(view.base, "is_sparse", False)
-                or os.environ.get("SNX_CG_PERSISTENT", "0") != "1"):
-            return False
-        if hb.owner is not self:
-            self._prepare()
-        base = view.base
-        _lib.call("snx_cg_solve", base.code, ptr(hb.xs), base.ld, view.n_rows, self.p, view.K,
-                  ptr(hb.h), self.scale, self.lam, ptr(g), float(theta), T, ptr(ws.r),
-                  ptr(ws.s), ptr(ws.p), ptr(ws.pb), ptr(ws.Hs), ptr(ws.dots), ptr(ws.state),
-                  *_ws(view), stream_handle())
-        return True
 
     def apply(self, v):
         if isinstance(v, torch.Tensor) or np.asarray(v).shape == (self.dim,):

@@ -1,0 +1,71 @@
+"""Per-CTA, per-block timeline of the one-pass cluster kernel (debug build).
+
+    python -c "from paper_1802_09113_b200 import _build; _build.build_timeline('tools/libsnx_cltl.so', ['-DSNX_CL_TIMELINE'])"
+    SNX_LIB=tools/libsnx_cltl.so python tools/cl_timeline.py [cifar|mnist|covertype]
+
+Events per block (consumer thread 0): 0 loop top, 1 row algebra done (after
+waiting for the peers' partial logits), 2 V phase of the next block done,
+3 after the CTA barrier, 4 partials sent, 5 X^T U done; producer: 6 X
+issued, 7 side data issued.  Kernel row (-1): 0 entry, 1 Q loaded, 2 first V
+sent, 3 loop end, 4 epilogue done, 5 exit."""
+import ctypes
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1802_09113_b200 as snx  # noqa: E402
+from paper_1802_09113_b200 import _lib  # noqa: E402
+
+SHAPES = {"cifar": (50000, 3072, 10), "mnist": (60000, 784, 10), "covertype": (581012, 54, 7)}
+name = sys.argv[1] if len(sys.argv) > 1 else "cifar"
+n, p, C = SHAPES[name]
+gen = np.random.default_rng(0)
+A = gen.standard_normal((n, p))
+A /= np.sqrt((A ** 2).sum(axis=0))
+y = gen.integers(0, C, size=n)
+ds = snx.DeviceDataset.from_numpy(A, y, C)
+x = torch.from_numpy(0.01 * np.random.default_rng(7).standard_normal((C - 1) * p)).cuda()
+orc = snx.SubsampledOracle(snx.SoftmaxProblem(ds, 1e-3), snx.SampleConfig(1.0, 0.05), 0)
+g, _ = orc.gradient_device(x)
+op = orc.hessian_operator(x)
+out = torch.empty_like(g)
+for _ in range(5):
+    op.apply_into(g, out)
+torch.cuda.synchronize()
+op.apply_into(g, out)
+torch.cuda.synchronize()
+NB = 26
+buf = (ctypes.c_ulonglong * (160 * NB * 10))()
+_lib.load().snx_debug_cl_timeline(buf)
+t = np.frombuffer(buf, dtype=np.uint64).reshape(160, NB, 10).astype(np.int64)
+used = [c for c in range(160) if t[c, 0, 0] != 0]
+if not used:
+    sys.exit(f'{name}: no stamps (kernel not used for this shape?)')
+t0 = min(t[c, 0, 0] for c in used)
+rel = lambda v: (v - t0) / 1e3 if v else float("nan")  # noqa: E731
+print(f"{name}: {len(used)} CTAs; kernel rows: entry / Q loaded / first V sent / loop end / epi / exit (us)")
+for c in used[:6] + used[-2:]:
+    print(f"cta {c:3d}: " + " ".join(f"{rel(t[c, 0, e]):7.2f}" for e in range(6)))
+print("per block (cta 0): top / rowalg / vphase / sync / vsend / xtu | V in / armed / z summed / rows done")
+for b in range(NB - 1):
+    if t[used[0], b + 1, 0] == 0 or t[used[0], b + 1, 0] < t0:
+        break
+    r = t[used[0], b + 1]
+    print(f"b{b:2d}: " + " ".join(f"{rel(r[e]):7.2f}" for e in range(6)) + " | " +
+          " ".join(f"{rel(r[e]):7.2f}" for e in (6, 8, 7, 9)))
+# medians of the phase durations over CTAs and blocks
+d = {k: [] for k in ("rowalg", "vphase", "sync", "vsend", "xtu")}
+for c in used:
+    for b in range(NB - 1):
+        r = t[c, b + 1]
+        if r[0] == 0 or r[5] == 0:
+            continue
+        d["rowalg"].append(r[1] - r[0])
+        d["vphase"].append(r[2] - r[1])
+        d["sync"].append(r[3] - r[2])
+        d["vsend"].append(r[4] - r[3])
+        d["xtu"].append(r[5] - r[4])
+print("median phase us: " + ", ".join(f"{k} {np.median(v) / 1e3:.3f}" for k, v in d.items() if v))

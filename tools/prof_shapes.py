@@ -1,0 +1,63 @@
+"""Timing driver: fp64 Hessian product / full gradient / captured CG solve /
+prepare at the BASELINE shapes (CUDA events, back-to-back launches).
+
+    python tools/prof_shapes.py [cifar,mnist,covertype] [reps]
+SNX_TWO_PASS=1 selects the two-GEMM kernels (snx_rowpass.cu) for an A/B."""
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1802_09113_b200 as snx  # noqa: E402
+from paper_1802_09113_b200 import cg as cgmod  # noqa: E402
+
+SHAPES = {"cifar": (50000, 3072, 10), "mnist": (60000, 784, 10), "covertype": (581012, 54, 7)}
+
+
+def timed(fn, reps, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps * 1e3
+
+
+def main():
+    names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(SHAPES)
+    reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+    tag = "two-pass" if os.environ.get("SNX_TWO_PASS") else "cluster"
+    for name in names:
+        n, p, C = SHAPES[name]
+        gen = np.random.default_rng(0)
+        A = gen.standard_normal((n, p))
+        A /= np.sqrt((A ** 2).sum(axis=0))
+        y = gen.integers(0, C, size=n)
+        ds = snx.DeviceDataset.from_numpy(A, y, C)
+        prob = snx.SoftmaxProblem(ds, 1e-3)
+        x = torch.from_numpy(0.01 * np.random.default_rng(7).standard_normal((C - 1) * p)).cuda()
+        orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, 0.05), 0)
+        g = orc.gradient_device(x)
+        g = g[0] if isinstance(g, tuple) else g
+        op = orc.hessian_operator(x)
+        out = torch.empty_like(g)
+        hv = timed(lambda: op.apply_into(g, out), reps)
+        gr = timed(lambda: snx.softmax.gradient_parts(ds, x, 1.0, 1e-3), max(5, reps // 10))
+        cgt = timed(lambda: cgmod.cg_graph_for(op, 10, 1e-4).run(g), max(5, reps // 5))
+        prep = timed(lambda: op._prepare(), max(5, reps // 5))
+        m = op.view.n_rows
+        print(f"{tag} {name}: m={m} hess_apply {hv:.1f} us | full grad {gr:.1f} us | "
+              f"cg_solve(10) {cgt:.1f} us | prepare {prep:.1f} us", flush=True)
+        del ds, prob, op, orc
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
