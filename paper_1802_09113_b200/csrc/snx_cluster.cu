@@ -1,4 +1,4 @@
-// One-pass fp64 row pass on thread-block clusters (sm_100a).
+// One-pass fp64 row pass (sm_100a): every row of X streamed ONCE per product.
 //
 // The sampled Hessian product of softmax.py:197-210
 //     V = X_S Q(v),  U = V.h - h.rowsum(V.h),  Hv = scale * X_S^T U + lam * v
@@ -7,32 +7,33 @@
 // have the same shape: a K-wide contraction of every row over all p features,
 // a row-local epilogue, and the transposed product with the SAME rows.  The
 // two-GEMM path (snx_rowpass.cu) streams X twice with a grid-wide dependency
-// between the GEMMs; this kernel streams every row ONCE:
+// between the GEMMs; the kernels here keep a block of rows in shared memory
+// for both products.  The contractions run on the fp64 tensor cores
+// (mma.sync.m8n8k4.f64, classes 0..7; class 8 of C = 10 by DFMA from the same
+// fragments); the row gather of a sample is fused into the TMA bulk copies
+// (one per row slice, through the sample's row indices: no X_S copy).
 //
-//   * a cluster of CS CTAs owns a contiguous range of rows; CTA q of the
-//     cluster owns the column slice [q*wc, (q+1)*wc) of every row.  A row
-//     block of R rows arrives in shared memory by TMA bulk copies (one per
-//     row slice, gathered through the sample's row indices -- the gather is
-//     fused, no X_S copy is materialised);
-//   * consumers compute the slice's partial logits V_q = X[:, slice] Q[slice]
-//     (register tiles, fixed-order in-warp butterflies, fixed-order sum over
-//     warps) and push them into every peer's shared memory with st.async
-//     (distributed shared memory, completion counted on the peer's mbarrier);
-//   * every CTA sums the CS slice partials in rank order -- identical bits on
-//     all peers -- and runs the row algebra (U, or the residual + loss);
-//   * the same shared-memory tile then feeds the transposed product: each
-//     thread owns a few columns x K classes of X^T U in registers for the
-//     whole kernel.  The block after next is already streaming in (3-4 stage
-//     ring), and the peers' partial logits of the NEXT block are computed
-//     before this block's X^T U, so the exchange latency hides behind it;
-//   * at the end each cluster writes its K x p partial; a small finalize
-//     kernel sums the cluster partials in a fixed order, applies scale, lam
-//     and emits the CG dot partials (the SNX_DOT_BLOCKS layout of
-//     snx_hess_apply).
-//
-// Every reduction has a fixed order and there are no float atomics: results
-// are bit-identical run to run.  fp64 only, K <= 9 (the BASELINE shapes:
-// covertype K = 6, MNIST / CIFAR-10 K = 9); other shapes use snx_rowpass.cu.
+// Two shapes of work decomposition:
+//   * column split (cluster_rowpass_kernel, p > 64): a cluster of CS CTAs
+//     owns a contiguous range of rows, CTA q of the cluster the column slice
+//     [q*wc, (q+1)*wc).  Per 8-row block, the 8 compute warps form the slice's
+//     partial logits (k split over the warps); an EXCHANGE warp sums the warp
+//     partials, pushes them into every peer's shared memory with st.async
+//     (distributed shared memory, completion counted on the peer's mbarrier),
+//     waits for the peers' partials, sums them in rank order (identical bits
+//     on every peer) and runs the row algebra -- all off the compute warps'
+//     critical path: they meanwhile compute the NEXT block's logits.  The
+//     transposed product then reuses the block's tile; each compute warp owns
+//     8-column tiles of X^T U in registers for the whole kernel;
+//   * row split (rowsplit_kernel, p <= 64, covertype): each warp owns 8 rows
+//     of a 64-row block completely, the row algebra runs in its registers, no
+//     block-level synchronisation at all.
+// Each cluster / CTA writes a K x p partial; a finalize kernel sums them in a
+// fixed order, applies scale and lam and emits the CG dot partials (the
+// SNX_DOT_BLOCKS layout of snx_hess_apply).  Every reduction has a fixed order
+// and there are no float atomics: results are bit-identical run to run.
+// fp64, K <= 9 (the BASELINE shapes: covertype K = 6, MNIST / CIFAR-10 K = 9);
+// other shapes use snx_rowpass.cu.
 #include <stdio.h>
 
 #include "snx_common.cuh"
@@ -44,56 +45,33 @@ namespace clp {
 
 enum Mode { kPrep = 0, kApply = 1, kGrad = 2 };
 
-constexpr int kNW = 8;               // consumer warps
-constexpr int kNC = kNW * 32;        // consumer threads
-constexpr int kNT = kNC + 32;        // + one producer warp
+constexpr int kNW = 12;            // compute warps (3 per SM sub-partition)
+constexpr int kNC = kNW * 32;      // compute threads
+constexpr int kNTA = kNC + 96;     // column split: + producer + send warp + row-algebra warp
+constexpr int kNTR = kNC + 32;     // row split: + producer warp
 constexpr int kMaxK = 9;
-
-// Thread-work shapes.
-//  V phase (partial logits): lane = (row group rg < RGL, k-slice ksl < KSL);
-//    a thread owns RT rows (rt*RGL + rg) x K classes over the column pairs
-//    2*(i*KS + kslice), i < npi; the KSL lanes of a row group read one 16-B
-//    pair each (a contiguous 16*KSL-byte run: no bank conflicts) and share the
-//    weight pairs (smem broadcasts).
-//  X^T U phase: thread t owns CPT consecutive columns of NCI chunks strided by
-//    NCOLT*CPT, x K classes, over the rows r = rsub (mod RS); U rows are smem
-//    broadcasts.
-template <int RGL_, int RT_, int NCOLT_, int CPT_, int NCI_, bool DM_ = false, int NMT_ = 1>
-struct Cfg {
-  static constexpr int RGL = RGL_, RT = RT_, NCOLT = NCOLT_, CPT = CPT_, NCI = NCI_;
-  static constexpr bool DM = DM_;   // fp64 tensor-core MMAs (m8n8k4) for classes 0..7
-  static constexpr int NMT = NMT_;  // DM: X^T U column tiles (8 wide) per warp
-  static constexpr int R = RGL * RT;      // rows per block
-  static constexpr int KSL = 32 / RGL;    // k-slices per warp
-  static constexpr int KS = kNW * KSL;    // k-slices per CTA
-  static constexpr int RS = kNC / NCOLT;  // row subsets of X^T U
-  static constexpr int LV = KSL == 1 ? 0 : KSL == 2 ? 1 : KSL == 4 ? 2 : KSL == 8 ? 3 : 4;
-  static constexpr int LR = RT == 1 ? 0 : RT == 2 ? 1 : RT == 4 ? 2 : 3;
-  static constexpr int LS = LV < LR ? LV : LR;  // reduce-scatter levels
-};
-// CfgA (DM): 8-row blocks, 16-column chunks; V = X Q on mma.m8n8k4.f64 (rows x
-//   classes 0..7 per warp, k split over the warps), class 8 by DFMA from the
-//   same fragments; X^T U on m8n8k4 with 8-column tiles owned by warps.
-using CfgA = Cfg<4, 2, 256, 1, 3, true, 12>;  // column slices of 65..768
-using CfgB = Cfg<16, 4, 16, 4, 1>;   // column slices of <= 64 (64-row blocks)
+constexpr int kRA = 8;             // rows per block, column split
+constexpr int kRR = 8 * kNW;       // rows per block, row split (8 per warp)
+constexpr int kNMT = 8;            // column split: X^T U tiles (8 columns) per warp -> wc <= 768
+constexpr int kUP = 10;            // U row stride: classes 0..8 + pad (bank spread)
+constexpr int kNCH = 4;            // V phase: 16-column chunks per warp (wc <= 768, p <= 64)
 
 struct Args {
   const double *X;
   int64_t ldx;
   const int64_t *rows;    // nullable: sample position -> source row
   int64_t nrows;
-  int p, K, cs, ncl, wc, npi, S, WS, WQ;
+  int p, K, cs, ncl, wc, S, WS, WQ;
   int mode;
   const double *w;        // [K][p] class-major weights (v for the Hessian product)
   const double *h;        // apply: [nrows][K] probabilities
   const int32_t *labels;  // grad: labels of the (source) rows
   double *hout;           // prep: [nrows][K]
-  double *gp;             // [ncl][K*p] cluster partials of X^T U
+  double *gp;             // [ncl][K*p] partials of X^T U
   double *lossp;          // grad: [ncl]
   unsigned long long *corrp;  // grad: [ncl]
   const double *skip;
   int early;              // programmatic dependent: stage rows before waiting
-  int qbulk;              // weight slices are 16-B aligned: TMA bulk copies
   // shared-memory carve-up (byte offsets)
   int o_tiles, o_q, o_side, o_u, o_vr, o_red, o_bar;
 };
@@ -140,13 +118,16 @@ __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, unsigned parity) {
+// spin on a phase (test_wait polls: a thread parked in try_wait is not woken
+// promptly by remote complete-tx).  The phase completes only once the peers'
+// st.async bytes have landed in this CTA's shared memory.
+__device__ __forceinline__ void mbar_poll(uint64_t *bar, unsigned parity) {
   asm volatile(
       "{\n"
       ".reg .pred p;\n"
-      "WAITC_%=:\n"
+      "WAITP_%=:\n"
       "mbarrier.test_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAITC_%=;\n"
+      "@!p bra WAITP_%=;\n"
       "}\n" ::"r"(smem_u32(bar)),
       "r"(parity)
       : "memory");
@@ -160,42 +141,55 @@ __device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// half-warp (16-lane) butterflies: fixed order, identical bits on every lane
-__device__ __forceinline__ double hsum(double v) {
+// xor butterflies over lane groups of width W (fixed order: identical bits on
+// every lane of a group)
+template <int W>
+__device__ __forceinline__ double gsum(double v) {
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  for (int o = W / 2; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
-__device__ __forceinline__ double hmax_nan(double v) {  // NaN wins (np.max propagates it)
+__device__ __forceinline__ double max_nan(double v, double u) {  // NaN wins (np.max)
+  return isnan(v) ? v : (isnan(u) ? u : (u > v ? u : v));
+}
+template <int W>
+__device__ __forceinline__ double gmax_nan(double v) {
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {
-    const double u = __shfl_xor_sync(0xffffffffu, v, o);
-    v = isnan(v) ? v : (isnan(u) ? u : (u > v ? u : v));
-  }
+  for (int o = W / 2; o > 0; o >>= 1) v = max_nan(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
 // argmax with numpy's rules: the first NaN, else the largest, ties -> lowest index
-__device__ __forceinline__ int hargmax(double v, int idx) {
+__device__ __forceinline__ void amax_take(double &v, int &idx, double u, int j) {
+  const bool vn = isnan(v), un = isnan(u);
+  const bool take = (vn || un) ? (un && (!vn || j < idx)) : (u > v || (u == v && j < idx));
+  if (take) {
+    v = u;
+    idx = j;
+  }
+}
+template <int W>
+__device__ __forceinline__ void gargmax(double &v, int &idx) {
 #pragma unroll
-  for (int o = 8; o > 0; o >>= 1) {
+  for (int o = W / 2; o > 0; o >>= 1) {
     const double u = __shfl_xor_sync(0xffffffffu, v, o);
     const int j = __shfl_xor_sync(0xffffffffu, idx, o);
-    const bool vn = isnan(v), un = isnan(u);
-    bool take;
-    if (vn || un)
-      take = un && (!vn || j < idx);
-    else
-      take = u > v || (u == v && j < idx);
-    if (take) {
-      v = u;
-      idx = j;
-    }
+    amax_take(v, idx, u, j);
   }
-  return idx;
 }
 
-// Optional per-CTA timeline (-DSNX_CL_TIMELINE; tools/cl_timeline.py): warp
-// 0 lane 0 and the producer stamp %globaltimer at fixed events per block.
+// pairwise (fixed-order) tree over v[B..E): short dependent chains
+template <int B, int E, int N>
+__device__ __forceinline__ double tree_sum(const double (&v)[N]) {
+  if constexpr (E - B == 1) {
+    return v[B];
+  } else {
+    constexpr int M = B + (E - B) / 2;
+    return tree_sum<B, M>(v) + tree_sum<M, E>(v);
+  }
+}
+
+// Optional per-CTA timeline (-DSNX_CL_TIMELINE; tools/cl_timeline.py): compute
+// thread 0 and exchange-warp lane 0 stamp %globaltimer at fixed events.
 #ifdef SNX_CL_TIMELINE
 constexpr int kTlBlocks = 24;
 __device__ unsigned long long g_cl_tl[160][kTlBlocks + 2][10];
@@ -208,48 +202,223 @@ __device__ __forceinline__ void cl_stamp(int b, int ev) {
   do {                                        \
     if (threadIdx.x == 0) cl_stamp((b), (ev)); \
   } while (0)
-#define CL_TLP(b, ev)                          \
-  do {                                         \
-    if (threadIdx.x == kNC) cl_stamp((b), (ev)); \
+#define CL_TLX(b, ev)                                                  \
+  do {                                                                 \
+    if (threadIdx.x == kNC + 32 || threadIdx.x == kNC + 64) cl_stamp((b), (ev)); \
   } while (0)
 #else
 #define CL_TL(b, ev) \
   do {               \
   } while (0)
-#define CL_TLP(b, ev) \
+#define CL_TLX(b, ev) \
   do {                \
   } while (0)
 #endif
 
-// ---------------------------------------------------------------- kernel
-template <int K, typename C>
-__global__ void __launch_bounds__(kNT, 1) cluster_rowpass_kernel(const __grid_constant__ Args a) {
-  constexpr int R = C::R, RT = C::RT, RGL = C::RGL, KSL = C::KSL, KS = C::KS;
-  // U row stride: 16-B multiple; DM: classes 0..8 + pad (10 doubles) so the
-  // X^T U B fragments (U[2t+s][g]) hit each bank at most twice
-  constexpr int KP = C::DM ? 10 : K + (K & 1);
-  constexpr int KQ = C::DM ? (K > 8 ? K : 8) : K;  // weight rows (DM: classes >= K zero)
+// ---------------------------------------------------------------- shared pieces
+struct Ring {
+  double *tiles, *Qs, *side;
+  uint64_t *full, *empty;
+};
+
+// Producer warp: row indices prefetched one block ahead; X slices by TMA bulk
+// copies (one per row); side data (h rows / labels) by cp.async; each lane
+// arrives on the stage's full barrier once its copies have landed.  With
+// `early` the first stages' X copies go out before the predecessor grid has
+// finished (X and the row indices are older than it); everything the
+// predecessor may write (weights, h, labels, the skip flag) waits.
+template <int R, int K>
+__device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t row_lo,
+                                        int64_t row_hi, int nb, int c0, int wq, int lane,
+                                        int *sh_skip) {
+  const int S = a.S, WS = a.WS, WQ = a.WQ;
+  const bool apply = a.mode == kApply, grad = a.mode == kGrad;
+  constexpr int IPL = (R + 31) / 32;
+  auto load_idx = [&](int b, int64_t(&dst)[IPL]) {
+    const int64_t r0 = row_lo + (int64_t)b * R;
+    const int nr = (int)min((int64_t)R, row_hi - r0);
+#pragma unroll
+    for (int j = 0; j < IPL; ++j) {
+      const int e = lane + 32 * j;
+      dst[j] = e < nr ? (a.rows ? a.rows[r0 + e] : r0 + e) : 0;
+    }
+  };
+  auto issue_x = [&](int b, const int64_t(&idx)[IPL]) {
+    const int s = b % S;
+    if (b >= S) mbar_wait(&rg.empty[s], ((b / S) - 1) & 1);
+    const int64_t r0 = row_lo + (int64_t)b * R;
+    const int nr = (int)min((int64_t)R, row_hi - r0);
+    double *tile = rg.tiles + (size_t)s * R * WS;
+    const unsigned bytes = (unsigned)wq * 8u;
+    if (lane == 0) mbar_expect_tx(&rg.full[s], bytes * (unsigned)nr);
+    if (bytes > 0) {
+#pragma unroll
+      for (int j = 0; j < IPL; ++j) {
+        const int e = lane + 32 * j;
+        if (e < nr) bulk_g2s(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s]);
+      }
+    }
+  };
+  auto issue_side = [&](int b, const int64_t(&idx)[IPL]) {
+    const int s = b % S;
+    const int64_t r0 = row_lo + (int64_t)b * R;
+    const int nr = (int)min((int64_t)R, row_hi - r0);
+    if (apply) {
+      double *hs = rg.side + (size_t)s * R * K;
+      for (int e = lane; e < nr * K; e += 32) cp_async8(hs + e, a.h + r0 * K + e);
+    } else if (grad) {
+      int *ls = reinterpret_cast<int *>(rg.side) + s * R;
+#pragma unroll
+      for (int j = 0; j < IPL; ++j) {
+        const int e = lane + 32 * j;
+        if (e < nr) cp_async4(ls + e, a.labels + idx[j]);
+      }
+    }
+    cp_async_mbar_arrive(&rg.full[s]);
+  };
+  int64_t idx[2][IPL];
+  int b = 0;
+  if (nb > 0) load_idx(0, idx[0]);
+  if (a.early) {
+    for (; b < nb && b < S; ++b) {
+      if (b + 1 < nb) load_idx(b + 1, idx[(b + 1) & 1]);
+      issue_x(b, idx[b & 1]);
+    }
+  }
+  pdl_wait();
+  if (lane == 0) *sh_skip = (a.skip != nullptr && *a.skip != 0.0) ? 1 : 0;
+  __syncwarp();
+  if (*sh_skip) {  // complete the staged phases (no copy left in flight), then leave
+    for (int bb = 0; bb < b; ++bb) {
+      mbar_arrive(&rg.full[bb % S]);
+      mbar_wait(&rg.full[bb % S], (bb / S) & 1);
+    }
+    return;
+  }
+  for (int bb = 0; bb < b; ++bb) issue_side(bb, idx[bb & 1]);
+  for (; b < nb; ++b) {
+    if (b + 1 < nb) load_idx(b + 1, idx[(b + 1) & 1]);
+    issue_x(b, idx[b & 1]);
+    issue_side(b, idx[b & 1]);
+  }
+}
+
+// The weights stay in registers for the whole kernel: a warp's V chunks are
+// fixed (ch = ch0 + step i), so lane (g, t) keeps the B fragments
+// w[g][16 ch + 4 t + s] (s = 0..3) of its NCH chunks (zero past the slice, past
+// p, or for classes >= K).  Class 8 (K = 9) is a shared-memory row (smem
+// broadcasts: the four lanes of a group read one 16-B pair).
+template <int K>
+__device__ __forceinline__ void load_qfrag(const Args &a, int c0, int wq, int g, int t, int ch0,
+                                           int step, int nch, double (&qf)[kNCH][4]) {
+#pragma unroll
+  for (int i = 0; i < kNCH; ++i) {
+    const int ch = ch0 + step * i;
+#pragma unroll
+    for (int s = 0; s < 4; ++s) {
+      const int j = 16 * ch + 4 * t + s, gc = c0 + j;
+      qf[i][s] = (ch < nch && g < K && j < wq && gc < a.p) ? a.w[(int64_t)g * a.p + gc] : 0.0;
+    }
+  }
+}
+template <int K>
+__device__ __forceinline__ void load_q8(const Args &a, double *q8, int c0, int wq, int n,
+                                        int tid, int nthreads) {
+  if constexpr (K == 9)
+    for (int j = tid; j < n; j += nthreads)
+      q8[j] = (j < wq && c0 + j < a.p) ? a.w[(int64_t)8 * a.p + c0 + j] : 0.0;
+}
+
+// V phase of one 8-row group: C = X[8 rows][chunks] Q^T on m8n8k4, the 16
+// columns of chunk ch at physical column 16 ch + 4 t + s for step s (so a
+// lane's A and B values are 2 contiguous 16-B loads each).  Returns the lane's
+// C = (V[g][2t], V[g][2t+1]) and v8 = the row's class-8 logit partial (summed
+// over the 4 lanes of the group, K == 9).
+template <int K>
+__device__ __forceinline__ void vgroup(const double *xrow, const double *q8row,
+                                       const double (&qf)[kNCH][4], int ch0, int step, int nch,
+                                       double (&c2)[2], double &v8) {
+  // two independent accumulator chains (steps 0,1 and 2,3), added at the end
+  double ca[2] = {0.0, 0.0}, cb[2] = {0.0, 0.0}, va = 0.0, vb = 0.0;
+#pragma unroll
+  for (int i = 0; i < kNCH; ++i) {
+    const int ch = ch0 + step * i;
+    if (ch < nch) {
+      const double2 xa = *reinterpret_cast<const double2 *>(xrow + 16 * ch);
+      const double2 xb = *reinterpret_cast<const double2 *>(xrow + 16 * ch + 2);
+      dmma(ca, xa.x, qf[i][0]);
+      dmma(cb, xb.x, qf[i][2]);
+      dmma(ca, xa.y, qf[i][1]);
+      dmma(cb, xb.y, qf[i][3]);
+      if constexpr (K == 9) {
+        const double2 ra = *reinterpret_cast<const double2 *>(q8row + 16 * ch);
+        const double2 rb = *reinterpret_cast<const double2 *>(q8row + 16 * ch + 2);
+        va = fma(xa.x, ra.x, va);
+        vb = fma(xb.x, rb.x, vb);
+        va = fma(xa.y, ra.y, va);
+        vb = fma(xb.y, rb.y, vb);
+      }
+    }
+  }
+  c2[0] = ca[0] + cb[0];
+  c2[1] = ca[1] + cb[1];
+  v8 = 0.0;
+  if constexpr (K == 9) v8 = gsum<4>(va + vb);
+}
+
+// X^T U of one 8-row group into the warp's column tiles: tile m covers
+// columns 8 (m0 + mstep m) .. +7; rows of step s, lane t: 2t + s (each bank
+// hit by two of the four rows).  u points at the group's U rows (stride kUP).
+template <int K, int NMT>
+__device__ __forceinline__ void xgroup(const double *x0, int WS, const double *u, int nr, int g,
+                                       int t, int m0, int mstep, int nmt, double (&acc)[NMT][2],
+                                       double (&acc8)[NMT]) {
+  const double ua0 = u[(2 * t) * kUP + g], ua1 = u[(2 * t + 1) * kUP + g];
+  const double u80 = K == 9 ? u[(2 * t) * kUP + 8] : 0.0;
+  const double u81 = K == 9 ? u[(2 * t + 1) * kUP + 8] : 0.0;
+  const bool ok0 = 2 * t < nr, ok1 = 2 * t + 1 < nr;
+  const double *xa = x0 + (size_t)(2 * t) * WS + g;
+  const double *xb = xa + WS;
+#pragma unroll
+  for (int m = 0; m < NMT; ++m) {
+    const int mt = m0 + mstep * m;
+    if (mt < nmt) {
+      const double a0 = ok0 ? xa[8 * mt] : 0.0;
+      const double a1 = ok1 ? xb[8 * mt] : 0.0;
+      dmma(acc[m], a0, ua0);
+      dmma(acc[m], a1, ua1);
+      if constexpr (K == 9) {
+        acc8[m] = fma(a0, u80, acc8[m]);
+        acc8[m] = fma(a1, u81, acc8[m]);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- column split
+template <int K>
+__global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_constant__ Args a) {
+  constexpr int R = kRA;
   pdl_trigger();  // the finalize kernel may launch now (it waits for this grid)
   extern __shared__ __align__(1024) unsigned char smem[];
-  double *tiles = reinterpret_cast<double *>(smem + a.o_tiles);  // [S][R][WS]
-  double *Qs = reinterpret_cast<double *>(smem + a.o_q);         // [K][WQ]
-  double *side = reinterpret_cast<double *>(smem + a.o_side);    // [S][R][K] h | [S][R] int
-  double *Us = reinterpret_cast<double *>(smem + a.o_u);         // [2][R][KP]
-  double *Vr = reinterpret_cast<double *>(smem + a.o_vr);        // [2][cs][R][K]
-  double *red = reinterpret_cast<double *>(smem + a.o_red);      // [2][NW][R][K]
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + a.o_bar);
-  uint64_t *empty = full + a.S;
-  uint64_t *vfull = empty + a.S;  // [2]
-  uint64_t *qbar = vfull + 2;
-  __shared__ double sh_loss[kNW];
-  __shared__ unsigned long long sh_corr[kNW];
+  Ring rg;
+  rg.tiles = reinterpret_cast<double *>(smem + a.o_tiles);          // [S][R][WS]
+  rg.side = reinterpret_cast<double *>(smem + a.o_side);            // [S][R][K] h | [S][R] int
+  double *Q8 = reinterpret_cast<double *>(smem + a.o_q);            // [WQ] class-8 weights
+  double *Us = reinterpret_cast<double *>(smem + a.o_u);            // [2][R][kUP]
+  double *Vr = reinterpret_cast<double *>(smem + a.o_vr);           // [2][cs][R][K]
+  double *red = reinterpret_cast<double *>(smem + a.o_red);         // [2][NW][R][K]
+  rg.full = reinterpret_cast<uint64_t *>(smem + a.o_bar);
+  rg.empty = rg.full + a.S;
+  uint64_t *vfull = rg.empty + a.S;  // [2] peers' partial logits landed
+  uint64_t *redfull = vfull + 2;     // [2] compute warps' partials written
+  uint64_t *ufull = redfull + 2;     // [2] U rows ready
   __shared__ int sh_skip;
 
-  // the warp index through a shuffle: provably warp-uniform for the compiler,
-  // so shuffles under warp-indexed loops need no divergent-collective lowering
+  // the warp index through a shuffle: provably warp-uniform for the compiler
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int S = a.S, WS = a.WS, WQ = a.WQ, cs = a.cs;
+  const int S = a.S, WS = a.WS, cs = a.cs;
   CL_TL(-1, 0);
   const unsigned q = cluster_rank();
   const int cl = (int)cluster_id();
@@ -257,22 +426,25 @@ __global__ void __launch_bounds__(kNT, 1) cluster_rowpass_kernel(const __grid_co
   const int nb = (int)((row_hi - row_lo + R - 1) / R);
   const int c0 = (int)q * a.wc;                                 // first column of the slice
   const int wq = max(0, min(a.wc, ((a.p + 3) & ~3) - c0));      // slice width (even)
-  const bool apply = a.mode == kApply, grad = a.mode == kGrad;
+  const bool apply = a.mode == kApply, grad = a.mode == kGrad, prep = a.mode == kPrep;
 
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], kNW);
+      mbar_init(&rg.full[s], 32);
+      mbar_init(&rg.empty[s], kNW);
     }
     mbar_init(&vfull[0], 1);
     mbar_init(&vfull[1], 1);
-    mbar_init(qbar, 1);
+    mbar_init(&redfull[0], kNW);
+    mbar_init(&redfull[1], kNW);
+    mbar_init(&ufull[0], 32);
+    mbar_init(&ufull[1], 32);
     mbar_fence_init();
   }
-  // zero the tile columns no bulk copy writes (the V phase streams zero pairs there)
-  for (int i = tid; i < S * R * (WS - wq); i += kNT) {
+  // zero the tile columns no bulk copy writes (the chunks / tiles read them)
+  for (int i = tid; i < S * R * (WS - wq); i += kNTA) {
     const int r = i / (WS - wq), j = i - r * (WS - wq);
-    tiles[(size_t)r * WS + wq + j] = 0.0;
+    rg.tiles[(size_t)r * WS + wq + j] = 0.0;
   }
   __syncthreads();
   if (tid == 0 && nb > 0) {
@@ -281,489 +453,221 @@ __global__ void __launch_bounds__(kNT, 1) cluster_rowpass_kernel(const __grid_co
   }
   cluster_sync_all();  // peers' barriers initialised before any st.async
 
-  // ------------------------------------------------------------ producer warp
-  if (warp == kNW) {
-    constexpr int IPL = (R + 31) / 32;  // row indices per lane and block
-    // source rows of block b (the next block's are loaded one block ahead, so
-    // their latency hides behind the current block's issue)
-    auto load_idx = [&](int b, int64_t(&dst)[IPL]) {
-      const int64_t r0 = row_lo + (int64_t)b * R;
-      const int nr = (int)min((int64_t)R, row_hi - r0);
-#pragma unroll
-      for (int j = 0; j < IPL; ++j) {
-        const int e = lane + 32 * j;
-        dst[j] = e < nr ? (a.rows ? a.rows[r0 + e] : r0 + e) : 0;
-      }
-    };
-    // X slices of block b: TMA bulk copies, tx bytes announced without arriving
-    auto issue_x = [&](int b, const int64_t(&idx)[IPL]) {
-      const int s = b % S;
-      if (b >= S) mbar_wait(&empty[s], ((b / S) - 1) & 1);
-      const int64_t r0 = row_lo + (int64_t)b * R;
-      const int nr = (int)min((int64_t)R, row_hi - r0);
-      double *tile = tiles + (size_t)s * R * WS;
-      const unsigned bytes = (unsigned)wq * 8u;
-      if (lane == 0) mbar_expect_tx(&full[s], bytes * (unsigned)nr);
-      if (bytes > 0) {
-#pragma unroll
-        for (int j = 0; j < IPL; ++j) {
-          const int e = lane + 32 * j;
-          if (e < nr) bulk_g2s(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &full[s]);
-        }
-      }
-    };
-    // side data of block b (h rows / labels: possibly the predecessor's
-    // outputs) by cp.async; each lane's arrival fires when its copies land
-    auto issue_side = [&](int b, const int64_t(&idx)[IPL]) {
-      const int s = b % S;
-      const int64_t r0 = row_lo + (int64_t)b * R;
-      const int nr = (int)min((int64_t)R, row_hi - r0);
-      if (apply) {
-        double *hs = side + (size_t)s * R * K;
-        for (int e = lane; e < nr * K; e += 32) cp_async8(hs + e, a.h + r0 * K + e);
-      } else if (grad) {
-        int *ls = reinterpret_cast<int *>(side) + s * R;
-#pragma unroll
-        for (int j = 0; j < IPL; ++j) {
-          const int e = lane + 32 * j;
-          if (e < nr) cp_async4(ls + e, a.labels + idx[j]);
-        }
-      }
-      cp_async_mbar_arrive(&full[s]);
-    };
-    int64_t idx[2][IPL];
-    int b = 0;
-    if (nb > 0) load_idx(0, idx[0]);
-    if (a.early) {  // X and the row indices are older than the predecessor
-      for (; b < nb && b < S; ++b) {
-        if (b + 1 < nb) load_idx(b + 1, idx[(b + 1) & 1]);
-        issue_x(b, idx[b & 1]);
-      }
-    }
-    pdl_wait();
-    if (lane == 0) sh_skip = (a.skip != nullptr && *a.skip != 0.0) ? 1 : 0;
-    __syncwarp();
-    if (sh_skip) {  // complete the staged phases (so no copy is in flight), then leave
-      for (int bb = 0; bb < b; ++bb) {
-        mbar_arrive(&full[bb % S]);
-        mbar_wait(&full[bb % S], (bb / S) & 1);
-      }
-    } else {
-      // the weight slice (consumers wait on qbar): one bulk copy per class
-      if (a.qbulk && lane < K) {
-        const int qc = min(wq, a.p - c0);
-        if (lane == 0) mbar_arrive_expect_tx(qbar, (unsigned)(K * max(qc, 0) * 8));
-        if (qc > 0)
-          bulk_g2s(Qs + lane * WQ, a.w + (int64_t)lane * a.p + c0, (unsigned)qc * 8u, qbar);
-      }
-      // early-staged blocks only need their side data now (h never needs idx)
-      for (int bb = 0; bb < b; ++bb) issue_side(bb, idx[bb & 1]);
-      for (; b < nb; ++b) {
-        if (b + 1 < nb) load_idx(b + 1, idx[(b + 1) & 1]);
-        issue_x(b, idx[b & 1]);
-        issue_side(b, idx[b & 1]);
-      }
-    }
+  if (warp == kNW) {  // ---------------------------------------- producer
+    produce<R, K>(a, rg, row_lo, row_hi, nb, c0, wq, lane, &sh_skip);
     cluster_sync_all();
     return;
   }
-
-  // ------------------------------------------------------------ consumers
-  pdl_wait();  // the weights and the skip flag are the predecessor's outputs
+  pdl_wait();  // the weights, h and the skip flag may be the predecessor's outputs
   if (a.skip != nullptr && *a.skip != 0.0) {
     cluster_sync_all();
     return;
   }
-  // weight slice Qs[c][j] = w[c*p + c0 + j], zero past the slice / p: the
-  // producer's bulk copies (qbulk) or direct loads (batched: one round trip)
-  {
-    const int qc = a.qbulk ? max(0, min(wq, a.p - c0)) : 0;  // columns the copies bring
-    for (int i0 = tid; i0 < KQ * WQ; i0 += 8 * kNC) {
-      double v[8];
+  const int g8 = lane >> 2, t4 = lane & 3;
+
+  if (warp == kNW + 1) {  // ---------------------------------------- send warp
+    // the CTA's partial logits of block b -> every peer's Vr[b & 1][q].  The
+    // FP64 pipe is shared with the compute warps' MMA stream, so the dependent
+    // FP64 chains here are kept short (independent elements per lane,
+    // pairwise fixed-order trees).
+    for (int b = 0; b < nb; ++b) {
+      const int64_t r0 = row_lo + (int64_t)b * R;
+      const int nr = (int)min((int64_t)R, row_hi - r0);
+      mbar_wait(&redfull[b & 1], (b >> 1) & 1);
+      __syncwarp();  // lanes leave a polling loop one by one: reconverge
+      CL_TLX(b, 6);
+      const double *rb = red + (size_t)(b & 1) * kNW * R * K;
+      const unsigned vr_local = smem_u32(Vr + ((size_t)(b & 1) * cs + q) * R * K);
+      const unsigned bar_local = smem_u32(&vfull[b & 1]);
+      constexpr int EPL = (R * K + 31) / 32;
+      double v[EPL][kNW];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {  // loads first: one round trip per 8
-        const int i = i0 + u * kNC;
-        const int c = i / WQ, j = i - c * WQ, gc = c0 + j;
-        v[u] = (!a.qbulk && c < K && j < wq && gc < a.p) ? a.w[(int64_t)c * a.p + gc] : 0.0;
+      for (int j = 0; j < EPL; ++j) {
+        const int e = lane + 32 * j;
+#pragma unroll
+        for (int w = 0; w < kNW; ++w) v[j][w] = e < nr * K ? rb[w * R * K + e] : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 8; ++u) {
-        const int i = i0 + u * kNC;
-        const int c = i / WQ;
-        if (i < KQ * WQ && (c >= K || i - c * WQ >= qc)) Qs[i] = v[u];
+      for (int j = 0; j < EPL; ++j) {
+        const int e = lane + 32 * j;
+        const double sm = tree_sum<0, kNW>(v[j]);
+        if (e < nr * K)
+          for (int pq = 0; pq < cs; ++pq)
+            st_async(mapa(vr_local + e * 8, pq), sm, mapa(bar_local, pq));
+      }
+      CL_TLX(b, 7);
+    }
+    cluster_sync_all();
+    return;
+  }
+
+  if (warp == kNW + 2) {  // ----------------------------- row-algebra warp
+    double loss_acc = 0.0;
+    unsigned long long corr_acc = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int s = b % S;
+      const int64_t r0 = row_lo + (int64_t)b * R;
+      const int nr = (int)min((int64_t)R, row_hi - r0);
+      // the peers' partials of block b, summed in rank order -> row algebra
+      mbar_poll(&vfull[b & 1], (b >> 1) & 1);
+      __syncwarp();
+      CL_TLX(b, 8);
+      if (lane == 0 && b + 1 < nb) {  // arm the other buffer for block b + 1
+        const int nr1 = (int)min((int64_t)R, row_hi - (r0 + R));
+        mbar_arrive_expect_tx(&vfull[(b + 1) & 1], (unsigned)(cs * nr1 * K * 8));
+      }
+      // all 8 rows at once: 4 lanes per row, lane `sub` owns classes sub,
+      // sub + 4, sub + 8
+      const double *vr = Vr + (size_t)(b & 1) * cs * R * K;
+      double *u = Us + (size_t)(b & 1) * R * kUP;
+      const int row = lane >> 2, sub = lane & 3;
+      const bool rv = row < nr;
+      double z[3];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int c = sub + 4 * j;
+        double pz[4] = {0.0, 0.0, 0.0, 0.0};
+        if (rv && c < K) {
+#pragma unroll
+          for (int pq = 0; pq < 4; ++pq)
+            if (pq < cs) pz[pq] = vr[(pq * R + row) * K + c];
+          for (int pq = 4; pq < cs; ++pq) pz[pq & 3] += vr[(pq * R + row) * K + c];
+        }
+        z[j] = (pz[0] + pz[1]) + (pz[2] + pz[3]);
+      }
+      double uo[3] = {0.0, 0.0, 0.0};
+      if (apply) {
+        double hv[3], vw[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+          const int c = sub + 4 * j;
+          hv[j] = (rv && c < K) ? rg.side[((size_t)s * R + row) * K + c] : 0.0;
+          vw[j] = z[j] * hv[j];
+        }
+        const double sm = gsum<4>((vw[0] + vw[1]) + vw[2]);  // softmax.py:207 rowsum(VW)
+#pragma unroll
+        for (int j = 0; j < 3; ++j) uo[j] = vw[j] - hv[j] * sm;
+      } else {
+        // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
+        double M = 0.0;
+#pragma unroll
+        for (int j = 0; j < 3; ++j)
+          if (sub + 4 * j < K) M = max_nan(M, z[j]);
+        M = gmax_nan<4>(M);
+        double E[3];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) E[j] = (sub + 4 * j < K) ? exp(z[j] - M) : 0.0;
+        const double eM = exp(-M);
+        const double alpha = eM + gsum<4>((E[0] + E[1]) + E[2]);
+        if (prep) {
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (rv && sub + 4 * j < K && q == 0) a.hout[(r0 + row) * K + sub + 4 * j] = E[j] / alpha;
+        } else {
+          // grad: residual (softmax.py:157-161), loss (:134), accuracy (:224-247)
+          const int y = rv ? reinterpret_cast<const int *>(rg.side)[s * R + row] : -1;
+          double pr[3], lin = 0.0;
+#pragma unroll
+          for (int j = 0; j < 3; ++j) {
+            const int c = sub + 4 * j;
+            pr[j] = E[j] / alpha;
+            uo[j] = pr[j] - (c == y ? 1.0 : 0.0);
+            if (c < K && c == y) lin = z[j];
+          }
+          lin = gsum<4>(lin);
+          if (rv && sub == 0 && q == 0) loss_acc += (M + log(alpha)) - lin;
+          double bv = -INFINITY;
+          int bi = K + 1;
+#pragma unroll
+          for (int j = 0; j < 3; ++j)
+            if (sub + 4 * j < K) amax_take(bv, bi, pr[j], sub + 4 * j);
+          gargmax<4>(bv, bi);
+          amax_take(bv, bi, eM / alpha, K);  // the reference class
+          if (rv && sub == 0 && q == 0 && bi == y) corr_acc += 1ull;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int c = sub + 4 * j;
+        if (c < kUP) u[row * kUP + c] = (rv && c < K) ? uo[j] : 0.0;
+      }
+      CL_TLX(b, 9);
+      mbar_arrive(&ufull[b & 1]);  // each lane releases its own U stores
+    }
+    if (grad) {
+      const double l = warp_allsum(loss_acc);
+      unsigned long long cc = corr_acc;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
+      if (lane == 0 && q == 0) {
+        a.lossp[cl] = l;
+        a.corrp[cl] = cc;
       }
     }
-    if (a.qbulk) mbar_wait(qbar, 0);
+    cluster_sync_all();
+    return;
   }
+
+  // ---------------------------------------------------------- compute warps
+  const int nch = (wq + 15) >> 4, nmt = (wq + 7) >> 3;
+  double qf[kNCH][4];
+  load_qfrag<K>(a, c0, wq, g8, t4, warp, kNW, nch, qf);
+  load_q8<K>(a, Q8, c0, wq, a.WQ, tid, kNC);
   consumer_sync(kNC);
+  CL_TL(-1, 1);
+  double acc[kNMT][2], acc8[kNMT];
+#pragma unroll
+  for (int m = 0; m < kNMT; ++m) acc[m][0] = acc[m][1] = acc8[m] = 0.0;
 
-  const int rg = lane / KSL, ksl = lane % KSL;
-  const int kslice = warp * KSL + ksl;
-  // X^T U ownership
-  const int cg = tid % C::NCOLT, rsub = tid / C::NCOLT;
-  constexpr int AI = C::DM ? 1 : C::NCI, AE = C::DM ? 1 : C::CPT;
-  double acc[AI][AE][K];
-#pragma unroll
-  for (int i = 0; i < AI; ++i)
-#pragma unroll
-    for (int e = 0; e < AE; ++e)
-#pragma unroll
-      for (int c = 0; c < K; ++c) acc[i][e][c] = 0.0;
-  // DM: X^T U tiles (classes 2t, 2t+1 of column 8*tile + g) and class-8 partials
-  constexpr int MT = C::DM ? C::NMT : 1;
-  double dacc[MT][2], dacc8[MT];
-#pragma unroll
-  for (int m = 0; m < MT; ++m) dacc[m][0] = dacc[m][1] = dacc8[m] = 0.0;
-  const int g8 = lane >> 2, t4 = lane & 3;
-  double loss_acc = 0.0;
-  unsigned long long corr_acc = 0;
-
-  // V phase of block b: partial logits of this slice, reduced over the CTA and
-  // pushed to every peer's Vr[b & 1][q]
+  // partial logits of block b (k split over the warps) -> red[b & 1][warp]
   auto vphase = [&](int b) {
     const int s = b % S;
-    const int64_t r0 = row_lo + (int64_t)b * R;
-    const int nr = (int)min((int64_t)R, row_hi - r0);
-    const int rtv = (nr + RGL - 1) / RGL;  // valid row slots (warp-uniform)
-    mbar_wait(&full[s], (b / S) & 1);
-    const double *tile = tiles + (size_t)s * R * WS;
-    if constexpr (C::DM) {
-      // 16-column chunks ch = warp, warp + 8, ...; physical column of (step s,
-      // lane t) = 16 ch + 4 t + s, so a lane's 4 A (and B) values are contiguous
-      double c2[2] = {0.0, 0.0}, v8 = 0.0;
-      const double *xrow = tile + (size_t)g8 * WS + 4 * t4;
-      const double *qrow = Qs + (size_t)g8 * WQ + 4 * t4;
-      const double *q8row = Qs + (size_t)8 * WQ + 4 * t4;
-      const int nch = (wq + 15) >> 4;
-#pragma unroll 2
-      for (int ch = warp; ch < nch; ch += kNW) {
-        const double2 xa = *reinterpret_cast<const double2 *>(xrow + 16 * ch);
-        const double2 xb = *reinterpret_cast<const double2 *>(xrow + 16 * ch + 2);
-        const double2 qa = *reinterpret_cast<const double2 *>(qrow + 16 * ch);
-        const double2 qb = *reinterpret_cast<const double2 *>(qrow + 16 * ch + 2);
-        dmma(c2, xa.x, qa.x);
-        dmma(c2, xa.y, qa.y);
-        dmma(c2, xb.x, qb.x);
-        dmma(c2, xb.y, qb.y);
-        if constexpr (K == 9) {
-          const double2 ra = *reinterpret_cast<const double2 *>(q8row + 16 * ch);
-          const double2 rb2 = *reinterpret_cast<const double2 *>(q8row + 16 * ch + 2);
-          v8 = fma(xa.x, ra.x, v8);
-          v8 = fma(xa.y, ra.y, v8);
-          v8 = fma(xb.x, rb2.x, v8);
-          v8 = fma(xb.y, rb2.y, v8);
-        }
-      }
-      double *rbw = red + (size_t)(b & 1) * kNW * R * K + (size_t)warp * R * K + g8 * K;
-      if (2 * t4 < K) rbw[2 * t4] = c2[0];
-      if (2 * t4 + 1 < K) rbw[2 * t4 + 1] = c2[1];
-      if constexpr (K == 9) {
-        v8 += __shfl_xor_sync(0xffffffffu, v8, 1);
-        v8 += __shfl_xor_sync(0xffffffffu, v8, 2);
-        if (t4 == 0) rbw[8] = v8;
-      }
-      return;
-    }
-    double v[RT][K];
-#pragma unroll
-    for (int rt = 0; rt < RT; ++rt)
-#pragma unroll
-      for (int c = 0; c < K; ++c) v[rt][c] = 0.0;
-#pragma unroll 2
-    for (int i = 0; i < a.npi; ++i) {
-      const int col = 2 * (i * KS + kslice);
-      double2 qv[K];
-#pragma unroll
-      for (int c = 0; c < K; ++c) qv[c] = *reinterpret_cast<const double2 *>(Qs + c * WQ + col);
-#pragma unroll
-      for (int rt = 0; rt < RT; ++rt) {
-        if (rt < rtv) {
-          const double2 x =
-              *reinterpret_cast<const double2 *>(tile + (size_t)(rt * RGL + rg) * WS + col);
-#pragma unroll
-          for (int c = 0; c < K; ++c) {
-            v[rt][c] = fma(x.x, qv[c].x, v[rt][c]);
-            v[rt][c] = fma(x.y, qv[c].y, v[rt][c]);
-          }
-        }
-      }
-    }
-    // in-warp reduction over the KSL lanes of a row group: reduce-scatter over
-    // the row slots, then full butterflies (fixed order)
-    int slot0 = 0;
-#pragma unroll
-    for (int L = 0; L < C::LV; ++L) {
-      const int o = 1 << L;
-      if (L < C::LS) {
-        const int half = RT >> (L + 1);
-        const int bit = (ksl >> L) & 1;
-#pragma unroll
-        for (int j = 0; j < (RT >> 1); ++j) {
-          if (j < half) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) {
-              const double send = bit ? v[j][c] : v[j + half][c];
-              const double keep = bit ? v[j + half][c] : v[j][c];
-              v[j][c] = keep + __shfl_xor_sync(0xffffffffu, send, o);
-            }
-          }
-        }
-        slot0 += bit * half;
-      } else {
-#pragma unroll
-        for (int j = 0; j < (RT >> C::LS); ++j)
-#pragma unroll
-          for (int c = 0; c < K; ++c) v[j][c] += __shfl_xor_sync(0xffffffffu, v[j][c], o);
-      }
-    }
-    // writers: lanes whose full-butterfly bits are zero
-    double *rb = red + (size_t)(b & 1) * kNW * R * K + (size_t)warp * R * K;
-    if ((ksl >> C::LS) == 0) {
-#pragma unroll
-      for (int j = 0; j < (RT >> C::LS); ++j) {
-        const int row = (slot0 + j) * RGL + rg;
-#pragma unroll
-        for (int c = 0; c < K; ++c) rb[row * K + c] = v[j][c];
-      }
-    }
+    mbar_wait(&rg.full[s], (b / S) & 1);
+    __syncwarp();  // reconverge before the warp-wide MMAs
+    const double *tile = rg.tiles + (size_t)s * R * WS;
+    double c2[2], v8;
+    vgroup<K>(tile + (size_t)g8 * WS + 4 * t4, Q8 + 4 * t4, qf, warp, kNW, nch, c2, v8);
+    double *rbw = red + (size_t)(b & 1) * kNW * R * K + (size_t)warp * R * K + g8 * K;
+    if (2 * t4 < K) rbw[2 * t4] = c2[0];
+    if (2 * t4 + 1 < K) rbw[2 * t4 + 1] = c2[1];
+    if (K == 9 && t4 == 0) rbw[8] = v8;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&redfull[b & 1]);
   };
 
-  // sum of the warp partials (fixed order) -> every peer's receive buffer
-  auto vsend = [&](int b) {
-    const int64_t r0 = row_lo + (int64_t)b * R;
-    const int nr = (int)min((int64_t)R, row_hi - r0);
-    const double *rb = red + (size_t)(b & 1) * kNW * R * K;
-    const unsigned vr_local = smem_u32(Vr + ((size_t)(b & 1) * cs + q) * R * K);
-    const unsigned bar_local = smem_u32(&vfull[b & 1]);
-    for (int e = tid; e < nr * K; e += kNC) {
-      double s = 0.0;
-#pragma unroll
-      for (int w = 0; w < kNW; ++w) s += rb[w * R * K + e];
-      for (int pq = 0; pq < cs; ++pq)
-        st_async(mapa(vr_local + e * 8, pq), s, mapa(bar_local, pq));
-    }
-  };
-
-  // row algebra of block b (half-warp per row, lanes over classes): U rows
-  // into Us[b & 1]; h (prep), loss / correct (grad)
-  auto rowalg = [&](int b) {
-    const int s = b % S;
-    const int64_t r0 = row_lo + (int64_t)b * R;
-    const int nr = (int)min((int64_t)R, row_hi - r0);
-    mbar_wait_cluster(&vfull[b & 1], (b >> 1) & 1);
-    CL_TL(b, 6);
-    if (tid == 0 && b + 1 < nb) {  // the next use of this buffer pair's other barrier
-      const int nr1 = (int)min((int64_t)R, row_hi - (r0 + R));
-      mbar_arrive_expect_tx(&vfull[(b + 1) & 1], (unsigned)(cs * nr1 * K * 8));
-    }
-    CL_TL(b, 8);
-    const double *vr = Vr + (size_t)(b & 1) * cs * R * K;
-    double *u = Us + (size_t)(b & 1) * R * KP;
-    const int hw = lane >> 4, c = lane & 15;
-    for (int rp = warp; rp < R / 2; rp += kNW) {  // warp-uniform trip count
-      const int row = 2 * rp + hw;
-      const bool rv = row < nr;
-      double z = 0.0;
-      if (rv && c < K)
-        for (int pq = 0; pq < cs; ++pq) z += vr[(pq * R + row) * K + c];
-      CL_TL(b, 7);
-      if (apply) {
-        const double hv = (rv && c < K) ? side[((size_t)s * R + row) * K + c] : 0.0;
-        const double vw = z * hv;
-        const double sm = hsum(vw);  // softmax.py:207 rowsum(VW)
-        if (c < KP) u[row * KP + c] = (rv && c < K) ? vw - hv * sm : 0.0;
-        continue;
-      }
-      // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
-      const double zc = (c < K) ? z : 0.0;
-      const double M = hmax_nan(zc);  // lanes >= K contribute 0 = the reference class logit
-      const double E = (c < K) ? exp(z - M) : 0.0;
-      const double alpha = exp(-M) + hsum(E);
-      if (a.mode == kPrep) {
-        if (rv && c < K && q == 0) a.hout[(r0 + row) * K + c] = E / alpha;
-        continue;
-      }
-      // grad: residual (softmax.py:157-161), loss (:134), accuracy (:224-247)
-      const int y = rv ? reinterpret_cast<const int *>(side)[s * R + row] : 0;
-      const double pr = (c < K) ? E / alpha : (c == K ? exp(-M) / alpha : -INFINITY);
-      if (c < KP) u[row * KP + c] = (rv && c < K) ? pr - (c == y ? 1.0 : 0.0) : 0.0;
-      const double lin = hsum((c < K && c == y) ? z : 0.0);
-      if (rv && c == 0 && q == 0) loss_acc += (M + log(alpha)) - lin;
-      const int best = hargmax(pr, c);
-      if (rv && c == 0 && q == 0 && best == y) corr_acc += 1ull;
-    }
-    CL_TL(b, 9);
-  };
-
-  auto xtu = [&](int b) {
-    const int s = b % S;
-    const int64_t r0 = row_lo + (int64_t)b * R;
-    const int nr = (int)min((int64_t)R, row_hi - r0);
-    const double *tile = tiles + (size_t)s * R * WS;
-    const double *u = Us + (size_t)(b & 1) * R * KP;
-    if constexpr (C::DM) {
-      // rows of step s, lane t: 2t + s (each bank hit by two of the four rows)
-      const double ua0 = u[(2 * t4) * KP + g8], ua1 = u[(2 * t4 + 1) * KP + g8];
-      const double u80 = K == 9 ? u[(2 * t4) * KP + 8] : 0.0;
-      const double u81 = K == 9 ? u[(2 * t4 + 1) * KP + 8] : 0.0;
-      const bool ok0 = 2 * t4 < nr, ok1 = 2 * t4 + 1 < nr;
-      const double *x0 = tile + (size_t)(2 * t4) * WS + g8;
-      const double *x1 = x0 + WS;
-      const int nmt = (wq + 7) >> 3;
-#pragma unroll
-      for (int m = 0; m < C::NMT; ++m) {
-        const int mt = warp + kNW * m;
-        if (mt < nmt) {
-          const double a0 = ok0 ? x0[8 * mt] : 0.0;
-          const double a1 = ok1 ? x1[8 * mt] : 0.0;
-          dmma(dacc[m], a0, ua0);
-          dmma(dacc[m], a1, ua1);
-          if constexpr (K == 9) {
-            dacc8[m] = fma(a0, u80, dacc8[m]);
-            dacc8[m] = fma(a1, u81, dacc8[m]);
-          }
-        }
-      }
-      return;
-    }
-    int nci = 0;  // active column chunks of this warp (warp-uniform)
-#pragma unroll
-    for (int i = 0; i < C::NCI; ++i)
-      if ((i * C::NCOLT + ((warp * 32) % C::NCOLT)) * C::CPT < wq) nci = i + 1;
-    for (int r = rsub; r < nr; r += C::RS) {
-      double ur[KP];
-#pragma unroll
-      for (int c = 0; c < KP; c += 2) {
-        const double2 t2 = *reinterpret_cast<const double2 *>(u + r * KP + c);
-        ur[c] = t2.x;
-        ur[c + 1] = t2.y;
-      }
-      const double *xr = tile + (size_t)r * WS;
-#pragma unroll
-      for (int i = 0; i < C::NCI; ++i) {
-        if (i < nci) {
-          double x[C::CPT];
-          const int col = (i * C::NCOLT + cg) * C::CPT;
-          if constexpr (C::CPT == 1) {
-            x[0] = xr[col];
-          } else {
-#pragma unroll
-            for (int e = 0; e < C::CPT; e += 2) {
-              const double2 t2 = *reinterpret_cast<const double2 *>(xr + col + e);
-              x[e] = t2.x;
-              x[e + 1] = t2.y;
-            }
-          }
-#pragma unroll
-          for (int e = 0; e < C::CPT; ++e)
-#pragma unroll
-            for (int c = 0; c < K; ++c) acc[i][e][c] = fma(x[e], ur[c], acc[i][e][c]);
-        }
-      }
-    }
-  };
-
-  CL_TL(-1, 1);
-  if (nb > 0) {
-    vphase(0);
-    consumer_sync(kNC);
-    vsend(0);
-  }
+  if (nb > 0) vphase(0);
   CL_TL(-1, 2);
   for (int b = 0; b < nb; ++b) {
     CL_TL(b, 0);
-    rowalg(b);
-    CL_TL(b, 1);
     if (b + 1 < nb) vphase(b + 1);
-    CL_TL(b, 2);
-    consumer_sync(kNC);  // U(b) and the warp partials of b + 1 visible
-    CL_TL(b, 3);
-    if (b + 1 < nb) vsend(b + 1);
-    CL_TL(b, 4);
-    if (a.mode != kPrep) xtu(b);
-    CL_TL(b, 5);
+    CL_TL(b, 1);
+    mbar_wait(&ufull[b & 1], (b >> 1) & 1);
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[b % S]);
+    CL_TL(b, 2);
+    if (!prep) {
+      const int64_t r0 = row_lo + (int64_t)b * R;
+      const int nr = (int)min((int64_t)R, row_hi - r0);
+      xgroup<K, kNMT>(rg.tiles + (size_t)(b % S) * R * WS, WS, Us + (size_t)(b & 1) * R * kUP,
+                      nr, g8, t4, warp, kNW, nmt, acc, acc8);
+    }
+    CL_TL(b, 3);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&rg.empty[b % S]);
   }
   CL_TL(-1, 3);
-
-  // ------------------------------------------------------------ epilogue
-  if (grad) {
-    double l = warp_allsum(loss_acc);
-    unsigned long long cc = corr_acc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
-    if (lane == 0) {
-      sh_loss[warp] = l;
-      sh_corr[warp] = cc;
-    }
-  }
-  if (a.mode != kPrep) {
+  if (!prep) {
     const int64_t d = (int64_t)K * a.p;
-    double *g = a.gp + (int64_t)cl * d;
-    if constexpr (C::DM) {
-      const int nmt = (wq + 7) >> 3;
+    double *gq = a.gp + (int64_t)cl * d;
 #pragma unroll
-      for (int m = 0; m < C::NMT; ++m) {
-        const int mt = warp + kNW * m;
-        double s8 = dacc8[m];
-        if constexpr (K == 9) {
-          s8 += __shfl_xor_sync(0xffffffffu, s8, 1);
-          s8 += __shfl_xor_sync(0xffffffffu, s8, 2);
-        }
-        const int col = 8 * mt + g8, gc = c0 + col;
-        if (mt < nmt && col < wq && gc < a.p) {
-          if (2 * t4 < K) g[(int64_t)(2 * t4) * a.p + gc] = dacc[m][0];
-          if (2 * t4 + 1 < K) g[(int64_t)(2 * t4 + 1) * a.p + gc] = dacc[m][1];
-          if (K == 9 && t4 == 0) g[(int64_t)8 * a.p + gc] = s8;
-        }
+    for (int m = 0; m < kNMT; ++m) {
+      const int mt = warp + kNW * m;
+      const double s8 = K == 9 ? gsum<4>(acc8[m]) : 0.0;
+      const int col = 8 * mt + g8, gc = c0 + col;
+      if (mt < nmt && col < wq && gc < a.p) {
+        if (2 * t4 < K) gq[(int64_t)(2 * t4) * a.p + gc] = acc[m][0];
+        if (2 * t4 + 1 < K) gq[(int64_t)(2 * t4 + 1) * a.p + gc] = acc[m][1];
+        if (K == 9 && t4 == 0) gq[(int64_t)8 * a.p + gc] = s8;
       }
-    } else if constexpr (C::RS == 1) {
-#pragma unroll
-      for (int i = 0; i < C::NCI; ++i)
-#pragma unroll
-        for (int e = 0; e < C::CPT; ++e) {
-          const int col = (i * C::NCOLT + cg) * C::CPT + e;
-          const int gc = c0 + col;
-          if (col < wq && gc < a.p) {
-#pragma unroll
-            for (int c = 0; c < K; ++c) g[(int64_t)c * a.p + gc] = acc[i][e][c];
-          }
-        }
-    } else {
-      // combine the RS row subsets in order through shared memory (the tiles are free)
-      consumer_sync(kNC);
-      constexpr int NCOL = C::NCOLT * C::CPT * C::NCI;
-      double *comb = tiles;  // [RS][NCOL][K]
-#pragma unroll
-      for (int i = 0; i < C::NCI; ++i)
-#pragma unroll
-        for (int e = 0; e < C::CPT; ++e)
-#pragma unroll
-          for (int c = 0; c < K; ++c)
-            comb[((size_t)rsub * NCOL + (i * C::NCOLT + cg) * C::CPT + e) * K + c] =
-                acc[i][e][c];
-      consumer_sync(kNC);
-      for (int t = tid; t < NCOL * K; t += kNC) {
-        const int c = t / NCOL, col = t - c * NCOL;
-        double s = 0.0;
-        for (int r = 0; r < C::RS; ++r) s += comb[((size_t)r * NCOL + col) * K + c];
-        const int gc = c0 + col;
-        if (col < wq && gc < a.p) g[(int64_t)c * a.p + gc] = s;
-      }
-    }
-  }
-  if (grad) {
-    consumer_sync(kNC);
-    if (tid == 0 && q == 0) {
-      double l = 0.0;
-      unsigned long long cc = 0;
-      for (int w = 0; w < kNW; ++w) {
-        l += sh_loss[w];
-        cc += sh_corr[w];
-      }
-      a.lossp[cl] = l;
-      a.corrp[cl] = cc;
     }
   }
   CL_TL(-1, 4);
@@ -771,6 +675,193 @@ __global__ void __launch_bounds__(kNT, 1) cluster_rowpass_kernel(const __grid_co
   CL_TL(-1, 5);
 }
 
+// ---------------------------------------------------------------- row split
+// p <= 64: warp w owns rows 8w..8w+7 of every 64-row block completely (V over
+// all columns, the row algebra in registers, X^T U of its rows); the CTA's
+// K x p partial is reduced over the warps once at the end.
+template <int K>
+__global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant__ Args a) {
+  constexpr int R = kRR;
+  constexpr int NMT = 8;  // column tiles: p <= 64
+  pdl_trigger();
+  extern __shared__ __align__(1024) unsigned char smem[];
+  Ring rg;
+  rg.tiles = reinterpret_cast<double *>(smem + a.o_tiles);  // [S][R][WS]
+  rg.side = reinterpret_cast<double *>(smem + a.o_side);    // [S][R][K] h | [S][R] int
+  double *Q8 = reinterpret_cast<double *>(smem + a.o_q);    // [WQ] class-8 weights
+  double *Uw = reinterpret_cast<double *>(smem + a.o_u);    // [NW][8][kUP] per warp
+  rg.full = reinterpret_cast<uint64_t *>(smem + a.o_bar);
+  rg.empty = rg.full + a.S;
+  __shared__ int sh_skip;
+  __shared__ double sh_loss[kNW];
+  __shared__ unsigned long long sh_corr[kNW];
+
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  const int S = a.S, WS = a.WS;
+  const int cl = blockIdx.x;
+  const int64_t row_lo = a.nrows * cl / a.ncl, row_hi = a.nrows * (cl + 1) / a.ncl;
+  const int nb = (int)((row_hi - row_lo + R - 1) / R);
+  const int wq = (a.p + 3) & ~3;  // the whole (padded) row
+  const bool apply = a.mode == kApply, grad = a.mode == kGrad, prep = a.mode == kPrep;
+
+  if (tid == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&rg.full[s], 32);
+      mbar_init(&rg.empty[s], kNW);
+    }
+    mbar_fence_init();
+  }
+  for (int i = tid; i < S * R * (WS - wq); i += kNTR) {
+    const int r = i / (WS - wq), j = i - r * (WS - wq);
+    rg.tiles[(size_t)r * WS + wq + j] = 0.0;
+  }
+  __syncthreads();
+  if (warp == kNW) {
+    produce<R, K>(a, rg, row_lo, row_hi, nb, 0, wq, lane, &sh_skip);
+    return;
+  }
+  pdl_wait();
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  const int g = lane >> 2, t = lane & 3;
+  const int nch = (wq + 15) >> 4, nmt = (wq + 7) >> 3;
+  double qf[kNCH][4];
+  load_qfrag<K>(a, 0, wq, g, t, 0, 1, nch, qf);
+  load_q8<K>(a, Q8, 0, wq, a.WQ, tid, kNC);
+  consumer_sync(kNC);
+  double acc[NMT][2], acc8[NMT];
+#pragma unroll
+  for (int m = 0; m < NMT; ++m) acc[m][0] = acc[m][1] = acc8[m] = 0.0;
+  double loss_acc = 0.0;
+  unsigned long long corr_acc = 0;
+  double *u = Uw + (size_t)warp * 8 * kUP;
+  const bool c0v = 2 * t < K, c1v = 2 * t + 1 < K;
+
+  for (int b = 0; b < nb; ++b) {
+    const int s = b % S;
+    const int64_t r0 = row_lo + (int64_t)b * R;
+    const int nr = (int)min((int64_t)R, row_hi - r0);
+    const int gr0 = 8 * warp;          // the warp's first row in the block
+    const int ng = min(8, nr - gr0);   // its valid rows (warp-uniform)
+    mbar_wait(&rg.full[s], (b / S) & 1);
+    __syncwarp();  // reconverge before the warp-wide MMAs
+    if (ng > 0) {
+      const double *tile = rg.tiles + (size_t)s * R * WS + (size_t)gr0 * WS;
+      double c2[2], v8;
+      vgroup<K>(tile + (size_t)g * WS + 4 * t, Q8 + 4 * t, qf, 0, 1, nch, c2, v8);
+      // row algebra: lane (g, t) holds classes 2t, 2t+1 of row g (+ class 8)
+      const int row = gr0 + g;
+      const bool rv = g < ng;
+      const double z0 = c0v ? c2[0] : 0.0, z1 = c1v ? c2[1] : 0.0, z8 = K == 9 ? v8 : 0.0;
+      double u0 = 0.0, u1 = 0.0, u8 = 0.0;
+      if (apply) {
+        const double *hr = rg.side + ((size_t)s * R + row) * K;
+        const double h0 = (rv && c0v) ? hr[2 * t] : 0.0, h1 = (rv && c1v) ? hr[2 * t + 1] : 0.0;
+        const double h8 = (rv && K == 9) ? hr[K == 9 ? 8 : 0] : 0.0;
+        const double w0 = z0 * h0, w1 = z1 * h1, w8 = z8 * h8;
+        const double sm = gsum<4>(w0 + w1) + w8;  // softmax.py:207 rowsum(VW)
+        u0 = w0 - h0 * sm;
+        u1 = w1 - h1 * sm;
+        u8 = w8 - h8 * sm;
+      } else {
+        // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
+        double M = max_nan(c0v ? z0 : 0.0, c1v ? z1 : 0.0);
+        M = gmax_nan<4>(M);
+        if (K == 9) M = max_nan(M, z8);
+        M = max_nan(M, 0.0);
+        const double E0 = c0v ? exp(z0 - M) : 0.0, E1 = c1v ? exp(z1 - M) : 0.0;
+        const double E8 = K == 9 ? exp(z8 - M) : 0.0;
+        const double eM = exp(-M);
+        const double alpha = eM + (gsum<4>(E0 + E1) + E8);
+        if (prep) {
+          if (rv) {
+            double *ho = a.hout + (r0 + row) * K;
+            if (c0v) ho[2 * t] = E0 / alpha;
+            if (c1v) ho[2 * t + 1] = E1 / alpha;
+            if (K == 9 && t == 0) ho[K == 9 ? 8 : 0] = E8 / alpha;
+          }
+        } else {
+          // grad: residual (softmax.py:157-161), loss (:134), accuracy (:224-247)
+          const int y = rv ? reinterpret_cast<const int *>(rg.side)[s * R + row] : -1;
+          const double p0 = E0 / alpha, p1 = E1 / alpha, p8 = E8 / alpha;
+          u0 = p0 - (2 * t == y ? 1.0 : 0.0);
+          u1 = p1 - (2 * t + 1 == y ? 1.0 : 0.0);
+          u8 = p8 - (y == 8 ? 1.0 : 0.0);
+          const double lin = gsum<4>((c0v && 2 * t == y ? z0 : 0.0) +
+                                     (c1v && 2 * t + 1 == y ? z1 : 0.0)) +
+                             (K == 9 && y == 8 ? z8 : 0.0);
+          if (rv && t == 0) loss_acc += (M + log(alpha)) - lin;
+          // argmax over [p_0..p_{K-1}, e^-M/alpha]: first NaN / first max wins
+          double bv = c0v ? p0 : -INFINITY;
+          int bi = 2 * t;
+          if (c1v) amax_take(bv, bi, p1, 2 * t + 1);
+          gargmax<4>(bv, bi);
+          if (K == 9) amax_take(bv, bi, p8, 8);
+          amax_take(bv, bi, eM / alpha, K);
+          if (rv && t == 0 && bi == y) corr_acc += 1ull;
+        }
+      }
+      if (!rv) u0 = u1 = u8 = 0.0;
+      u[g * kUP + 2 * t] = u0;
+      u[g * kUP + 2 * t + 1] = u1;
+      if (t == 0) {
+        u[g * kUP + 8] = u8;
+        u[g * kUP + 9] = 0.0;
+      }
+      __syncwarp();
+      if (!prep)
+        xgroup<K, NMT>(rg.tiles + (size_t)s * R * WS + (size_t)gr0 * WS, WS, u, ng, g, t, 0, 1,
+                       nmt, acc, acc8);
+      __syncwarp();
+    }
+    if (lane == 0) mbar_arrive(&rg.empty[s]);
+  }
+  // the CTA's partial: warps reduced in order through shared memory (the tiles)
+  consumer_sync(kNC);
+  if (!prep) {
+    double *comb = rg.tiles;  // [NW][64 columns][kUP]
+#pragma unroll
+    for (int m = 0; m < NMT; ++m) {
+      const double s8 = K == 9 ? gsum<4>(acc8[m]) : 0.0;
+      double *cp = comb + ((size_t)warp * 64 + 8 * m + g) * kUP;
+      cp[2 * t] = acc[m][0];
+      cp[2 * t + 1] = acc[m][1];
+      if (t == 0) cp[8] = s8;
+    }
+    consumer_sync(kNC);
+    const int64_t d = (int64_t)K * a.p;
+    for (int e = tid; e < K * 64; e += kNC) {
+      const int c = e / 64, col = e - c * 64;
+      double sm = 0.0;
+#pragma unroll
+      for (int w = 0; w < kNW; ++w) sm += comb[((size_t)w * 64 + col) * kUP + c];
+      if (col < a.p) a.gp[(int64_t)cl * d + (int64_t)c * a.p + col] = sm;
+    }
+  }
+  if (grad) {
+    const double l = warp_allsum(loss_acc);
+    unsigned long long cc = corr_acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
+    if (lane == 0) {
+      sh_loss[warp] = l;
+      sh_corr[warp] = cc;
+    }
+    consumer_sync(kNC);
+    if (tid == 0) {
+      double lt = 0.0;
+      unsigned long long ct = 0;
+      for (int w = 0; w < kNW; ++w) {
+        lt += sh_loss[w];
+        ct += sh_corr[w];
+      }
+      a.lossp[cl] = lt;
+      a.corrp[cl] = ct;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- finalize
 // out[i] = scale * sum_cl gp[cl][i] + lam * base[i] (fixed order: F lanes per
 // element sum the partials cl = f (mod F) in order, then an xor butterfly),
 // block b owns elements [b*EPB, (b+1)*EPB) -> dots[b] = base.out, dots[B+b] =
@@ -839,16 +930,41 @@ __global__ void __launch_bounds__(kFinThreads)
 // ---------------------------------------------------------------- host side
 struct Plan {
   int ok;
-  int cfg;  // 0: CfgA, 1: CfgB
-  int cs, ncl, wc, npi, S, WS, WQ, R;
+  int split;  // 0: column split (clusters), 1: row split
+  int cs, ncl, wc, S, WS, WQ, R;
   size_t smem;
   int o_tiles, o_q, o_side, o_u, o_vr, o_red, o_bar;
 };
 
-template <int K, typename C>
+template <typename KernT>
+static size_t smem_cap(KernT kern) {
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
+          cudaSuccess ||
+      optin <= 0)
+    optin = 227 * 1024;
+  cudaFuncAttributes fa{};
+  cudaFuncGetAttributes(&fa, kern);
+  cudaGetLastError();
+  return (size_t)optin - fa.sharedSizeBytes;
+}
+
+template <int K>
+static size_t cap_a() {
+  static size_t c = 0;
+  if (!c) c = smem_cap(cluster_rowpass_kernel<K>);
+  return c;
+}
+template <int K>
+static size_t cap_r() {
+  static size_t c = 0;
+  if (!c) c = smem_cap(rowsplit_kernel<K>);
+  return c;
+}
+
+template <int K>
 static void layout(Plan &pl, int S) {
-  constexpr int KP = C::DM ? 10 : K + (K & 1);
-  constexpr int KQ = C::DM ? (K > 8 ? K : 8) : K;
   size_t off = 0;
   auto take = [&](size_t bytes, size_t align) {
     off = (off + align - 1) / align * align;
@@ -856,69 +972,36 @@ static void layout(Plan &pl, int S) {
     off += bytes;
     return (int)o;
   };
-  pl.o_tiles = take((size_t)S * C::R * pl.WS * 8, 1024);
-  pl.o_q = take((size_t)KQ * pl.WQ * 8, 16);
-  pl.o_side = take((size_t)S * C::R * K * 8, 16);
-  pl.o_u = take((size_t)2 * C::R * KP * 8, 16);
-  pl.o_vr = take((size_t)2 * pl.cs * C::R * K * 8, 16);
-  pl.o_red = take((size_t)2 * kNW * C::R * K * 8, 16);
-  pl.o_bar = take((size_t)(2 * S + 3) * 8, 8);
+  pl.o_tiles = take((size_t)S * pl.R * pl.WS * 8, 1024);
+  pl.o_q = take((size_t)pl.WQ * 8, 16);
+  pl.o_side = take((size_t)S * pl.R * K * 8, 16);
+  if (pl.split == 0) {
+    pl.o_u = take((size_t)2 * kRA * kUP * 8, 16);
+    pl.o_vr = take((size_t)2 * pl.cs * kRA * K * 8, 16);
+    pl.o_red = take((size_t)2 * kNW * kRA * K * 8, 16);
+    pl.o_bar = take((size_t)(2 * S + 6) * 8, 8);
+  } else {
+    pl.o_u = take((size_t)kNW * 8 * kUP * 8, 16);
+    pl.o_vr = pl.o_red = 0;
+    pl.o_bar = take((size_t)(2 * S) * 8, 8);
+    // the final warp reduction reuses the tiles: [NW][64][kUP] doubles
+    if ((size_t)S * pl.R * pl.WS * 8 < (size_t)kNW * 64 * kUP * 8) off = (size_t)1 << 30;
+  }
   pl.smem = off;
   pl.S = S;
 }
 
-// the dynamic shared-memory ceiling is raised once to the maximum: plans of
-// different sizes share one instantiation
-// (opt-in per-block maximum minus the kernel's static shared memory)
-template <int K, typename C>
-static size_t smem_cap() {
-  static size_t cap = 0;
-  if (cap == 0) {
-    int dev = 0, optin = 0;
-    cudaGetDevice(&dev);
-    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) !=
-            cudaSuccess ||
-        optin <= 0)
-      optin = 227 * 1024;
-    cudaFuncAttributes fa{};
-    cudaFuncGetAttributes(&fa, cluster_rowpass_kernel<K, C>);
-    cudaGetLastError();
-    cap = (size_t)optin - fa.sharedSizeBytes;
-  }
-  return cap;
-}
-
-template <int K, typename C>
-static bool set_max_smem() {
-  static bool done = false;
-  if (!done) {
-    if (cudaFuncSetAttribute(cluster_rowpass_kernel<K, C>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_cap<K, C>()) != cudaSuccess)
-      return false;
-    done = true;
-  }
-  return true;
-}
-
-template <int K, typename C>
+template <int K>
 static int max_clusters(int cs, size_t smem) {
-  static int cache[9][2048];
-  static bool init = false;
-  if (!init) {
-    for (auto &row : cache)
-      for (int &v : row) v = -1;
-    init = true;
-  }
-  const int key = (int)(smem / 1024);
+  static int cache[4] = {-1, -1, -1, -1};
+  static size_t cache_smem[4] = {0, 0, 0, 0};
   const int ci = cs == 1 ? 0 : cs == 2 ? 1 : cs == 4 ? 2 : 3;
-  int &slot = cache[ci * 2 + (C::R == 8 ? 0 : 1)][key < 2048 ? key : 2047];
-  if (slot >= 0) return slot;
-  auto kern = cluster_rowpass_kernel<K, C>;
-  set_max_smem<K, C>();
+  if (cache[ci] >= 0 && cache_smem[ci] == smem) return cache[ci];
+  auto kern = cluster_rowpass_kernel<K>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_a<K>());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs * 64);
-  cfg.blockDim = dim3(kNT);
+  cfg.blockDim = dim3(kNTA);
   cfg.dynamicSmemBytes = smem;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeClusterDimension;
@@ -932,65 +1015,63 @@ static int max_clusters(int cs, size_t smem) {
     cudaGetLastError();
     n = sm_count() / cs;
   }
-  slot = n;
+  cache[ci] = n;
+  cache_smem[ci] = smem;
   return n;
-}
-
-template <int K, typename C>
-static Plan plan_cfg(int P, int64_t nrows, int cs, int cfg_id) {
-  Plan pl{};
-  pl.cfg = cfg_id;
-  pl.cs = cs;
-  pl.R = C::R;
-  pl.wc = ((P + cs - 1) / cs + 1) & ~1;
-  if constexpr (C::DM) {
-    // 16-column chunks; row strides = 2 (mod 16) doubles: the fragment loads of
-    // neighbouring rows interleave across the banks
-    pl.npi = (pl.wc + 15) / 16;
-    pl.WQ = pl.npi * 16 + 2;
-    pl.WS = pl.npi * 16 + 2;
-    if ((pl.wc + 7) / 8 > kNW * C::NMT) return pl;  // slice too wide for the tiles
-  } else {
-    pl.npi = (pl.wc / 2 + C::KS - 1) / C::KS;
-    pl.WQ = 2 * C::KS * pl.npi;
-    const int xcols = (pl.wc + 32 * C::CPT - 1) / (32 * C::CPT) * (32 * C::CPT);
-    const int need = pl.WQ > xcols ? pl.WQ : xcols;
-    pl.WS = (need + 15) / 16 * 16 + 4;  // row stride: 4 doubles of bank skew
-  }
-  int S = 4;
-  const size_t cap = smem_cap<K, C>();
-  for (; S >= 3; --S) {
-    layout<K, C>(pl, S);
-    if (pl.smem <= cap) break;
-  }
-  if (pl.smem > cap) return pl;  // ok = 0
-  const int maxcl = max_clusters<K, C>(cs, pl.smem);
-  const int64_t want = nrows > 0 ? (nrows + C::R - 1) / C::R : 1;
-  pl.ncl = (int)(want < maxcl ? want : maxcl);
-  if (pl.ncl < 1) pl.ncl = 1;
-  pl.ok = 1;
-  return pl;
 }
 
 template <int K>
 static Plan make_plan(int P, int64_t nrows) {
-  Plan none{};
+  Plan pl{};
+  if (P <= 64) {  // row split: the whole row in one CTA
+    pl.split = 1;
+    pl.cs = 1;
+    pl.R = kRR;
+    pl.wc = P;
+    pl.WS = pl.WQ = (P + 15) / 16 * 16 + 2;  // = 2 (mod 16): fragment loads spread over banks
+    int S = 4;
+    for (; S >= 2; --S) {
+      layout<K>(pl, S);
+      if (pl.smem <= cap_r<K>()) break;
+    }
+    if (pl.smem > cap_r<K>()) return Plan{};
+    const int64_t want = nrows > 0 ? (nrows + kRR - 1) / kRR : 1;
+    pl.ncl = (int)(want < sm_count() ? want : sm_count());
+    pl.ok = 1;
+    return pl;
+  }
   for (int cs : {1, 2, 4, 8}) {
     const int wc = ((P + cs - 1) / cs + 1) & ~1;
-    if (cs == 1 && wc <= 64) return plan_cfg<K, CfgB>(P, nrows, cs, 1);
-    if (wc <= 768) {
-      Plan pl = plan_cfg<K, CfgA>(P, nrows, cs, 0);
-      if (pl.ok) return pl;
+    if ((wc + 7) / 8 > kNW * kNMT) continue;  // > 768 columns per CTA
+    pl = Plan{};
+    pl.split = 0;
+    pl.cs = cs;
+    pl.R = kRA;
+    pl.wc = wc;
+    pl.WS = pl.WQ = (wc + 15) / 16 * 16 + 2;
+    int S = 4;
+    for (; S >= 3; --S) {
+      layout<K>(pl, S);
+      if (pl.smem <= cap_a<K>()) break;
     }
+    if (pl.smem > cap_a<K>()) continue;
+    const int maxcl = max_clusters<K>(cs, pl.smem);
+    const int64_t want = nrows > 0 ? (nrows + kRA - 1) / kRA : 1;
+    pl.ncl = (int)(want < maxcl ? want : maxcl);
+    if (pl.ncl < 1) pl.ncl = 1;
+    pl.ok = 1;
+    return pl;
   }
-  return none;
+  return Plan{};
+}
+
+static bool disabled() {
+  static const int off = getenv("SNX_TWO_PASS") != nullptr ? 1 : 0;  // A/B: snx_rowpass.cu
+  return off != 0;
 }
 
 static Plan plan_for(int dtype, int p, int K, int64_t nrows) {
-  Plan none{};
-  // A/B switch (work in progress: opt in with SNX_CLUSTER=1)
-  static const bool off = getenv("SNX_TWO_PASS") != nullptr || getenv("SNX_CLUSTER") == nullptr;
-  if (dtype != SNX_F64 || K < 1 || K > kMaxK || off) return none;
+  if (dtype != SNX_F64 || K < 1 || K > kMaxK || disabled()) return Plan{};
   const int P = padded(p);
   switch (K) {
 #define SNX_CL_K(KK) \
@@ -1000,19 +1081,14 @@ static Plan plan_for(int dtype, int p, int K, int64_t nrows) {
     SNX_CL_K(8) SNX_CL_K(9)
 #undef SNX_CL_K
     default:
-      return none;
+      return Plan{};
   }
 }
 
-template <int K, typename C>
-static int launch_main(const Plan &pl, Args &a, cudaStream_t st) {
-  auto kern = cluster_rowpass_kernel<K, C>;
-  if (!set_max_smem<K, C>()) return check_launch("cluster_rowpass attributes");
-  carveout(kern);
+static void fill(Args &a, const Plan &pl) {
   a.cs = pl.cs;
   a.ncl = pl.ncl;
   a.wc = pl.wc;
-  a.npi = pl.npi;
   a.S = pl.S;
   a.WS = pl.WS;
   a.WQ = pl.WQ;
@@ -1023,38 +1099,71 @@ static int launch_main(const Plan &pl, Args &a, cudaStream_t st) {
   a.o_vr = pl.o_vr;
   a.o_red = pl.o_red;
   a.o_bar = pl.o_bar;
+}
+
+template <int K>
+static int launch_k(const Plan &pl, Args &a, cudaStream_t st) {
+  fill(a, pl);
   cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (pl.split == 0) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = pl.cs;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (a.early) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.gridDim = dim3(pl.ncl * pl.cs);
-  cfg.blockDim = dim3(kNT);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = st;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = pl.cs;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = a.early ? 2 : 1;
+  cfg.numAttrs = na;
+  if (pl.split == 0) {
+    static bool attr = false;
+    auto kern = cluster_rowpass_kernel<K>;
+    if (!attr) {
+      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)cap_a<K>()) != cudaSuccess)
+        return check_launch("cluster_rowpass attributes");
+      attr = true;
+    }
+    carveout(kern);
+    cfg.blockDim = dim3(kNTA);
+    cudaLaunchKernelEx(&cfg, kern, a);
+    return check_launch("cluster_rowpass");
+  }
+  static bool attr = false;
+  auto kern = rowsplit_kernel<K>;
+  if (!attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)cap_r<K>()) != cudaSuccess)
+      return check_launch("rowsplit attributes");
+    attr = true;
+  }
+  carveout(kern);
+  cfg.blockDim = dim3(kNTR);
   cudaLaunchKernelEx(&cfg, kern, a);
-  return check_launch("cluster_rowpass");
+  return check_launch("rowsplit_rowpass");
 }
 
 static int launch_any(const Plan &pl, int K, Args &a, cudaStream_t st) {
-  int rc = 1;
   switch (K) {
-#define SNX_CL_K(KK)                                                                  \
-  case KK:                                                                            \
-    rc = pl.cfg == 0 ? launch_main<KK, CfgA>(pl, a, st) : launch_main<KK, CfgB>(pl, a, st); \
-    break;
+#define SNX_CL_K(KK) \
+  case KK:           \
+    return launch_k<KK>(pl, a, st);
     SNX_CL_K(1) SNX_CL_K(2) SNX_CL_K(3) SNX_CL_K(4) SNX_CL_K(5) SNX_CL_K(6) SNX_CL_K(7)
     SNX_CL_K(8) SNX_CL_K(9)
 #undef SNX_CL_K
     default:
-      set_error("snx: cluster row pass: K = %d unsupported", K);
+      set_error("snx: one-pass row pass: K = %d unsupported", K);
+      return 1;
   }
-  return rc;
 }
 
 // Workspace: [counters (shared with the two-pass layout) | gp[ncl][K*p] | lossp | corrp]
@@ -1086,6 +1195,17 @@ bool cluster_supported(int dtype, int32_t p, int32_t K) {
   return clp::plan_for(dtype, p, K, 1).ok != 0;
 }
 
+// The full-data objective + gradient pass takes the one-pass kernel where it
+// measured faster than the two GEMMs of snx_rowpass.cu: the row split (p <= 64).
+// The column split streams X from HBM once, but its row algebra (exp / log per
+// row) on the shared FP64 pipe makes it slower than the two-pass kernels at
+// MNIST / CIFAR shape (SNX_ONEPASS_GRAD=1 forces it, for A/B runs).
+bool cluster_grad_preferred(int dtype, int32_t p, int32_t K) {
+  static const bool force = getenv("SNX_ONEPASS_GRAD") != nullptr;
+  const clp::Plan pl = clp::plan_for(dtype, p, K, 1);
+  return pl.ok && (pl.split == 1 || force);
+}
+
 size_t cluster_ws_bytes(int dtype, int64_t nrows, int32_t p, int32_t K) {
   const clp::Plan pl = clp::plan_for(dtype, p, K, nrows);
   if (!pl.ok) return 0;
@@ -1103,12 +1223,12 @@ int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows,
   using namespace clp;
   const Plan pl = plan_for(SNX_F64, p, K, nrows);
   if (!pl.ok) {
-    set_error("snx: no cluster row-pass plan for p=%d K=%d", p, K);
+    set_error("snx: no one-pass row-pass plan for p=%d K=%d", p, K);
     return 1;
   }
   const ClWs cw = ws_layout(ws, pl, p, K);
   if (ws == nullptr || ws_bytes < cw.total) {
-    set_error("snx: workspace too small for the cluster row pass (%zu < %zu)", ws_bytes,
+    set_error("snx: workspace too small for the one-pass row pass (%zu < %zu)", ws_bytes,
               cw.total);
     return 1;
   }
@@ -1129,8 +1249,6 @@ int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows,
   a.corrp = cw.corrp;
   a.skip = skip;
   a.early = early;
-  // weight slices by TMA: every class row slice 16-B aligned, whole 16-B units
-  a.qbulk = (reinterpret_cast<uintptr_t>(w) % 16 == 0 && p % 2 == 0 && pl.wc % 2 == 0) ? 1 : 0;
   if (launch_any(pl, K, a, st)) return 1;
   if (mode == kPrep) return 0;
   const int64_t d = (int64_t)K * p;
@@ -1142,7 +1260,7 @@ int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows,
                 mode == kGrad ? (const double *)cw.lossp : nullptr,
                 mode == kGrad ? (const unsigned long long *)cw.corrp : nullptr,
                 mode == kGrad ? loss_out : nullptr, corr_out);
-  return check_launch("cluster finalize");
+  return check_launch("one-pass finalize");
 }
 
 }  // namespace snx

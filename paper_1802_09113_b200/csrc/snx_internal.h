@@ -91,6 +91,7 @@ inline void carveout(F *kernel) {
 // one-pass fp64 row pass on thread-block clusters (snx_cluster.cu)
 size_t rowpass_counter_bytes();  // the zero-at-rest counter block at workspace offset 0
 bool cluster_supported(int dtype, int32_t p, int32_t K);
+bool cluster_grad_preferred(int dtype, int32_t p, int32_t K);
 size_t cluster_ws_bytes(int dtype, int64_t nrows, int32_t p, int32_t K);
 int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
                     int32_t p, int32_t K, const int32_t *labels, const double *w,

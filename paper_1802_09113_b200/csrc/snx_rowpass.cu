@@ -1805,8 +1805,9 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   double *dotp = reinterpret_cast<double *>(wsb + lay.dot_part);
 
   // fp64, K <= 9: the one-pass cluster kernel (X streamed once per product)
-  if (nrows > 0 && cg == nullptr && (mode == kGradient || mode == kHessApply) &&
-      cluster_supported(dtype, p, K)) {
+  if (nrows > 0 && cg == nullptr &&
+      ((mode == kHessApply && cluster_supported(dtype, p, K)) ||
+       (mode == kGradient && cluster_grad_preferred(dtype, p, K)))) {
     if (mode == kGradient && out != nullptr &&
         launch_prep_weights(dtype, w, nullptr, 0.0, K, p, P, nullptr, dotp, counters + 15,
                             out + 1, st))

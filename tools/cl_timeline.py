@@ -3,11 +3,11 @@
     python -c "from paper_1802_09113_b200 import _build; _build.build_timeline('tools/libsnx_cltl.so', ['-DSNX_CL_TIMELINE'])"
     SNX_LIB=tools/libsnx_cltl.so python tools/cl_timeline.py [cifar|mnist|covertype]
 
-Events per block (consumer thread 0): 0 loop top, 1 row algebra done (after
-waiting for the peers' partial logits), 2 V phase of the next block done,
-3 after the CTA barrier, 4 partials sent, 5 X^T U done; producer: 6 X
-issued, 7 side data issued.  Kernel row (-1): 0 entry, 1 Q loaded, 2 first V
-sent, 3 loop end, 4 epilogue done, 5 exit."""
+Events per block, compute thread 0: 0 loop top, 1 next block's V done,
+2 U(b) ready (waited), 3 X^T U(b) done; exchange-warp lane 0: 6 warp partials
+ready, 7 sent to the peers, 8 peers' partials in, 9 U rows written.  Kernel
+row (-1): 0 entry, 1 weights loaded, 2 first V done, 3 loop end, 4 partial
+written, 5 exit."""
 import ctypes
 import os
 import sys
@@ -32,11 +32,21 @@ orc = snx.SubsampledOracle(snx.SoftmaxProblem(ds, 1e-3), snx.SampleConfig(1.0, 0
 g, _ = orc.gradient_device(x)
 op = orc.hessian_operator(x)
 out = torch.empty_like(g)
+mode = sys.argv[2] if len(sys.argv) > 2 else "b2b"
+st = torch.cuda.current_stream()
+e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for _ in range(5):
     op.apply_into(g, out)
 torch.cuda.synchronize()
-op.apply_into(g, out)
+e0.record(st)
+for _ in range(20):
+    op.apply_into(g, out)
+e1.record(st)
 torch.cuda.synchronize()
+print(f"20 back-to-back products: {e0.elapsed_time(e1) / 20 * 1e3:.1f} us each (events)")
+if mode == "sync":  # the stamps below: one product on an idle GPU
+    op.apply_into(g, out)
+    torch.cuda.synchronize()
 NB = 26
 buf = (ctypes.c_ulonglong * (160 * NB * 10))()
 _lib.load().snx_debug_cl_timeline(buf)
@@ -46,26 +56,28 @@ if not used:
     sys.exit(f'{name}: no stamps (kernel not used for this shape?)')
 t0 = min(t[c, 0, 0] for c in used)
 rel = lambda v: (v - t0) / 1e3 if v else float("nan")  # noqa: E731
-print(f"{name}: {len(used)} CTAs; kernel rows: entry / Q loaded / first V sent / loop end / epi / exit (us)")
+print(f"{name}: {len(used)} CTAs; kernel rows: entry / Q loaded / first V / loop end / partial out / exit (us)")
 for c in used[:6] + used[-2:]:
     print(f"cta {c:3d}: " + " ".join(f"{rel(t[c, 0, e]):7.2f}" for e in range(6)))
-print("per block (cta 0): top / rowalg / vphase / sync / vsend / xtu | V in / armed / z summed / rows done")
+print("per block (cta 0): compute top / V(b+1) done / U(b) ready / XtU done | xchg red in / sent / peers in / U out")
 for b in range(NB - 1):
     if t[used[0], b + 1, 0] == 0 or t[used[0], b + 1, 0] < t0:
         break
     r = t[used[0], b + 1]
-    print(f"b{b:2d}: " + " ".join(f"{rel(r[e]):7.2f}" for e in range(6)) + " | " +
-          " ".join(f"{rel(r[e]):7.2f}" for e in (6, 8, 7, 9)))
+    print(f"b{b:2d}: " + " ".join(f"{rel(r[e]):7.2f}" for e in range(4)) + " | " +
+          " ".join(f"{rel(r[e]):7.2f}" for e in (6, 7, 8, 9)))
 # medians of the phase durations over CTAs and blocks
-d = {k: [] for k in ("rowalg", "vphase", "sync", "vsend", "xtu")}
+d = {k: [] for k in ("vphase", "u_wait", "xtu", "xchg_send", "xchg_peers", "xchg_rows")}
 for c in used:
     for b in range(NB - 1):
         r = t[c, b + 1]
-        if r[0] == 0 or r[5] == 0:
+        if r[0] == 0 or r[3] == 0 or r[0] < t0:
             continue
-        d["rowalg"].append(r[1] - r[0])
-        d["vphase"].append(r[2] - r[1])
-        d["sync"].append(r[3] - r[2])
-        d["vsend"].append(r[4] - r[3])
-        d["xtu"].append(r[5] - r[4])
+        d["vphase"].append(r[1] - r[0])
+        d["u_wait"].append(r[2] - r[1])
+        d["xtu"].append(r[3] - r[2])
+        if r[9] > 0:
+            d["xchg_send"].append(r[7] - r[6])
+            d["xchg_peers"].append(r[8] - r[7])
+            d["xchg_rows"].append(r[9] - r[8])
 print("median phase us: " + ", ".join(f"{k} {np.median(v) / 1e3:.3f}" for k, v in d.items() if v))
