@@ -88,20 +88,32 @@ def load_libsvm(path, n_classes, n_features=None, storage="auto", dtype="f64"):
     return _to_device(csr, labels, n_classes, storage, dtype)
 
 
+def parse_csv(path, n_classes):
+    """Host part of load_csv (dataset.py:298-311): (features n x p, 0-based
+    labels); the empty table gives a 0 x 0 matrix; ParseError on malformed
+    text, DataError on more distinct labels than classes."""
+    import warnings
+
+    with warnings.catch_warnings():  # numpy warns on an empty file; the reference too
+        warnings.simplefilter("ignore", UserWarning)
+        try:
+            table = np.loadtxt(path, delimiter=",", dtype=np.float64, ndmin=2)
+        except ValueError as exc:
+            raise ParseError(str(exc)) from None
+    if table.size == 0:
+        return np.zeros((0, 0)), np.zeros(0, dtype=np.int64)
+    return table[:, :-1], remap_labels(table[:, -1], n_classes)
+
+
 def load_csv(path, n_classes, storage="dense", dtype="f64"):
-    """Dense CSV, last column = label (dataset.py:296-311)."""
+    """Dense CSV, last column = label (dataset.py:296-311) -> device dataset."""
     import scipy.sparse as sp
 
-    try:
-        table = np.loadtxt(path, delimiter=",", dtype=np.float64, ndmin=2)
-    except ValueError as exc:
-        raise ParseError(str(exc)) from None
-    if table.size == 0:
-        return DeviceDataset.from_numpy(np.zeros((0, 0)), np.zeros(0, dtype=np.int64), n_classes,
-                                        dtype=dtype)
-    labels = remap_labels(table[:, -1], n_classes)
-    return _to_device(sp.csr_array(table[:, :-1]), labels, n_classes, storage, dtype)
+    features, labels = parse_csv(path, n_classes)
+    if features.size == 0 and len(labels) == 0:
+        return DeviceDataset.from_numpy(features, labels, n_classes, dtype=dtype)
+    return _to_device(sp.csr_array(features), labels, n_classes, storage, dtype)
 
 
-__all__ = ["load_libsvm", "load_csv", "read_libsvm", "parse_libsvm", "picks_dense",
-           "remap_labels"]
+__all__ = ["load_libsvm", "load_csv", "read_libsvm", "parse_libsvm", "parse_csv",
+           "picks_dense", "remap_labels"]

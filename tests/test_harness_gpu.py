@@ -1,0 +1,106 @@
+"""The experiment harness end to end on the GPU solver:
+load_csv onto the device, and a Newton-only run_experiment (LIBSVM load ->
+device normalise -> split -> newton_solve -> trace + summary CSVs) against the
+CSVs the unmodified reference wrote for the same spec (bench.py:270-311,
+tests/test_bench.py:74-136).  Structure, ints, accuracies, step sizes, CG
+counts and termination must match exactly; objectives to 1e-10 (our fp64
+sums run in a different order); timing columns are skipped."""
+
+import csv
+import io as pyio
+import os
+import tempfile
+from dataclasses import dataclass, field
+
+import numpy as np
+import pytest
+
+import paper_1802_09113_b200 as snx
+from conftest import GOLDEN, load_golden
+from paper_1802_09113_b200 import harness
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def g():
+    return load_golden("harness_golden.npz")
+
+
+@dataclass
+class SolverRun:  # the reference's bench.SolverRun fields (bench.py:54-69)
+    method: str
+    learning_rate: object = None
+    batch_size: float = 128
+    epochs: int = 100
+    cg_tol: float = 1e-4
+    cg_max_iters: int = 10
+    epsilon: float = 1e-8
+    seed: int = 0
+
+
+@dataclass
+class ExperimentSpec:  # bench.py:72-92
+    dataset_path: str
+    fmt: str = "libsvm"
+    n_classes: int = 2
+    solvers: list = field(default_factory=list)
+    normalize: bool = True
+    split_fraction: float = 0.8
+    seed: int = 0
+    lam: float = 1e-3
+    out_dir: str = "."
+    target_accuracy: float = None
+    figures: bool = True
+    lipschitz_iters: int = 200
+    n_features: int = None
+
+
+def rows_of(b):
+    return list(csv.reader(pyio.StringIO(b.decode() if isinstance(b, bytes) else b)))
+
+
+def same_rows(ours, ref, float_cols, skip_cols):
+    assert len(ours) == len(ref)
+    assert ours[0] == ref[0]
+    for ro, rr in zip(ours[1:], ref[1:]):
+        for j, (a, b) in enumerate(zip(ro, rr)):
+            col = ref[0][j]
+            if col in skip_cols:
+                continue
+            if col in float_cols and a != b:
+                fa, fb = float(a), float(b)
+                assert abs(fa - fb) <= 1e-10 * max(abs(fb), 1.0), (col, a, b)
+            else:
+                assert a == b, (col, a, b)
+
+
+def test_run_experiment_matches_reference(g, cuda_ok):
+    spec = ExperimentSpec(
+        dataset_path=os.path.join(GOLDEN, "libsvm", "experiment.svm"), n_classes=3,
+        solvers=[SolverRun(method="subnewton-20", epochs=6, seed=11),
+                 SolverRun(method="full-newton", epochs=4),
+                 SolverRun(method="subnewton-100", epochs=5, seed=3)],
+        figures=False, target_accuracy=0.5)
+    with tempfile.TemporaryDirectory() as td:
+        spec.out_dir = td
+        res = harness.run_experiment(spec)
+        assert len(res.runs) == 3
+        for i, r in enumerate(res.runs):
+            assert r.label == str(g[f"exp_trace{i}_label"])
+            with open(r.trace_path, "rb") as fh:
+                same_rows(rows_of(fh.read()), rows_of(bytes(g[f"exp_trace{i}_bytes"])),
+                          {"objective"}, {"cum_seconds"})
+        with open(res.summary_path, "rb") as fh:
+            same_rows(rows_of(fh.read()), rows_of(bytes(g["exp_summary_bytes"])),
+                      {"final_objective"}, {"time_to_target_seconds"})
+
+
+def test_load_csv_on_device(g, cuda_ok):
+    for name in ("basic", "raw_labels", "single_row"):
+        ds = snx.load_csv(os.path.join(GOLDEN, "csv", name + ".csv"), int(g[f"csv_{name}_C"]))
+        X = ds.X[:, :ds.n_features].cpu().numpy()
+        assert np.array_equal(X, g[f"csv_{name}_X"])
+        assert np.array_equal(ds.labels.cpu().numpy(), g[f"csv_{name}_y"])
+    empty = snx.load_csv(os.path.join(GOLDEN, "csv", "empty.csv"), 3)
+    assert empty.n_rows == 0 and empty.n_features == 0
