@@ -1,15 +1,23 @@
 """Benchmark: sub-sampled Hessian-vector products/s at CIFAR-10 shape
 (BASELINE.json metric; configs[2]: 50k x 3072, C=10, 5% Hessian sample).
 
-One step = one outer iteration's sampled-Hessian work on fresh inputs:
-snx_hess_prepare on a new S_H (rows gathered from the 1.23 GB X in HBM) and a
-device CG solve (theta=1e-4, <=10 Hessian products, reference cg.py).
-value = Hessian products applied / device time.  Also reported: e2e through
-the public numpy API (host buffers, H2D/D2H in the timed region), the
-roofline of the Hessian product, a CPU baseline (the oracle port on this
-host), and time-to-tolerance of a full newton_solve.
+One step = one outer iteration's sampled-Hessian work on fresh inputs: the
+step's S_H indices uploaded (pinned H2D inside the timed region), the Hessian
+operator prepared on them (gather fused into the one-pass kernel) and a device
+CG solve (theta=1e-4, <=10 Hessian products, reference cg.py), all device
+resident.  value = Hessian products applied / device time.  Also reported:
+e2e through the public numpy API (host buffers, H2D/D2H in the timed
+region), the roofline of the Hessian product, the CG kernels' GB/s, a CPU
+baseline (the oracle port on this host), time-to-tolerance per SURVEY 8(d)
+(planted-softmax labels, eps = 1e-6 |grad F(0)|, 100-iteration cap, the CPU
+port run to the same tolerance), the trust-region config #4, and the other
+BASELINE shapes.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+With --gpus N > 1 and no torchrun environment the script re-launches itself
+under torch.distributed.run with N ranks (one per GPU, NCCL); rows are then
+sharded over the ranks (strong scaling of the CIFAR problem).
 """
 
 import argparse
@@ -17,6 +25,7 @@ import json
 import math
 from dataclasses import replace
 import os
+import socket
 import subprocess
 import sys
 import threading
@@ -31,6 +40,12 @@ N, P, C = 50000, 3072, 10
 F_H, LAM, THETA, T_CG = 0.05, 1e-3, 1e-4, 10
 METRIC = "subsampled Hessian-vector products/s (CIFAR-10 shape, 5% sample)"
 UNIT = "Hv/s"
+# the workload both arms run (printed identically by both)
+CONFIG = {"workload": "cifar10-shape 50000x3072 C=10, 5% S_H (m=2500) per step: S_H gather + "
+                      "h-prep + CG (theta=1e-4, <=10 Hv)",
+          "n": N, "p": P, "C": C, "hessian_fraction": F_H, "lam": LAM, "theta": THETA,
+          "cg_max_iters": T_CG, "data": "N(0,1) features, unit-norm columns, uniform labels",
+          "l2": "inputs > L2: 1.23 GB X in HBM, fresh S_H gathered every step"}
 
 
 def peaks():
@@ -88,9 +103,14 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
-# dram__bytes_read.sum + dram__bytes_write.sum of one Hessian product's two GEMM
-# kernels, from the committed ncu --set full capture (per launch, cold cache)
-TRAFFIC = {"f64": 61.913088e6 + 0.429568e6 + 61.913344e6 + 0.436992e6}
+# dram__bytes_read.sum + dram__bytes_write.sum of one Hessian product (the
+# one-pass kernel + its finalize), from the committed ncu --set full capture
+# (per launch, cold cache); None until profiled
+TRAFFIC = {"f64": None}
+TRAFFIC_SOURCE = "profiles/r02_onepass_ncu_full.txt"
+KERNEL_NAME = {"f64": "one-pass cluster row pass (cluster_rowpass_kernel<9> + finalize_kernel, "
+                      "csrc/snx_cluster.cu)",
+               "f32": "tcgen05 tc_gemm1 + tc_gemm2 (csrc/snx_tc.cu)"}
 
 
 def synthetic_problem(n, p, nC, seed=0, normalize=True, ill_conditioned=False):
@@ -174,8 +194,8 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": "cifar10-shape 50000x3072 C=10, 5% S_H",
-                                        "n": N, "p": P, "C": C, "hessian_fraction": F_H},
+        "data": "synthetic", "config": CONFIG,
+        "parallelism": f"host CPU, {os.cpu_count()} threads (numpy/OpenBLAS), rank 0 only",
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": os.cpu_count(), "kind": "port",
                          "sample": f"{args.steps} steps, oracle port (numpy/OpenBLAS fp64)"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -376,21 +396,167 @@ def secondary(snx, torch, args):
     res, _, _, _ = large_shard.measure(1_000_000, 10, solve_iters=5)
     out["large_c100_shard_f32"] = res
     torch.cuda.empty_cache()
-    # BASELINE config #4: trust region (Steihaug-CG), ill-conditioned CIFAR shape, 10% S_H
+    return out
+
+
+def planted_problem(n, p, nC, seed=0, scale=3.0):
+    """Planted-softmax labels (SURVEY 8(d) time-to-tolerance): unit-norm N(0,1)
+    columns, labels drawn from softmax(A W*) with W* ~ scale * N(0,1), so the
+    regularised solve has a meaningful optimum (tools/tol_probe.py)."""
+    gen = np.random.default_rng(seed)
+    A = gen.standard_normal((n, p))
+    A /= np.sqrt((A ** 2).sum(axis=0))
+    W = gen.standard_normal((p, nC)) * scale
+    Z = A @ W
+    Z -= Z.max(axis=1, keepdims=True)
+    Pr = np.exp(Z)
+    Pr /= Pr.sum(axis=1, keepdims=True)
+    u = gen.random(n)[:, None]
+    y = (Pr.cumsum(axis=1) < u).sum(axis=1).clip(0, nC - 1)
+    return np.ascontiguousarray(A), y.astype(np.int64)
+
+
+def time_to_tolerance(snx, torch, rank, world, skip_cpu):
+    """SURVEY 8(d) metric 2: newton_solve from x0 = 0 until |grad| < 1e-6 |grad F(0)|
+    (100-iteration cap) on planted labels at CIFAR shape, the reference's timed
+    region (newton.py:72-104: objective / accuracy passes included); the oracle
+    port runs the same solve on the host (all threads, and a 1-thread sample)."""
+    from paper_1802_09113_b200 import softmax
+    from paper_1802_09113_b200.device import dot
+
+    A, y = planted_problem(N, P, C)
+    ds = snx.DeviceDataset.from_numpy(A, y, C)
+    prob = snx.SoftmaxProblem(ds, LAM)
+    x0 = torch.zeros((C - 1) * P, dtype=torch.float64, device="cuda")
+    gz = softmax.gradient_parts(ds, x0, 1.0, LAM)[0]
+    g0 = math.sqrt(float(dot(gz, gz)))
+    eps = 1e-6 * g0
+    out = {"workload": "cifar10-shape 50000x3072 C=10, planted-softmax labels (scale 3), "
+                       "lam=1e-3, x0=0", "epsilon": eps, "epsilon_rel_to_grad0": 1e-6,
+           "max_outer_iters": 100}
+    for name, variant in (("subsampled_100", "subsampled-100"), ("full_newton", "full")):
+        ncfg = snx.make_variant(variant, snx.NewtonConfig(epsilon=eps, max_outer_iters=100))
+        # warm-up: one outer iteration captures this variant's CUDA graphs
+        snx.newton_solve(prob, replace(ncfg, max_outer_iters=1), x0=x0.clone())
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        tr = snx.newton_solve(prob, ncfg, x0=x0.clone())
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+        out[name] = {"time_to_tol_s": dt, "outer_iters": tr.iterations,
+                     "ms_per_outer_iter": 1e3 * dt / max(tr.iterations, 1), "reason": tr.reason,
+                     "final_objective": tr.final_objective,
+                     "cg_iters": [r.cg_iters for r in tr.records[1:]],
+                     "alphas": sorted({r.step_size for r in tr.records[1:]})}
+    del ds, prob
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not skip_cpu:
+        import oracle
+        from threadpoolctl import threadpool_limits
+
+        cpu = {"cores": os.cpu_count(), "kind": "port",
+               "note": "oracle port (numpy/OpenBLAS fp64, the reference's arithmetic) on this "
+                       "host, same problem, same epsilon and cap"}
+        for name, variant in (("subsampled_100", "subsampled-100"), ("full_newton", "full")):
+            t0 = time.perf_counter()
+            ref = oracle.newton_solve(A, y, C, LAM, variant, epsilon=eps, max_outer_iters=100)
+            dt = time.perf_counter() - t0
+            it = len(ref["records"]) - 1
+            cpu[name] = {"time_to_tol_s": dt, "outer_iters": it, "reason": ref["reason"],
+                         "final_objective": ref["records"][-1][1],
+                         "gpu_speedup": dt / out[name]["time_to_tol_s"]}
+            with threadpool_limits(limits=1):  # 1-thread row: a 2-iteration sample
+                t0 = time.perf_counter()
+                oracle.newton_solve(A, y, C, LAM, variant, epsilon=eps, max_outer_iters=2)
+                per = (time.perf_counter() - t0) / 2
+            cpu[name]["one_thread_s_per_outer_iter"] = per
+            cpu[name]["one_thread_time_to_tol_s_extrapolated"] = per * it
+        out["cpu_port"] = cpu
+    return out
+
+
+def trust_region_config4(snx, torch, rank, world, skip_cpu):
+    """BASELINE config #4: TR Steihaug-CG, ill-conditioned CIFAR shape
+    (logspace(2,-4,p) columns), 10% S_H, eps = 1e-6 |grad F(0)|, 100-iteration
+    cap; the CPU restatement (oracle/trust_region.py) timed on a bounded sample."""
+    from paper_1802_09113_b200 import softmax
+    from paper_1802_09113_b200.device import dot
+
     A, y = synthetic_problem(N, P, C, seed=0, normalize=False, ill_conditioned=True)
-    prob = snx.SoftmaxProblem(snx.DeviceDataset.from_numpy(A, y, C), LAM)
-    cfg = snx.TrustRegionConfig(max_outer_iters=20)
+    ds = snx.DeviceDataset.from_numpy(A, y, C)
+    prob = snx.SoftmaxProblem(ds, LAM)
+    x0 = torch.zeros((C - 1) * P, dtype=torch.float64, device="cuda")
+    gz = softmax.gradient_parts(ds, x0, 1.0, LAM)[0]
+    eps = 1e-6 * math.sqrt(float(dot(gz, gz)))
+    cfg = snx.TrustRegionConfig(epsilon=eps, max_outer_iters=100)
     snx.trust_region_solve(prob, snx.TrustRegionConfig(max_outer_iters=2))  # warm-up
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     tr = snx.trust_region_solve(prob, cfg)
     torch.cuda.synchronize()
-    out["trust_region_cifar10_illcond"] = {
-        "seconds": time.perf_counter() - t0, "outer_iters": tr.iterations, "reason": tr.reason,
-        "final_objective": tr.final_objective, "hessian_fraction": 0.1,
-        "workload": "cifar10-shape ill-conditioned (logspace(2,-4,p) columns), TR Steihaug-CG, "
-                    "<= 20 outer iterations"}
-    return out
+    dt = time.perf_counter() - t0
+    res = {"time_to_tol_s": dt, "outer_iters": tr.iterations, "reason": tr.reason,
+           "ms_per_outer_iter": 1e3 * dt / max(tr.iterations, 1),
+           "final_objective": tr.final_objective, "epsilon": eps, "hessian_fraction": 0.1,
+           "workload": "cifar10-shape ill-conditioned (logspace(2,-4,p) columns), TR "
+                       "Steihaug-CG, eps = 1e-6 |grad F(0)|, <= 100 outer iterations"}
+    del ds, prob
+    torch.cuda.empty_cache()
+    if rank == 0 and world == 1 and not skip_cpu:
+        import oracle
+
+        k = 3
+        t0 = time.perf_counter()
+        oracle.trust_region_solve(A, y, C, LAM, oracle.TrustRegionConfig(
+            epsilon=eps, max_outer_iters=k), hessian_fraction=0.1)
+        per = (time.perf_counter() - t0) / k
+        res["cpu_port"] = {"s_per_outer_iter": per, "sample_outer_iters": k,
+                           "time_to_tol_s_extrapolated": per * tr.iterations,
+                           "cores": os.cpu_count(), "kind": "port (restatement; parity unpinned)"}
+    return res
+
+
+def cg_kernel_rate(torch, ws, d, reps=50):
+    """Achieved GB/s of the CG vector kernels (snx_cg_update = cg_step1 + cg_step2,
+    cg.py:77-96): d-vector bytes per update (step1 reads p s r Hs, writes p r;
+    step2 reads r s p, writes s pb) over their CUDA-event time."""
+    from paper_1802_09113_b200 import _lib
+    from paper_1802_09113_b200.device import ptr, stream_handle
+
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    state = ws.state.clone()
+    state[2::_lib.CG_SLOT] = 0.0  # clear the done flags: every update does its work
+
+    def upd():
+        _lib.call("snx_cg_update", 0, ws.T, d, ptr(ws.Hs), ptr(ws.dots), ptr(ws.r), ptr(ws.s),
+                  ptr(ws.p), ptr(ws.pb), ptr(state), stream_handle())
+
+    # the updates captured in a CUDA graph (as in the CG solve): kernel time,
+    # not the host's ctypes launch rate
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        for _ in range(3):
+            upd()
+    torch.cuda.current_stream().wait_stream(side)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _ in range(reps):
+            upd()
+    graph.replay()
+    torch.cuda.synchronize()
+    e0.record(st)
+    graph.replay()
+    e1.record(st)
+    torch.cuda.synchronize()
+    us = e0.elapsed_time(e1) / reps * 1e3
+    nbytes = 11 * d * 8
+    return {"us_per_update": us, "bytes_per_update": nbytes,
+            "achieved_gb_s": nbytes / (us * 1e-6) / 1e9,
+            "note": "graph-replayed; latency-bound at d = 27648 (2 kernels of 256 fixed "
+                    "blocks, SURVEY 8(d)): the 2.4 MB move in well under a microsecond at HBM "
+                    "speed"}
 
 
 def run_ours(args):
@@ -398,16 +564,17 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1802_09113_b200 as snx
-    from paper_1802_09113_b200 import _lib, cg as cgmod, softmax
-    from paper_1802_09113_b200.device import ptr, stream_handle
+    from paper_1802_09113_b200 import cg as cgmod, softmax
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl")
-    # the row-sharded code path (NCCL all-reduce per product); SNX_BENCH_SHARDED=1
+        dist.init_process_group(os.environ.get("SNX_BENCH_BACKEND", "nccl"))
+    # the row-sharded code path (one all-reduce per product); SNX_BENCH_SHARDED=1
     # runs it at world size 1 too (all-reduce = identity) to exercise it on one GPU
     sharded = world > 1 or os.environ.get("SNX_BENCH_SHARDED") == "1"
 
@@ -418,17 +585,19 @@ def run_ours(args):
     total = args.warmup + args.steps
     samples = snx.SampleConfig(1.0, F_H)
     iters = torch.zeros(total, dtype=torch.float64, device=dev)
+    # each step's S_H is drawn on the host up front (numpy, as the reference);
+    # its upload to the device happens inside the step (timed)
+    s_h = [snx.draw_samples(samples, N, k)[1] for k in range(total)]
     if not sharded:
         ds = snx.DeviceDataset.from_numpy(A, y, C, dtype=args.dtype)
         prob = snx.SoftmaxProblem(ds, LAM)
         g, _ = softmax.gradient_parts(ds, x, 1.0, LAM)
-        # inputs of every step (fresh S_H per step) resident before timing
-        views = [ds.take(snx.draw_samples(samples, N, k)[1]) for k in range(total)]
-        m = views[0].n_rows
+        m = len(s_h[0])
         ops = [None]
 
         def step(k):
-            op = softmax.HessianOperator(views[k], x, LAM, scale=N / m)
+            view = ds.take(s_h[k])  # pinned H2D copy of the indices
+            op = softmax.HessianOperator(view, x, LAM, scale=N / m)
             ops[0] = op  # keep only the latest operator alive
             ws = cgmod.cg_graph_for(op, T_CG, THETA).run(g)  # CUDA-graph replay of the CG loop
             iters[k:k + 1].copy_(ws.slot(T_CG)[3:4])
@@ -439,14 +608,13 @@ def run_ours(args):
         sp = sd.ShardedProblem.from_global(A, y, C, LAM, dtype=args.dtype)
         ds = sp.local
         prob = None
-        oracles = [sd.ShardedOracle(sp, samples, k) for k in range(total)]
-        g = oracles[0].gradient_device(x)
-        m = len(oracles[0].s_h)
+        g = sd.ShardedOracle(sp, samples, 0).gradient_device(x)
+        m = len(s_h[0])
         cgws = cgmod.CgWorkspace(ds.dim, T_CG, dev)
         ops = [None]
 
         def step(k):
-            op = oracles[k].hessian_operator(x)
+            op = sd.ShardedOracle(sp, samples, k).hessian_operator(x)
             ops[0] = op
             cgmod.enqueue_cg(op, g, THETA, T_CG, cgws)
             iters[k:k + 1].copy_(cgws.slot(T_CG)[3:4])
@@ -460,12 +628,6 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
-        prof = None
-        if os.environ.get("SNX_BENCH_PROFILE"):
-            import cProfile
-
-            prof = cProfile.Profile()
-            prof.enable()
         e0.record(st)
         h0 = time.perf_counter()
         for k in range(args.warmup, total):
@@ -473,11 +635,6 @@ def run_ours(args):
         host_ms = (time.perf_counter() - h0) * 1e3
         e1.record(st)
         torch.cuda.synchronize()
-        if prof is not None:
-            import pstats
-
-            prof.disable()
-            pstats.Stats(prof, stream=sys.stderr).sort_stats("cumulative").print_stats(25)
     ms = e0.elapsed_time(e1)
     if world > 1:
         t = torch.tensor([ms], device=dev)
@@ -486,7 +643,7 @@ def run_ours(args):
     hv_count = int(iters[args.warmup:].sum())
     value = hv_count / (ms / 1e3)
 
-    # ---- roofline of the dominant op: one Hessian product (snx_hess_apply)
+    # ---- roofline of the dominant op: one Hessian product
     op = ops[0]
     v = g.clone()
     out = torch.empty_like(v)
@@ -504,30 +661,30 @@ def run_ours(args):
     torch.cuda.synchronize()
     hv_ms = ev[0].elapsed_time(ev[1]) / reps
     tb = 8 if args.dtype == "f64" else 4
-    m = op.view.n_rows  # rows this GPU streams per product
-    alg_bytes = m * P * tb + m * (C - 1) * tb + 2 * ds.dim * 8
+    m_loc = op.view.n_rows  # rows this GPU streams per product
+    alg_bytes = m_loc * P * tb + m_loc * (C - 1) * tb + 2 * ds.dim * 8
     pk, pk_kind = peaks()
     achieved = alg_bytes / (hv_ms / 1e3) / 1e9
+    flops = 4 * m_loc * P * (C - 1)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": achieved / pk["hbm_gbs"], "traffic": TRAFFIC.get(args.dtype),
-                "traffic_source": "profiles/r01_hv_gemms_ncu_full.txt: dram read+write of gemm1+gemm2 "
-                                  "per product, ncu cold cache (X_S read once per GEMM)",
-                "kernel": "snx_hess_apply (rowpass GEMM1+ComputeU, xtu GEMM2, finalize)",
-                "peak_kind": pk_kind, "ms_per_launch": hv_ms,
-                "flops_per_launch": 4 * m * P * (C - 1),
-                "note": "X_S rows re-read from L2 across CG iterations; bytes counted once",
-                # the same launch against the other ceilings it could hit (B200
-                # microbenchmarks in profiles/r01_microbench.txt): X_S read twice
-                # from L2 per product, and the FP64 FMA pipe
-                "alt_bounds": {
-                    "l2_read_gb_s": 2 * m * P * tb / (hv_ms / 1e3) / 1e9,
-                    "l2_read_peak_gb_s": 18037.0,
-                    "fp64_tflops": 4 * m * P * (C - 1) / (hv_ms / 1e3) / 1e12,
-                    "fp64_peak_tflops": 36.0}}
+                "traffic_source": TRAFFIC_SOURCE,
+                "kernel": KERNEL_NAME.get(args.dtype), "peak_kind": pk_kind,
+                "ms_per_launch": hv_ms, "bytes_per_launch": alg_bytes,
+                "flops_per_launch": flops,
+                "note": "algorithmic bytes: X_S read once + h + v + Hv (SURVEY 8(d)); in the "
+                        "CG loop the sample rows are re-read from L2/HBM every product",
+                # the same launch against the ceiling it is closest to: the fp64
+                # tensor / FMA pipe (36.5 TFLOP/s measured, profiles/r02_fp64_pipe.txt)
+                "alt_bounds": {"fp64_tflops": flops / (hv_ms / 1e3) / 1e12,
+                               "fp64_peak_tflops": 36.5,
+                               "fp64_frac": flops / (hv_ms / 1e3) / 1e12 / 36.5}}
+    cg_rate = None
+    if not sharded:
+        wsx = cgmod.cg_graph_for(ops[0], T_CG, THETA).ws
+        cg_rate = cg_kernel_rate(torch, wsx, ds.dim)
 
     # ---- e2e: the public numpy API, host buffers in and out
-    if sharded:
-        args.skip_solve = True
     g_host = g.cpu().numpy()
     cfg = snx.CgConfig(THETA, T_CG)
     e2e_steps = max(10, min(args.steps, 50))
@@ -547,51 +704,21 @@ def run_ours(args):
     for k in range(e2e_steps):
         e2e_hv += e2e_step(500 + k)
     e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t)
     e2e = {"value": e2e_hv / e2e_s, "unit": UNIT,
            "h2d_bytes_per_step": 2 * ds.dim * 8 + m * 8,
-           "d2h_bytes_per_step": ds.dim * 8 + 8 * 8}
+           "d2h_bytes_per_step": ds.dim * 8 + 8 * 8,
+           "note": "public numpy API: SubsampledOracle + hessian_operator + cg_solve per step"}
 
-    # ---- time-to-tolerance of Newton solves (device resident, reference timed region:
-    # newton.py:72-104 incl. objective / accuracy passes).  On this synthetic problem
-    # the 5%-Hessian method (BASELINE config) reaches eps = 1e-2 |grad F(0)| (it
-    # stalls before 1e-3); full Newton reaches 1e-6 in a few iterations.
-    solve = None
-    if not args.skip_solve:
-        from paper_1802_09113_b200.device import dot
-
-        gz = softmax.gradient_parts(ds, torch.zeros_like(x), 1.0, LAM)[0]
-        g0 = math.sqrt(float(dot(gz, gz)))
-        solve = {}
-        for name, variant, rel, cap in (("subsampled_100", "subsampled-100", 1e-2, 400),
-                                        ("full_newton", "full", 1e-6, 50)):
-            ncfg = snx.make_variant(variant, snx.NewtonConfig(epsilon=rel * g0,
-                                                              max_outer_iters=cap))
-            # warm-up: one outer iteration captures the CUDA graphs of this
-            # variant's sample size (a one-time cost per dataset and size)
-            snx.newton_solve(prob, replace(ncfg, max_outer_iters=1), x0=torch.zeros_like(x))
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            tr = snx.newton_solve(prob, ncfg, x0=torch.zeros_like(x))
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
-            solve[name] = {"time_to_tol_s": dt, "outer_iters": tr.iterations,
-                           "ms_per_outer_iter": 1e3 * dt / max(tr.iterations, 1),
-                           "reason": tr.reason, "final_objective": tr.final_objective,
-                           "epsilon": rel * g0, "epsilon_rel_to_grad0": rel,
-                           "cg_iters_total": int(sum(r.cg_iters for r in tr.records[1:]))}
-        if rank == 0 and world == 1 and not args.skip_cpu:
-            # the oracle port's Newton iteration on the same problem (2 iterations,
-            # extrapolated to the GPU's iteration count)
-            import oracle
-
-            t0 = time.perf_counter()
-            oracle.newton_solve(A, y, C, LAM, "subsampled-100", max_outer_iters=2)
-            per_it = (time.perf_counter() - t0) / 2
-            solve["cpu_port_s_per_outer_iter"] = per_it
-            solve["cpu_port_time_to_tol_s_extrapolated"] = (
-                per_it * solve["subsampled_100"]["outer_iters"])
-            solve["cpu_cores"] = os.cpu_count()
-
+    solve = tr4 = None
+    if not sharded and not args.skip_solve:
+        del A, y
+        solve = time_to_tolerance(snx, torch, rank, world, args.skip_cpu)
+        tr4 = trust_region_config4(snx, torch, rank, world, args.skip_cpu)
+        A, y = make_problem()
     cpu = cpu_baseline(A, y, x_host) if (rank == 0 and world == 1 and not args.skip_cpu) \
         else None
     shapes = None
@@ -604,22 +731,32 @@ def run_ours(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
             "host_ms_per_step": host_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": "cifar10-shape 50000x3072 C=10, 5% S_H (m=2500)",
-                       "n": N, "p": P, "C": C, "hessian_fraction": F_H, "lam": LAM,
-                       "theta": THETA, "cg_max_iters": T_CG, "parallelism": f"rows sharded over {world} GPU(s), NCCL all-reduce per Hv",
-                       "l2": "inputs > L2: 1.23 GB X in HBM, fresh S_H gathered every step"},
+            "dtype": args.dtype, "data": "synthetic", "config": CONFIG,
+            "parallelism": (f"rows sharded over {world} GPU(s), one all-reduce per Hv"
+                            if sharded else "1 GPU"),
             "hv_applied": hv_count, "gpu_launches": args.steps * (
-                # per step: gather + GEMM1 (h prepare), cg_init x2, T x (GEMM1, GEMM2,
-                # cg_step1, cg_step2) [+ snx_finish_hv per product when sharded];
-                # matches profiles/r01_launches.csv (44 per step at N = 1)
-                2 + 2 + T_CG * (4 + (1 if sharded else 0))),
-            "clocks": clk.summary(), "roofline": roofline, "e2e": e2e,
-            "cpu_baseline": cpu, "newton_solve": solve, "other_shapes": shapes,
+                # per step: the H2D index copy, prepare (1 kernel), cg_init x2, T x
+                # (product + finalize, cg_step1, cg_step2) [+ snx_finish_hv when sharded]
+                1 + 2 + T_CG * (4 + (1 if sharded else 0))),
+            "clocks": clk.summary(), "roofline": roofline, "cg_kernels": cg_rate, "e2e": e2e,
+            "cpu_baseline": cpu, "time_to_tolerance": solve, "trust_region_config4": tr4,
+            "other_shapes": shapes,
         }
         print(json.dumps(line))
     if world > 1:
         dist.destroy_process_group()
+
+
+def spawn(args):
+    """--gpus N > 1 without a torchrun environment: re-launch this script under
+    torch.distributed.run with N ranks on 127.0.0.1; its rank 0 prints the line."""
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 def main():
@@ -635,6 +772,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
+    elif args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn(args))
     else:
         run_ours(args)
 
