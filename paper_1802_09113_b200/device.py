@@ -232,6 +232,21 @@ class DeviceView:
             self._dense._ws_owner = b
         return self._dense
 
+    def take(self, indices):
+        """Rows `indices` of this view (a view of the base's rows[indices]):
+        sampling from a train split works as on the reference's materialised
+        LabeledDataset (dataset.py:180-185)."""
+        idx = np.asarray(indices, dtype=np.int64)
+        n = self._n
+        if len(idx) == n and np.array_equal(idx, np.arange(n)):
+            return self
+        if len(idx) and (idx.min() < 0 or idx.max() >= n):
+            raise DimensionError("row index out of range")
+        return DeviceView(self.base, self.rows[upload(idx, self.rows.device)], len(idx))
+
+    def slice_rows(self, i0, i1):
+        return self.take(np.arange(i0, i1))
+
     n_features = property(lambda self: self.base.n_features)
     n_classes = property(lambda self: self.base.n_classes)
     K = property(lambda self: self.base.K)
