@@ -571,6 +571,8 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world != args.gpus:
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if os.environ.get("SNX_BENCH_ONE_DEVICE") == "1":
+        local = 0  # smoke test of the N-rank path on a one-GPU box (with SNX_BENCH_BACKEND=gloo)
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group(os.environ.get("SNX_BENCH_BACKEND", "nccl"))
