@@ -17,6 +17,7 @@ full-data pass.
 """
 
 import math
+import os
 import time
 from dataclasses import dataclass, field, replace
 
@@ -150,7 +151,12 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     the host waits for iteration k's scalars, iteration k + 1 is already enqueued
     speculatively from x + alpha0 p: the GPU never idles through the host's
     Armijo / bookkeeping step.  When the line search picks another step (or the
-    loop stops) the speculative work is simply discarded.  The decisions and the
+    loop stops) the speculative work is discarded; its sample draw (the
+    SubsampledOracle of k + 1) is kept for the re-launch from x + alpha p, and
+    speculation pauses after a backtracked iteration (backtracking tends to
+    repeat) until alpha0 is accepted again -- so a backtracking phase does not
+    queue a whole wasted iteration in front of every Armijo trial.
+    SNX_SPECULATE=always|never overrides this (A/B runs).  The decisions and the
     trace are the reference's (newton.py:80-104).
     """
     ds = as_device(prob.dataset)
@@ -192,8 +198,10 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
         if test is not None:
             reads.append(softmax.correct_count(test, x_try))
         return {"p": p, "x_try": x_try, "g_try": g_try, "read": AsyncRead(*reads),
-                "cgws": cgws}
+                "cgws": cgws, "oracle": oracle}
 
+    policy = os.environ.get("SNX_SPECULATE", "adaptive")
+    speculate = policy != "never"
     t0 = time.perf_counter()
     out, corr = softmax.objective_parts(ds, x, want_correct=True)
     loss, wsq = out.tolist()
@@ -205,9 +213,10 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
     for k in range(cfg.max_outer_iters):
         # speculate: iteration k + 1 from x + alpha0 p, before reading iteration k
         nxt = None
-        if k + 1 < cfg.max_outer_iters:
-            nxt = launch(k + 1, SubsampledOracle(dev_prob, cfg.samples, k + 1), cur["x_try"],
-                         cur["g_try"])
+        orc_next = SubsampledOracle(dev_prob, cfg.samples, k + 1) \
+            if k + 1 < cfg.max_outer_iters else None
+        if orc_next is not None and speculate:
+            nxt = launch(k + 1, orc_next, cur["x_try"], cur["g_try"])
         h = cur["read"].wait()
         h_gg, h_slope, h_out, h_corr, h_slot = h[:5]
         if math.sqrt(float(h_gg)) < cfg.epsilon:
@@ -227,12 +236,16 @@ def newton_solve(prob, cfg, x0=None, test_set=None, solver_name="newton"):
         if alpha == a0:
             x = cur["x_try"]  # the same numpy-rounded x + a0 p (snx_axpy)
             te = float(h[5][0]) / test.n_rows if test is not None else math.nan
-            cur = nxt  # the speculation holds
+            g_next = cur["g_try"]
+            cur = nxt  # the speculation holds (None when it was paused)
+            if cur is None and orc_next is not None:
+                cur = launch(k + 1, orc_next, x, g_next)
+            speculate = policy != "never"
         else:
             x = axpy(x, alpha, p)
             te = test_acc(x)
-            cur = launch(k + 1, SubsampledOracle(dev_prob, cfg.samples, k + 1), x, None) \
-                if k + 1 < cfg.max_outer_iters else None
+            cur = launch(k + 1, orc_next, x, None) if orc_next is not None else None
+            speculate = policy == "always"
         f_cur, ncorr = trial.seen[alpha]
         records.append(RunRecord(solver_name, k + 1, time.perf_counter() - t0, f_cur,
                                  ncorr / n, te, alpha, report.iterations))
