@@ -8,6 +8,8 @@
 // a 1-based integer idx and a float val.  A malformed token is a parse error
 // with its 1-based line number.
 #include <errno.h>
+#include <locale.h>
+#include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -28,21 +30,89 @@ struct Parsed {
 
 inline bool is_space(char c) { return c == ' ' || c == '\t' || c == '\r' || c == '\v' || c == '\f'; }
 
-// strtod / strtoll over a token [b, e); true when the whole token was consumed
-bool parse_double(const char *b, const char *e, double *out) {
-  std::string t(b, e);
-  char *end = nullptr;
-  errno = 0;
-  *out = strtod(t.c_str(), &end);
-  return end == t.c_str() + t.size() && !t.empty();
+// The reference parses tokens with Python's float() and int() (dataset.py:266-279),
+// so the grammar here is theirs, not strtod's: digit groups may be separated by
+// single underscores (PEP 515: "1_000", "2.5e1_0"), inf / infinity / nan in any
+// case, no hexadecimal floats, no locale-dependent decimal point.  A valid token
+// is stripped of its underscores and converted in the C locale (correctly
+// rounded, as Python's conversion).
+inline bool is_digit(char c) { return c >= '0' && c <= '9'; }
+
+// digitpart: digit ("_"? digit)* starting at s[i]; appends the digits to out
+bool digit_part(const std::string &s, size_t &i, std::string &out) {
+  if (i >= s.size() || !is_digit(s[i])) return false;
+  out.push_back(s[i++]);
+  while (i < s.size()) {
+    if (is_digit(s[i])) {
+      out.push_back(s[i++]);
+    } else if (s[i] == '_' && i + 1 < s.size() && is_digit(s[i + 1])) {
+      ++i;
+    } else {
+      break;
+    }
+  }
+  return true;
 }
 
+bool ieq(const std::string &a, const char *b) {
+  if (a.size() != strlen(b)) return false;
+  for (size_t k = 0; k < a.size(); ++k) {
+    char c = a[k];
+    if (c >= 'A' && c <= 'Z') c = (char)(c - 'A' + 'a');
+    if (c != b[k]) return false;
+  }
+  return true;
+}
+
+locale_t c_locale() {
+  static locale_t loc = newlocale(LC_ALL_MASK, "C", (locale_t)0);
+  return loc;
+}
+
+// Python float(token) for a token [b, e) without surrounding whitespace
+bool parse_double(const char *b, const char *e, double *out) {
+  const std::string s(b, e);
+  size_t i = 0;
+  std::string clean;
+  if (i < s.size() && (s[i] == '+' || s[i] == '-')) clean.push_back(s[i++]);
+  const std::string rest = s.substr(i);
+  if (ieq(rest, "inf") || ieq(rest, "infinity")) {
+    *out = clean == "-" ? -HUGE_VAL : HUGE_VAL;
+    return true;
+  }
+  if (ieq(rest, "nan")) {
+    *out = clean == "-" ? -NAN : NAN;
+    return true;
+  }
+  bool mant = false;
+  if (i < s.size() && is_digit(s[i])) mant = digit_part(s, i, clean);
+  if (i < s.size() && s[i] == '.') {
+    clean.push_back(s[i++]);
+    if (i < s.size() && is_digit(s[i])) mant = digit_part(s, i, clean) || mant;
+  }
+  if (!mant) return false;
+  if (i < s.size() && (s[i] == 'e' || s[i] == 'E')) {
+    clean.push_back(s[i++]);
+    if (i < s.size() && (s[i] == '+' || s[i] == '-')) clean.push_back(s[i++]);
+    if (!digit_part(s, i, clean)) return false;
+  }
+  if (i != s.size()) return false;
+  char *end = nullptr;
+  *out = strtod_l(clean.c_str(), &end, c_locale());
+  return end == clean.c_str() + clean.size();
+}
+
+// Python int(token) in base 10 (sign, digits with single underscores)
 bool parse_int(const char *b, const char *e, long long *out) {
-  std::string t(b, e);
+  const std::string s(b, e);
+  size_t i = 0;
+  std::string clean;
+  if (i < s.size() && (s[i] == '+' || s[i] == '-')) clean.push_back(s[i++]);
+  if (!digit_part(s, i, clean) || i != s.size()) return false;
   char *end = nullptr;
   errno = 0;
-  *out = strtoll(t.c_str(), &end, 10);
-  return end == t.c_str() + t.size() && !t.empty() && errno == 0;
+  *out = strtoll(clean.c_str(), &end, 10);
+  return end == clean.c_str() + clean.size() && errno == 0;
 }
 
 int parse_file(const char *path, Parsed *P) {

@@ -1165,6 +1165,11 @@ static int tc_apply(const void *X1, const void *X2, int64_t ldb, int64_t nrows, 
   __nv_bfloat16 *B = reinterpret_cast<__nv_bfloat16 *>(wsb + lay.tc_b);
   __nv_bfloat16 *UT = reinterpret_cast<__nv_bfloat16 *>(wsb + lay.tc_ut);
   const int64_t ldu = tc_ld((int32_t)nrows);
+  // MUST stay a plain (non-PDL) launch: tc_gemm1 triggers its dependents at its
+  // first instruction, so tc_gemm2 may start while tc_gemm1 runs and it reads
+  // the CG / Steihaug done flag (`skip`) at entry, before any griddepcontrol.wait.
+  // That read is final only because this launch serialises behind the kernel
+  // that writes the flag (cg_step2 / tr_step3): a PDL launch here would race.
   tc_prep_b_kernel<<<64, 256, 0, st>>>(v, K, p, (int)PB, KP, B);
   if (check_launch("tc_prep_b")) return 1;
 

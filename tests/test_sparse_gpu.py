@@ -112,8 +112,8 @@ def test_load_libsvm_to_device(libsvm_golden):
     from conftest import libsvm_cases
 
     for name, path, C, nf, storage, g in libsvm_cases(libsvm_golden):
-        if str(g["error"]):
-            continue
+        if str(g["error"]) or not np.all(np.isfinite(g["X"])):
+            continue  # parse errors / inf-nan tokens: covered by tests/test_io_cpu.py
         ds = snx.load_libsvm(path, C, n_features=nf, storage=storage)
         assert getattr(ds, "is_sparse", False) == bool(g["is_sparse"]), name
         X, y = g["X"], g["y"]
