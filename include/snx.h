@@ -205,29 +205,6 @@ int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
                   const double *dots, double *r, double *s, double *p, double *p_best,
                   double *state, void *stream);
 
-/* The whole CG solve of cg.py:51-98 on the sampled Hessian of
- * softmax.py:197-210 (Xs, H from snx_hess_prepare; fp64 data) in ONE
- * persistent cooperative launch: equivalent to snx_cg_init followed by
- * max_iters x (snx_hess_apply(s -> Hs, dots, skip) + snx_cg_update), with
- * bit-identical results and the same r / s / p / p_best / Hs / dots / state
- * buffers (state: (max_iters + 2) * SNX_CG_SLOT + SNX_DOT_BLOCKS doubles). */
-int snx_cg_solve(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
-                 const void *H, double scale, double lam, const double *g, double theta,
-                 int32_t max_iters, double *r, double *s, double *p_vec, double *p_best,
-                 double *Hs, double *dots, double *state, void *ws, size_t ws_bytes,
-                 void *stream);
-
-/* snx_hess_apply(s -> Hs, dots, skip = done flag of slot t) followed by
- * snx_cg_update(t, ...), with the CG update fused into the tail of the
- * Hessian product's second GEMM (no separate update kernels).  The r.r
- * reduction is fixed-order over column tiles instead of SNX_DOT_BLOCKS blocks,
- * so the iterates agree with the unfused pair to rounding, not bitwise. */
-int snx_hess_apply_cg(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p,
-                      int32_t K, const void *H, double scale, double lam, int32_t t,
-                      int32_t max_iters, double *r, double *s, double *p_vec, double *p_best,
-                      double *Hs, double *dots, double *state, void *ws, size_t ws_bytes,
-                      void *stream);
-
 /* Address of the "done" field of slot t (pass as snx_hess_apply's skip). */
 const double *snx_cg_done_flag(const double *state, int32_t t);
 

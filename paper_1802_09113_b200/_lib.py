@@ -64,12 +64,6 @@ SIGNATURES = {
     "snx_cg_update": (_c_int, [_c_i32, _c_i32, _c_i64, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
                                _c_p]),
     "snx_cg_done_flag": (_c_p, [_c_p, _c_i32]),
-    "snx_hess_apply_cg": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_dbl,
-                                   _c_dbl, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
-                                   _c_p, _c_p, _c_size, _c_p]),
-    "snx_cg_solve": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_dbl, _c_dbl,
-                              _c_p, _c_dbl, _c_i32, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p, _c_p,
-                              _c_p, _c_size, _c_p]),
     "snx_power_step": (_c_int, [_c_p, _c_p, _c_i64, _c_p, _c_p]),
     "snx_colnorm_workspace_bytes": (_c_size, [_c_i32]),
     "snx_column_norms": (_c_int, [_c_int, _c_p, _c_i64, _c_i64, _c_i32, _c_p, _c_p, _c_p, _c_size,

@@ -50,7 +50,7 @@ constexpr int kG2Rows = 32;                  // rows per GEMM2 item
 constexpr int kMaxTiles = kDotBlocks;
 constexpr size_t kSmemBudget = 220 * 1024;
 constexpr int64_t kMaxRowBlocks = 1 << 17;   // 12.5M rows per call
-constexpr int kCounterWords = 16 + kMaxTiles + 2 * kMaxRowBlocks;  // + u_ready flags
+constexpr int kCounterWords = 16 + kMaxTiles + kMaxRowBlocks;
 
 __host__ __device__ constexpr size_t cround(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
@@ -64,17 +64,7 @@ __device__ unsigned long long g_timeline[3][160][8];
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
     if (blockIdx.x < 160) g_timeline[slot][blockIdx.x][ev] = t_;          \
   } while (0)
-__device__ unsigned long long g_cg_timeline[160][10];
-#define SNX_CTL(ev)                                                        \
-  do {                                                                     \
-    unsigned long long t_;                                                 \
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                 \
-    if (blockIdx.x < 160) g_cg_timeline[blockIdx.x][ev] = t_;             \
-  } while (0)
 #else
-#define SNX_CTL(ev) \
-  do {              \
-  } while (0)
 #define SNX_TL(slot, ev) \
   do {                   \
   } while (0)
@@ -205,7 +195,6 @@ struct G1Args {
   double *loss_out;
   long long *corr_out;
   const double *skip;
-  unsigned *u_ready;   // persistent CG kernel: publish U rows of a row block (epoch)
   int32_t *pred_out;   // kProbs: most probable class per row (nullable)
   double *stats_out;   // kProbs: [M, sum E, linear] per row (nullable)
   int early_x;         // launched as a programmatic dependent: stage the first X
@@ -390,12 +379,6 @@ __device__ __forceinline__ void block_epilogue(const G1Args &a, int64_t rb, int 
     row_epilogue<T, K>(a, r, z, hw, y, loss, corr);
   }
   if (tid == 0) a.rb_count[rb] = 0u;  // rest state for the next launch
-  if (a.u_ready != nullptr) {  // publish this row block's U rows (release)
-    consumer_sync(kConsumers);
-    if (tid == 0)
-      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(a.u_ready + rb), "r"(epoch)
-                   : "memory");
-  }
   if (a.mode != kObjective && a.mode != kGradient) return;
   const double bl = consumer_sum(loss, shd);
   const unsigned long long bc = consumer_sum_u64(corr, shu);
@@ -684,12 +667,6 @@ struct G2Args {
   const double *base;    // v (Hessian) / w (gradient)
   double *out;           // scale * X^T U + lam * base, flat class-major
   double *dots;          // nullable: [tile] partials of base.out, [kDotBlocks + tile] of base.base
-  const unsigned *u_ready;  // persistent CG kernel: [row_blocks] U publication epochs
-  // CG iteration fused into the tail (snx_hess_apply_cg; cg_state == NULL: off)
-  double *cg_state;      // slots (cg.py state), scratch = per-tile r.r partials
-  double *cg_r, *cg_p, *cg_pb;  // base == s
-  unsigned *cg_sync;     // [3] arrival counters (zero at rest)
-  int cg_t, cg_T;
 };
 
 // out[c*p + j] = scale * sum_seg gp[tile][seg][c][jj] + lam * base[c*p + j] for
@@ -756,153 +733,7 @@ __device__ __forceinline__ void tile_finalize(const G2Args &a, int tile, int G, 
     }
 }
 
-__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned *p) {
-  unsigned x;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(x) : "l"(p) : "memory");
-  return x;
-}
-
-// The CG iteration of cg.py:77-96 fused into GEMM2's tail (snx_hess_apply_cg),
-// run by the CTAs that finalized column tiles, once they have finished all
-// their items (so the waits below never wait on their own work): wait until
-// every tile's H s and curvature partials are out, then alpha, p += a s,
-// r -= a H s on the own tiles' elements and the tiles' r.r partials, wait for
-// every tile's partial, then beta, the best copy, the new direction and (by the
-// finalizer of tile 0) the next state slot.  Reductions are fixed-order over
-// tiles, so the result does not depend on which CTA finalized which tile.
-template <int K, int TCOL>
-__device__ __forceinline__ void cg_tail(const G2Args &a, const int *tiles, int n, double *shd,
-                                     double *shx) {
-  const int tid = threadIdx.x;
-  const int t = a.cg_t;
-  const double *st = slot(a.cg_state, t);
-  double *nx = slot(a.cg_state, t + 1);
-  double *rrp = scratch(a.cg_state, a.cg_T);
-  // shared scalars (the caller's smem: no static __shared__ in this function)
-  double &s_alpha = shx[0], &s_curv = shx[1], &s_rr = shx[2];
-  double &s_bad = shx[3], &s_last = shx[4];
-  constexpr int kPer = (K * TCOL + kConsumers - 1) / kConsumers;
-  bool own0 = false;
-  for (int k = 0; k < n; ++k) own0 |= tiles[k] == 0;
-  // ---- every tile's H s and s.Hs / s.s partials are out
-  consumer_sync(kConsumers);
-  if (tid == 0) {
-    atomic_add_acq_rel(a.cg_sync, (unsigned)n);
-    while (ld_acquire_gpu(a.cg_sync) < (unsigned)a.col_tiles) __nanosleep(32);
-  }
-  consumer_sync(kConsumers);
-  if (tid < 32) {  // cg_step1: the same fixed-order sums in every CTA
-    const double curv = warp_sum_partials_cg(a.dots);
-    const double ss = warp_sum_partials_cg(a.dots + kDotBlocks);
-    if (tid == 0) {
-      s_bad = curv <= 1e-32 * ss ? 1.0 : 0.0;  // cg.py:16, :79
-      s_alpha = __ldcg(st + kRs) / curv;
-      s_curv = curv;
-    }
-  }
-  consumer_sync(kConsumers);
-  if (s_bad != 0.0) {
-    if (own0 && tid == 0) {
-      nx[kErr] = 1.0;
-      nx[kCurv] = s_curv;
-      nx[kRs] = st[kRs];
-      nx[kBest] = st[kBest];
-      nx[kThr] = st[kThr];
-      nx[kConv] = 0.0;
-      nx[kIters] = t + 1;
-      nx[kDone] = 1.0;
-    }
-  } else {
-    const double alpha = s_alpha;
-    for (int k = 0; k < n; ++k) {
-      const int tile = tiles[k];
-      double acc = 0.0;
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const int e = tid + q * kConsumers;
-        const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
-        if (e < K * TCOL && j < a.p) {
-          const int64_t i = (int64_t)c * a.p + j;
-          a.cg_p[i] = np_axpy(a.cg_p[i], alpha, __ldcg(a.base + i));
-          const double ri = np_axmy(a.cg_r[i], alpha, __ldcg(a.out + i));
-          a.cg_r[i] = ri;
-          acc += ri * ri;
-        }
-      }
-      const double b = consumer_sum(acc, shd);
-      if (tid == 0) rrp[tile] = b;
-    }
-    // ---- every tile's r.r partial is out
-    consumer_sync(kConsumers);
-    if (tid == 0) {
-      atomic_add_acq_rel(a.cg_sync + 1, (unsigned)n);
-      while (ld_acquire_gpu(a.cg_sync + 1) < (unsigned)a.col_tiles) __nanosleep(32);
-    }
-    consumer_sync(kConsumers);
-    if (tid < 32) {
-      double v = 0.0;
-      for (int k = tid; k < a.col_tiles; k += 32) v += __ldcg(rrp + k);
-      v = warp_allsum(v);
-      if (tid == 0) s_rr = v;
-    }
-    consumer_sync(kConsumers);
-    // cg_step2
-    const double rr = s_rr;
-    const double rn = sqrt(rr);
-    const double rs0 = __ldcg(st + kRs), best0 = __ldcg(st + kBest), thr = __ldcg(st + kThr);
-    const bool best = rn <= best0;
-    const bool conv = rn <= thr;
-    const double beta = rr / rs0;
-    for (int k = 0; k < n; ++k) {
-      const int tile = tiles[k];
-#pragma unroll
-      for (int q = 0; q < kPer; ++q) {
-        const int e = tid + q * kConsumers;
-        const int c = e / TCOL, j = tile * TCOL + (e - c * TCOL);
-        if (e < K * TCOL && j < a.p) {
-          const int64_t i = (int64_t)c * a.p + j;
-          if (best) a.cg_pb[i] = a.cg_p[i];
-          if (!conv) const_cast<double *>(a.base)[i] = np_axpy(a.cg_r[i], beta, a.base[i]);
-        }
-      }
-    }
-    if (own0 && tid == 0) {
-      nx[kRs] = conv ? rs0 : rr;
-      nx[kBest] = best ? rn : best0;
-      nx[kThr] = thr;
-      nx[kConv] = conv ? 1.0 : 0.0;
-      nx[kIters] = t + 1;
-      nx[kDone] = (conv || t + 1 >= a.cg_T) ? 1.0 : 0.0;
-    }
-  }
-  // ---- the last finalizer out resets the counters for the next launch
-  consumer_sync(kConsumers);
-  if (tid == 0) {
-    s_last = atomic_add_acq_rel(a.cg_sync + 2, (unsigned)n) == (unsigned)(a.col_tiles - n);
-    if (s_last != 0.0) {
-      a.cg_sync[0] = 0u;
-      a.cg_sync[1] = 0u;
-      a.cg_sync[2] = 0u;
-    }
-  }
-  consumer_sync(kConsumers);
-}
-
-// Acquire a U-ready flag written by another CTA of the same kernel (the
-// persistent CG kernel), then order the TMA (async proxy) reads after it.
-__device__ __forceinline__ void wait_flag_geq(const unsigned *f, unsigned v) {
-  unsigned x;
-  for (;;) {
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(x) : "l"(f) : "memory");
-    if (x >= v) break;
-    __nanosleep(32);
-  }
-  asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-
-// GEMM2 work of one CTA (see gemm1_body).  With a.u_ready set, the U rows of
-// a 32-row chunk are loaded only once their row block's epilogue has
-// published them (u_ready[rb] >= a.epoch).
+// GEMM2 work of one CTA (see gemm1_body).
 template <typename T, int K, int S>
 __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem, double *red,
                                            uint64_t *full, uint64_t *empty, int G, int64_t &itp,
@@ -918,9 +749,6 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
   const int rc0 = (int)(i0 - (int64_t)tile0 * a.rchunks);
   __shared__ double shd[2 * kWarps];
   __shared__ int last_tile;
-  __shared__ int fin_tiles[4], nfin;  // tiles this CTA finalized (fused CG tail)
-  __shared__ double shx[8];
-  if (tid == 0) nfin = 0;
 
   if (warp == kWarps) {
     // ------------------------------------------------ producer warp (TMA)
@@ -937,7 +765,6 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
         mbar_arrive_expect_tx(&full[s], (unsigned)Sh::XB + ub);
         unsigned char *st = smem + s * Sh::STAGE;
         tma_load_2d(st, &a.xmap, tile * TCOL, (int)c0, &full[s]);
-        if (a.u_ready != nullptr) wait_flag_geq(a.u_ready + c0 / kRB, epoch);
         if (i == i0) pdl_wait();  // no-op unless launched as a programmatic dependent
         bulk_g2s(st + Sh::XB, U + c0 * KP, ub, &full[s]);
         // the done flag of a captured CG loop is read only after the wait: the
@@ -958,11 +785,7 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
 
   // -------------------------------------------------- consumer warps
   pdl_wait();  // no-op unless launched as a programmatic dependent
-  if (a.skip != nullptr && *a.skip != 0.0) {
-    if (a.cg_state != nullptr && cta == 0 && tid < SNX_CG_SLOT)  // cg_step2 on a done slot
-      slot(a.cg_state, a.cg_t + 1)[tid] = slot(a.cg_state, a.cg_t)[tid];
-    return;
-  }
+  if (a.skip != nullptr && *a.skip != 0.0) return;
   T acc[LC][K];
 #pragma unroll
   for (int v = 0; v < LC; ++v)
@@ -1014,13 +837,11 @@ __device__ __forceinline__ void gemm2_body(const G2Args &a, unsigned char *smem,
       if (i == i1 && tid == 0) SNX_TL(1, 5);
       if (last_tile) {
         tile_finalize<K, TCOL>(a, ftile, G, shd);
-        if (tid == 0) fin_tiles[nfin++] = ftile;
         consumer_sync(kConsumers);
         if (i == i1 && tid == 0) SNX_TL(1, 6);
       }
     }
     if (i == i1) {
-      if (a.cg_state != nullptr && nfin > 0) cg_tail<K, TCOL>(a, fin_tiles, nfin, shd, shx);
       if (tid == 0) SNX_TL(1, 3);
       break;
     }
@@ -1168,301 +989,6 @@ __global__ void __launch_bounds__(kDotThreads)
     }
   }
   if (threadIdx.x == 0) SNX_TL(2, 3);
-}
-
-// ---------------------------------------------------------------- persistent CG
-// cg.py:51-98 with the Hessian product of softmax.py:197-210: the whole CG
-// solve in ONE launch of one CTA per SM (co-resident, cooperative launch).
-// Per iteration: GEMM1 items -> U rows published per row block (release
-// flag, no grid barrier: GEMM2 producers acquire the flags of the rows they
-// load, so the GEMM1 epilogues overlap the GEMM2 stream) -> GEMM2 items with
-// the fused finalize (Hs tiles + curvature partials) -> grid barrier ->
-// alpha, p / r update -> grid barrier -> beta, best copy, new direction ->
-// grid barrier.  The arithmetic (stream-K splits, segment orders, the 256
-// fixed dot partials emulated as virtual blocks) is exactly that of
-// snx_hess_apply + snx_cg_update, so results are bit-identical to the
-// multi-kernel path.
-template <typename T, int K> struct CgShape {
-  using G1 = G1Shape<T, K>;
-  using G2 = G2Shape<T, K>;
-  static constexpr int S1 = G1::S;
-  static constexpr size_t RING = (size_t)S1 * G1::STAGE;  // both rings' stages
-  // GEMM2 stages + its reduction buffer fit inside RING; GEMM1's reduction
-  // buffer (in use by its epilogue while GEMM2 tiles stream in) sits after it
-  static constexpr int S2 = (4 * G2::STAGE + G2::RED <= RING)   ? 4
-                            : (3 * G2::STAGE + G2::RED <= RING) ? 3
-                                                                : 2;
-  static constexpr bool OK = S2 * G2::STAGE + G2::RED <= RING;
-  static constexpr size_t RED2 = (size_t)S2 * G2::STAGE;
-  static constexpr size_t SMEM = RING + G1::RED;
-};
-
-struct CgArgs {
-  G1Args g1;  // mode kHessApply; W = sw, U -> rowout; u_ready set
-  G2Args g2;  // base = s, out = Hs, dots; u_ready set
-  int grid1, grid2;
-  int T;
-  double theta;
-  int64_t d;
-  int p, P;
-  const double *g;
-  double *r, *s, *pv, *pb, *Hs, *dots, *state;
-  void *sw;           // s in the X dtype, [K][P] (GEMM1's W operand)
-  unsigned *bar;      // grid barrier [count, generation]
-  unsigned *u_ready;  // [row_blocks] (zero at rest)
-  int64_t row_blocks;
-};
-
-__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned *p) {
-  unsigned x;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(x) : "l"(p) : "memory");
-  return x;
-}
-
-// Sense-free grid barrier over nblk co-resident CTAs: the last arriver resets
-// the count and bumps the generation (release); the others wait for the bump.
-__device__ __forceinline__ void grid_barrier(unsigned *bar, unsigned nblk) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const unsigned gen = ld_acquire_u32(bar + 1);
-    if (atomic_add_acq_rel(bar, 1u) == nblk - 1) {
-      bar[0] = 0u;
-      asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(bar + 1), "r"(gen + 1u)
-                   : "memory");
-    } else {
-      while (ld_acquire_u32(bar + 1) == gen) __nanosleep(20);
-    }
-  }
-  __syncthreads();
-}
-
-// Producer: wait until the consumers released every stage still in flight.
-__device__ __forceinline__ void ring_drain(uint64_t *empty, int S, int64_t itp) {
-  for (int64_t k = itp > S ? itp - S : 0; k < itp; ++k)
-    mbar_wait(&empty[k % S], (unsigned)((k / S) & 1));
-}
-
-struct CgSlot {
-  double rs, best, thr, iters, conv, done, err, curv;
-};
-
-template <typename T>
-__device__ __forceinline__ void store_sw(const CgArgs &a, int64_t i, double v) {
-  const int64_t c = i / a.p;
-  static_cast<T *>(a.sw)[c * a.P + (i - c * a.p)] = (T)v;
-}
-
-template <typename T, int K>
-__global__ void __launch_bounds__(kThreads, 1) cg_solve_kernel(const __grid_constant__ CgArgs a) {
-  using Sh = CgShape<T, K>;
-  constexpr int S1 = Sh::S1, S2 = Sh::S2;
-  extern __shared__ __align__(1024) unsigned char smem[];
-  double *red1 = reinterpret_cast<double *>(smem + Sh::RING);
-  double *red2 = reinterpret_cast<double *>(smem + Sh::RED2);
-  __shared__ uint64_t full1[S1], empty1[S1], full2[S2], empty2[S2];
-  __shared__ double shd[2 * kWarps];
-  __shared__ CgSlot cur;
-  const int tid = threadIdx.x;
-  const bool consumer = tid < kConsumers;
-  const int Gp = gridDim.x, cta = blockIdx.x;
-  if (tid == 0) {
-    for (int s = 0; s < S1; ++s) {
-      mbar_init(&full1[s], 1);
-      mbar_init(&empty1[s], kWarps);
-    }
-    for (int s = 0; s < S2; ++s) {
-      mbar_init(&full2[s], 1);
-      mbar_init(&empty2[s], kWarps);
-    }
-    mbar_fence_init();
-  }
-  __syncthreads();
-  const int64_t d = a.d;
-  constexpr int64_t kStride = (int64_t)kDotBlocks * kDotThreads;
-  double *scr = scratch(a.state, a.T);
-
-  // ---- init (cg_init_kernel): r = s = -g, p = 0, p_best = -g, g.g partials
-  if (cta == 0)
-    for (int i = tid; i < (a.T + 2) * SNX_CG_SLOT; i += kThreads) a.state[i] = 0.0;
-  if (consumer) {
-    for (int vb = cta; vb < kDotBlocks; vb += Gp) {
-      double acc = 0.0;
-      for (int64_t i = (int64_t)vb * kDotThreads + tid; i < d; i += kStride) {
-        const double gi = a.g[i];
-        a.r[i] = -gi;
-        a.s[i] = -gi;
-        a.pv[i] = 0.0;
-        a.pb[i] = -gi;
-        store_sw<T>(a, i, -gi);
-        acc += gi * gi;
-      }
-      const double b = consumer_sum(acc, shd);
-      if (tid == 0) scr[vb] = b;
-    }
-    if (cta == 0 && a.P != a.p)  // zero pad columns of sw
-      for (int i = tid; i < K * (a.P - a.p); i += kConsumers)
-        static_cast<T *>(a.sw)[(i / (a.P - a.p)) * a.P + a.p + i % (a.P - a.p)] = T(0);
-  }
-  grid_barrier(a.bar, Gp);
-  if (tid < 32) {  // cg_init_final_kernel, computed by every CTA
-    const double gg = warp_sum_partials_cg(scr);
-    if (tid == 0) {
-      const double gn = sqrt(gg);
-      cur.rs = gg;
-      cur.best = gn;
-      cur.thr = a.theta * gn;
-      cur.iters = 0.0;
-      cur.conv = gn == 0.0 ? 1.0 : 0.0;
-      cur.done = gn == 0.0 ? 1.0 : 0.0;
-      cur.err = 0.0;
-      cur.curv = 0.0;
-      if (cta == 0) {
-        double *s0 = slot(a.state, 0);
-        s0[kRs] = cur.rs;
-        s0[kBest] = cur.best;
-        s0[kThr] = cur.thr;
-        s0[kIters] = 0.0;
-        s0[kConv] = cur.conv;
-        s0[kDone] = cur.done;
-      }
-    }
-  }
-  __syncthreads();
-
-  int64_t itp1 = 0, itc1 = 0, itp2 = 0, itc2 = 0;
-  int t = 0;
-  for (; t < a.T; ++t) {
-    if (cur.done != 0.0) break;
-    const unsigned epoch = (unsigned)t + 1u;
-    const bool tl = t == 5 && tid == 0;
-    if (tl) SNX_CTL(0);
-    // ---- Hs = H s (snx_hess_apply with the dots of s.Hs and s.s)
-    if (tid == kConsumers) asm volatile("fence.proxy.async.global;\n" ::: "memory");  // sw via TMA
-    gemm1_body<T, K, S1>(a.g1, smem, red1, full1, empty1, a.grid1, itp1, itc1, epoch);
-    if (tl) SNX_CTL(1);
-    if (tid == kConsumers && cta < a.grid1) ring_drain(empty1, S1, itp1);
-    gemm2_body<T, K, S2>(a.g2, smem, red2, full2, empty2, a.grid2, itp2, itc2, epoch);
-    if (tl) SNX_CTL(2);
-    grid_barrier(a.bar, Gp);
-    if (tl) SNX_CTL(3);
-    // ---- cg_step1: curvature test, alpha, p += a s, r -= a Hs
-    __shared__ double s_alpha;
-    __shared__ int s_bad;
-    if (tid < 32) {
-      const double curv = warp_sum_partials_cg(a.dots);
-      const double ss = warp_sum_partials_cg(a.dots + kDotBlocks);
-      if (tid == 0) {
-        s_bad = curv <= 1e-32 * ss;  // cg.py:16, :79
-        s_alpha = cur.rs / curv;
-        if (s_bad) {
-          cur.err = 1.0;
-          cur.curv = curv;
-          if (cta == 0) {
-            slot(a.state, t + 1)[kErr] = 1.0;
-            slot(a.state, t + 1)[kCurv] = curv;
-          }
-        }
-      }
-    }
-    __syncthreads();
-    const bool bad = s_bad != 0;
-    if (!bad) {
-      if (consumer) {
-        const double alpha = s_alpha;
-        for (int vb = cta; vb < kDotBlocks; vb += Gp) {
-          double acc = 0.0;
-          for (int64_t i = (int64_t)vb * kDotThreads + tid; i < d; i += kStride) {
-            a.pv[i] = np_axpy(a.pv[i], alpha, a.s[i]);
-            const double ri = np_axmy(a.r[i], alpha, __ldcg(a.Hs + i));
-            a.r[i] = ri;
-            acc += ri * ri;
-          }
-          const double b = consumer_sum(acc, shd);
-          if (tid == 0) scr[vb] = b;
-        }
-      }
-      if (tl) SNX_CTL(4);
-      grid_barrier(a.bar, Gp);
-      if (tl) SNX_CTL(5);
-    }
-    // ---- cg_step2: best-iterate copy, stop test, new direction
-    if (bad) {
-      if (tid == 0) {
-        cur.conv = 0.0;
-        cur.iters = t + 1;
-        cur.done = 1.0;
-        if (cta == 0) {
-          double *nx = slot(a.state, t + 1);
-          nx[kRs] = cur.rs;
-          nx[kBest] = cur.best;
-          nx[kThr] = cur.thr;
-          nx[kConv] = 0.0;
-          nx[kIters] = t + 1;
-          nx[kDone] = 1.0;
-        }
-      }
-      __syncthreads();
-      ++t;
-      break;
-    }
-    __shared__ double s_rr;
-    if (tid < 32) {
-      const double rr = warp_sum_partials_cg(scr);
-      if (tid == 0) s_rr = rr;
-    }
-    __syncthreads();
-    const double rr = s_rr;
-    const double rn = sqrt(rr);
-    const bool best = rn <= cur.best;
-    const bool conv = rn <= cur.thr;
-    const double beta = rr / cur.rs;
-    if (consumer) {
-      for (int vb = cta; vb < kDotBlocks; vb += Gp)
-        for (int64_t i = (int64_t)vb * kDotThreads + tid; i < d; i += kStride) {
-          if (best) a.pb[i] = a.pv[i];
-          if (!conv) {
-            const double si = np_axpy(a.r[i], beta, a.s[i]);
-            a.s[i] = si;
-            store_sw<T>(a, i, si);
-          }
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-      cur.rs = conv ? cur.rs : rr;
-      cur.best = best ? rn : cur.best;
-      cur.conv = conv ? 1.0 : 0.0;
-      cur.iters = t + 1;
-      cur.done = (conv || t + 1 >= a.T) ? 1.0 : 0.0;
-      if (cta == 0) {
-        double *nx = slot(a.state, t + 1);
-        nx[kRs] = cur.rs;
-        nx[kBest] = cur.best;
-        nx[kThr] = cur.thr;
-        nx[kConv] = cur.conv;
-        nx[kIters] = cur.iters;
-        nx[kDone] = cur.done;
-      }
-    }
-    __syncthreads();
-    if (tl) SNX_CTL(6);
-    if (cur.done != 0.0) {
-      ++t;
-      break;
-    }
-    grid_barrier(a.bar, Gp);  // s / sw complete before the next GEMM1
-    if (tl) SNX_CTL(7);
-  }
-  // slots after the last iteration repeat it (cg_step2 copies a done slot)
-  if (cta == 0 && tid == 0) {
-    const double *last = slot(a.state, t);
-    for (int u = t + 1; u <= a.T; ++u)
-      for (int k = 0; k < SNX_CG_SLOT; ++k) slot(a.state, u)[k] = last[k];
-  }
-  // every CTA is past its last GEMM phase once all arrive here
-  grid_barrier(a.bar, Gp);
-  if (cta == 0)
-    for (int64_t i = tid; i < a.row_blocks; i += kThreads) a.u_ready[i] = 0u;
 }
 
 // out = lam * base (the empty dataset: every data term vanishes), with the
@@ -1780,11 +1306,6 @@ int validate(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
 }
 
 // Common driver of the row-pass entry points (rows contiguous).
-struct CgFuse {  // snx_hess_apply_cg: the CG iteration fused into GEMM2's tail
-  double *state, *r, *p, *pb;
-  int t, T;
-};
-
 struct ProbsOut {
   int32_t *pred;
   double *stats;
@@ -1795,7 +1316,7 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
                    double alpha, const void *H, void *rowout, double scale, double lam,
                    const double *base, double *out, long long *corr_out, double *vec_out,
                    double *dots, const double *skip, void *ws, size_t ws_bytes,
-                   cudaStream_t st, const CgFuse *cg = nullptr, const ProbsOut *po = nullptr) {
+                   cudaStream_t st, const ProbsOut *po = nullptr) {
   if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
   const int32_t P = padded(p);
   const Geometry g = geometry(dtype, nrows, P, K);
@@ -1805,7 +1326,7 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   double *dotp = reinterpret_cast<double *>(wsb + lay.dot_part);
 
   // fp64, K <= 9: the one-pass cluster kernel (X streamed once per product)
-  if (nrows > 0 && cg == nullptr &&
+  if (nrows > 0 &&
       ((mode == kHessApply && cluster_supported(dtype, p, K)) ||
        (mode == kGradient && cluster_grad_preferred(dtype, p, K)))) {
     if (mode == kGradient && out != nullptr &&
@@ -1900,130 +1421,11 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   b.base = base;
   b.out = vec_out;
   b.dots = dots;
-  if (cg != nullptr) {
-    b.cg_state = cg->state;
-    b.cg_r = cg->r;
-    b.cg_p = cg->p;
-    b.cg_pb = cg->pb;
-    b.cg_sync = counters + 6;  // [3]
-    b.cg_t = cg->t;
-    b.cg_T = cg->T;
-  }
   if (dtype == SNX_F64) {
     SNX_K_SWITCH(K, (rc = launch_gemm2<double, KK>(b, g.grid2, st)));
   } else {
     SNX_K_SWITCH(K, (rc = launch_gemm2<float, KK>(b, g.grid2, st)));
   }
-  return rc;
-}
-
-template <typename T, int K>
-static int launch_cg_solve(const CgArgs &a, int grid, cudaStream_t st) {
-  using Sh = CgShape<T, K>;
-  if constexpr (!Sh::OK) {
-    set_error("snx_cg_solve: no shared-memory layout for this dtype / K");
-    return 1;
-  } else {
-    static bool configured = false;
-    if (!configured) {
-      if (cudaFuncSetAttribute(cg_solve_kernel<T, K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)Sh::SMEM) != cudaSuccess)
-        return check_launch("cg_solve attributes");
-      configured = true;
-    }
-    carveout(cg_solve_kernel<T, K>);
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = Sh::SMEM;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // all CTAs co-resident (grid barriers)
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    cudaLaunchKernelEx(&cfg, cg_solve_kernel<T, K>, a);
-    return check_launch("cg_solve");
-  }
-}
-
-static int cg_solve(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
-                    const void *H, double scale, double lam, const double *g, double theta,
-                    int32_t T, double *r, double *s, double *pv, double *pb, double *Hs,
-                    double *dots, double *state, void *ws, size_t ws_bytes, cudaStream_t st) {
-  if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
-  if (dtype != SNX_F64) {
-    set_error("snx_cg_solve: fp64 data only (the f32 path uses the tensor-core product)");
-    return 1;
-  }
-  if (nrows == 0 || T < 1 || H == nullptr || g == nullptr) {
-    set_error("snx_cg_solve: needs nrows > 0, max_iters >= 1, H and g");
-    return 1;
-  }
-  const int32_t P = padded(p);
-  const Geometry geo = geometry(dtype, nrows, P, K);
-  const Workspace lay = workspace_layout(dtype, nrows, p, K);
-  char *wsb = static_cast<char *>(ws);
-  unsigned *counters = reinterpret_cast<unsigned *>(wsb + lay.counters);
-  void *sw = wsb + lay.weights;
-  void *rowbuf = wsb + lay.rowbuf;
-  unsigned *u_ready = counters + 16 + kMaxTiles + kMaxRowBlocks;
-  CgArgs a{};
-  if (make_map(&a.g1.xmap, dtype, X, P, nrows, ldx, 128 / 8, kRB, true)) return 1;
-  if (make_map(&a.g1.wmap, dtype, sw, P, K, P, 512 / 8, K, false)) return 1;
-  a.g1.nrows = nrows;
-  a.g1.nchunks = geo.nchunks;
-  a.g1.maxseg = geo.g1_maxseg;
-  a.g1.items = geo.g1_items;
-  a.g1.row_blocks = geo.row_blocks;
-  a.g1.mode = kHessApply;
-  a.g1.ustride = u_stride(dtype, K);
-  a.g1.zp = reinterpret_cast<double *>(wsb + lay.zp);
-  a.g1.rb_count = counters + 16 + kMaxTiles;
-  a.g1.done_rb = counters + 2;
-  a.g1.H = H;
-  a.g1.rowout = rowbuf;
-  a.g1.loss_part = reinterpret_cast<double *>(wsb + lay.loss_part);
-  a.g1.corr_part = reinterpret_cast<unsigned long long *>(wsb + lay.corr_part);
-  a.g1.u_ready = u_ready;
-  if (make_map(&a.g2.xmap, dtype, X, P, nrows, ldx, (uint32_t)geo.tcol, kG2Rows, false)) return 1;
-  a.g2.nrows = nrows;
-  a.g2.rchunks = geo.rchunks;
-  a.g2.maxseg = geo.g2_maxseg;
-  a.g2.items = geo.g2_items;
-  a.g2.U = rowbuf;
-  a.g2.gp = reinterpret_cast<double *>(wsb + lay.gp);
-  a.g2.tile_count = counters + 16;
-  a.g2.col_tiles = geo.col_tiles;
-  a.g2.p = p;
-  a.g2.scale = scale;
-  a.g2.lam = lam;
-  a.g2.base = s;
-  a.g2.out = Hs;
-  a.g2.dots = dots;
-  a.g2.u_ready = u_ready;
-  a.grid1 = geo.grid1;
-  a.grid2 = geo.grid2;
-  a.T = T;
-  a.theta = theta;
-  a.d = (int64_t)K * p;
-  a.p = p;
-  a.P = P;
-  a.g = g;
-  a.r = r;
-  a.s = s;
-  a.pv = pv;
-  a.pb = pb;
-  a.Hs = Hs;
-  a.dots = dots;
-  a.state = state;
-  a.sw = sw;
-  a.bar = counters + 4;
-  a.u_ready = u_ready;
-  a.row_blocks = geo.row_blocks;
-  const int grid = geo.grid1 > geo.grid2 ? geo.grid1 : geo.grid2;
-  int rc = 1;
-  SNX_K_SWITCH(K, (rc = launch_cg_solve<double, KK>(a, grid, st)));
   return rc;
 }
 
@@ -2063,11 +1465,6 @@ using namespace snx;
 extern "C" {
 
 #ifdef SNX_TIMELINE
-int snx_debug_cg_timeline(unsigned long long *host_out) {
-  return cudaMemcpyFromSymbol(host_out, g_cg_timeline, sizeof(g_cg_timeline)) == cudaSuccess ? 0
-                                                                                             : 1;
-}
-
 int snx_debug_timeline(unsigned long long *host_out) {
   return cudaMemcpyFromSymbol(host_out, g_timeline, sizeof(g_timeline)) == cudaSuccess ? 0 : 1;
 }
@@ -2124,7 +1521,7 @@ int snx_class_probabilities(int dtype, const void *X, int64_t ldx, int64_t nrows
   const ProbsOut po{pred_out, stats_out};
   return rowpass(kProbs, dtype, X, ldx, nrows, p, K, labels, w, nullptr, 0.0, nullptr,
                  probs_out, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ws,
-                 ws_bytes, (cudaStream_t)stream, nullptr, &po);
+                 ws_bytes, (cudaStream_t)stream, &po);
 }
 
 int snx_objective_grad_acc(int dtype, const void *X, int64_t ldx, int64_t nrows, int32_t p,
@@ -2169,42 +1566,6 @@ int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
   return rowpass(kHessPrep, dtype, Xs, lds, nrows, p, K, nullptr, w, nullptr, 0.0, nullptr,
                  H_out, 1.0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, ws,
                  ws_bytes, st);
-}
-
-int snx_hess_apply_cg(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p,
-                      int32_t K, const void *H, double scale, double lam, int32_t t,
-                      int32_t max_iters, double *r, double *s, double *p_vec, double *p_best,
-                      double *Hs, double *dots, double *state, void *ws, size_t ws_bytes,
-                      void *stream) {
-  if (s == nullptr || Hs == nullptr || dots == nullptr || state == nullptr || r == nullptr ||
-      p_vec == nullptr || p_best == nullptr || (nrows > 0 && H == nullptr)) {
-    set_error("snx_hess_apply_cg: NULL argument");
-    return 1;
-  }
-  if (t < 0 || t >= max_iters) {
-    set_error("snx_hess_apply_cg: iteration %d outside [0, %d)", t, max_iters);
-    return 1;
-  }
-  if (nrows == 0) {  // no GEMM2 to fuse into: the separate update
-    if (snx_hess_apply(dtype, Xs, ldx, nrows, p, K, H, s, scale, lam, Hs, dots,
-                       snx_cg_done_flag(state, t), ws, ws_bytes, stream))
-      return 1;
-    return snx_cg_update(t, max_iters, (int64_t)K * p, Hs, dots, r, s, p_vec, p_best, state,
-                         stream);
-  }
-  const CgFuse cg{state, r, p_vec, p_best, t, max_iters};
-  return rowpass(kHessApply, dtype, Xs, ldx, nrows, p, K, nullptr, s, nullptr, 0.0, H, nullptr,
-                 scale, lam, s, nullptr, nullptr, Hs, dots, snx_cg_done_flag(state, t), ws,
-                 ws_bytes, (cudaStream_t)stream, &cg);
-}
-
-int snx_cg_solve(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,
-                 const void *H, double scale, double lam, const double *g, double theta,
-                 int32_t max_iters, double *r, double *s, double *p_vec, double *p_best,
-                 double *Hs, double *dots, double *state, void *ws, size_t ws_bytes,
-                 void *stream) {
-  return cg_solve(dtype, Xs, ldx, nrows, p, K, H, scale, lam, g, theta, max_iters, r, s, p_vec,
-                  p_best, Hs, dots, state, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_t p, int32_t K,

@@ -75,17 +75,3 @@ if dtype == "f64":
             if len(col):
                 print(f"  {nm} {names[ev]:13s} n={len(col):3d} med {(np.median(col) - b0) / 1e3:7.2f}"
                       f" max {(col.max() - b0) / 1e3:7.2f}")
-
-# persistent kernel (snx_cg_solve): phase stamps of iteration 5 per CTA
-if os.environ.get("SNX_CG_PERSISTENT", "1") != "0" and dtype == "f64":
-    cb = (ctypes.c_ulonglong * (160 * 10))()
-    assert lib.snx_debug_cg_timeline(cb) == 0
-    c = np.frombuffer(cb, dtype=np.uint64).reshape(160, 10).astype(np.int64)[:148]
-    c0 = c[:, 0][c[:, 0] > 0].min()
-    names = ["iter start", "gemm1 done", "gemm2 done", "B1 passed", "step1 done", "B2 passed",
-             "step2 done", "B3 passed"]
-    for ev, nm in enumerate(names):
-        col = c[:, ev]
-        col = col[col > 0]
-        print(f"  cg {nm:11s} med {(np.median(col) - c0) / 1e3:7.2f}  max {(col.max() - c0) / 1e3:7.2f}"
-              f"  min {(col.min() - c0) / 1e3:7.2f}")
