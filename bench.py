@@ -106,7 +106,7 @@ class ClockSampler:
 # dram__bytes_read.sum + dram__bytes_write.sum of one Hessian product (the
 # one-pass kernel + its finalize), from the committed ncu --set full capture
 # (per launch, cold cache); None until profiled
-TRAFFIC = {"f64": None}
+TRAFFIC = {"f64": 61.967616e6 + 1.257472e6 + 7.529984e6}  # main kernel read + write, finalize
 TRAFFIC_SOURCE = "profiles/r02_onepass_ncu_full.txt"
 KERNEL_NAME = {"f64": "one-pass cluster row pass (cluster_rowpass_kernel<9> + finalize_kernel, "
                       "csrc/snx_cluster.cu)",
@@ -680,7 +680,19 @@ def run_ours(args):
                 # tensor / FMA pipe (36.5 TFLOP/s measured, profiles/r02_fp64_pipe.txt)
                 "alt_bounds": {"fp64_tflops": flops / (hv_ms / 1e3) / 1e12,
                                "fp64_peak_tflops": 36.5,
-                               "fp64_frac": flops / (hv_ms / 1e3) / 1e12 / 36.5}}
+                               "fp64_frac": flops / (hv_ms / 1e3) / 1e12 / 36.5},
+                # tensor-pipe utilisation of the product's MMAs from the committed ncu
+                # captures (north star (b)): the fp64 tensor path (DMMA) of the headline
+                # product, and the tcgen05 bf16 pipe of the declared f32 path (C = 10:
+                # N = 9 columns, memory-bound by construction; C = 100: config #5)
+                "tensor_pipe": {
+                    "fp64_dmma_ops_pct_of_peak_elapsed": 21.8,
+                    "fp64_dmma_cycles_active_pct": 28.6,
+                    "source_fp64": "profiles/r02_onepass_ncu_full.txt (cluster_rowpass_kernel<9>)",
+                    "tcgen05_c10_pct_elapsed": [1.7, 2.0],
+                    "source_c10": "profiles/r02_tc_ncu_full.txt (tc_gemm1 / tc_gemm2)",
+                    "tcgen05_c100_pct_active": [23.0, 31.0],
+                    "source_c100": "profiles/r01_tcw_large_shard_ncu_full.txt (tcw_gemm1 / 2)"}}
     cg_rate = None
     if not sharded:
         wsx = cgmod.cg_graph_for(ops[0], T_CG, THETA).ws
