@@ -45,16 +45,18 @@ namespace clp {
 
 enum Mode { kPrep = 0, kApply = 1, kGrad = 2 };
 
-constexpr int kNW = 12;            // compute warps (3 per SM sub-partition)
+constexpr int kNW = 8;             // compute warps (2 per SM sub-partition)
 constexpr int kNC = kNW * 32;      // compute threads
 constexpr int kNTA = kNC + 96;     // column split: + producer + send warp + row-algebra warp
 constexpr int kNTR = kNC + 32;     // row split: + producer warp
 constexpr int kMaxK = 9;
 constexpr int kRA = 8;             // rows per block, column split
 constexpr int kRR = 8 * kNW;       // rows per block, row split (8 per warp)
-constexpr int kNMT = 8;            // column split: X^T U tiles (8 columns) per warp -> wc <= 768
+constexpr int kNMT = 12;           // column split: X^T U tiles (8 columns) per warp -> wc <= 768
 constexpr int kUP = 10;            // U row stride: classes 0..8 + pad (bank spread)
-constexpr int kNCH = 4;            // V phase: 16-column chunks per warp (wc <= 768, p <= 64)
+constexpr int kNCH = 6;            // V phase: 16-column chunks per warp (wc <= 768, p <= 64)
+constexpr int kLA = 2;             // column split: logits computed kLA blocks ahead of X^T U
+constexpr int kNB3 = kLA + 1;      // red / U rings (blocks in flight between V and X^T U)
 
 struct Args {
   const double *X;
@@ -117,6 +119,11 @@ __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// arrive on an mbarrier in a cluster peer's shared memory (release at cluster scope)
+__device__ __forceinline__ void mbar_remote_arrive(unsigned raddr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr)
+               : "memory");
 }
 // spin on a phase (test_wait polls: a thread parked in try_wait is not woken
 // promptly by remote complete-tx).  The phase completes only once the peers'
@@ -405,14 +412,15 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   rg.tiles = reinterpret_cast<double *>(smem + a.o_tiles);          // [S][R][WS]
   rg.side = reinterpret_cast<double *>(smem + a.o_side);            // [S][R][K] h | [S][R] int
   double *Q8 = reinterpret_cast<double *>(smem + a.o_q);            // [WQ] class-8 weights
-  double *Us = reinterpret_cast<double *>(smem + a.o_u);            // [2][R][kUP]
+  double *Us = reinterpret_cast<double *>(smem + a.o_u);            // [3][R][kUP]
   double *Vr = reinterpret_cast<double *>(smem + a.o_vr);           // [2][cs][R][K]
-  double *red = reinterpret_cast<double *>(smem + a.o_red);         // [2][NW][R][K]
+  double *red = reinterpret_cast<double *>(smem + a.o_red);         // [3][NW][R][K]
   rg.full = reinterpret_cast<uint64_t *>(smem + a.o_bar);
   rg.empty = rg.full + a.S;
   uint64_t *vfull = rg.empty + a.S;  // [2] peers' partial logits landed
-  uint64_t *redfull = vfull + 2;     // [2] compute warps' partials written
-  uint64_t *ufull = redfull + 2;     // [2] U rows ready
+  uint64_t *credit = vfull + 2;      // [2] every peer has consumed this CTA's slot (b & 1)
+  uint64_t *redfull = credit + 2;    // [3] compute warps' partials written
+  uint64_t *ufull = redfull + kNB3;  // [3] U rows ready
   __shared__ int sh_skip;
 
   // the warp index through a shuffle: provably warp-uniform for the compiler
@@ -433,12 +441,14 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
       mbar_init(&rg.full[s], 32);
       mbar_init(&rg.empty[s], kNW);
     }
-    mbar_init(&vfull[0], 1);
-    mbar_init(&vfull[1], 1);
-    mbar_init(&redfull[0], kNW);
-    mbar_init(&redfull[1], kNW);
-    mbar_init(&ufull[0], 32);
-    mbar_init(&ufull[1], 32);
+    for (int j = 0; j < 2; ++j) {
+      mbar_init(&vfull[j], 1);
+      mbar_init(&credit[j], a.cs);
+    }
+    for (int j = 0; j < kNB3; ++j) {
+      mbar_init(&redfull[j], kNW);
+      mbar_init(&ufull[j], 32);
+    }
     mbar_fence_init();
   }
   // zero the tile columns no bulk copy writes (the chunks / tiles read them)
@@ -473,10 +483,13 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     for (int b = 0; b < nb; ++b) {
       const int64_t r0 = row_lo + (int64_t)b * R;
       const int nr = (int)min((int64_t)R, row_hi - r0);
-      mbar_wait(&redfull[b & 1], (b >> 1) & 1);
+      mbar_wait(&redfull[b % kNB3], (b / kNB3) & 1);
+      // credit: every peer has read its slot (b & 1) of block b - 2 (so its
+      // receive buffer and vfull phase are free for block b)
+      if (b >= 2) mbar_wait(&credit[b & 1], ((b >> 1) - 1) & 1);
       __syncwarp();  // lanes leave a polling loop one by one: reconverge
       CL_TLX(b, 6);
-      const double *rb = red + (size_t)(b & 1) * kNW * R * K;
+      const double *rb = red + (size_t)(b % kNB3) * kNW * R * K;
       const unsigned vr_local = smem_u32(Vr + ((size_t)(b & 1) * cs + q) * R * K);
       const unsigned bar_local = smem_u32(&vfull[b & 1]);
       constexpr int EPL = (R * K + 31) / 32;
@@ -519,7 +532,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
       // all 8 rows at once: 4 lanes per row, lane `sub` owns classes sub,
       // sub + 4, sub + 8
       const double *vr = Vr + (size_t)(b & 1) * cs * R * K;
-      double *u = Us + (size_t)(b & 1) * R * kUP;
+      double *u = Us + (size_t)(b % kNB3) * R * kUP;
       const int row = lane >> 2, sub = lane & 3;
       const bool rv = row < nr;
       double z[3];
@@ -535,6 +548,9 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
         }
         z[j] = (pz[0] + pz[1]) + (pz[2] + pz[3]);
       }
+      // this CTA's receive slot (b & 1) is read: hand the credit to every sender
+      __syncwarp();
+      if (lane < cs) mbar_remote_arrive(mapa(smem_u32(&credit[b & 1]), (unsigned)lane));
       double uo[3] = {0.0, 0.0, 0.0};
       if (apply) {
         double hv[3], vw[3];
@@ -592,7 +608,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
         if (c < kUP) u[row * kUP + c] = (rv && c < K) ? uo[j] : 0.0;
       }
       CL_TLX(b, 9);
-      mbar_arrive(&ufull[b & 1]);  // each lane releases its own U stores
+      mbar_arrive(&ufull[b % kNB3]);  // each lane releases its own U stores
     }
     if (grad) {
       const double l = warp_allsum(loss_acc);
@@ -627,28 +643,31 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     const double *tile = rg.tiles + (size_t)s * R * WS;
     double c2[2], v8;
     vgroup<K>(tile + (size_t)g8 * WS + 4 * t4, Q8 + 4 * t4, qf, warp, kNW, nch, c2, v8);
-    double *rbw = red + (size_t)(b & 1) * kNW * R * K + (size_t)warp * R * K + g8 * K;
+    double *rbw = red + (size_t)(b % kNB3) * kNW * R * K + (size_t)warp * R * K + g8 * K;
     if (2 * t4 < K) rbw[2 * t4] = c2[0];
     if (2 * t4 + 1 < K) rbw[2 * t4 + 1] = c2[1];
     if (K == 9 && t4 == 0) rbw[8] = v8;
     __syncwarp();
-    if (lane == 0) mbar_arrive(&redfull[b & 1]);
+    if (lane == 0) mbar_arrive(&redfull[b % kNB3]);
   };
 
-  if (nb > 0) vphase(0);
+  // logits run kLA blocks ahead of X^T U: the exchange (warp sums, DSMEM
+  // push, peers' partials, row algebra) of a block has kLA blocks of compute
+  // to hide behind
+  for (int b = 0; b < kLA && b < nb; ++b) vphase(b);
   CL_TL(-1, 2);
   for (int b = 0; b < nb; ++b) {
     CL_TL(b, 0);
-    if (b + 1 < nb) vphase(b + 1);
+    if (b + kLA < nb) vphase(b + kLA);
     CL_TL(b, 1);
-    mbar_wait(&ufull[b & 1], (b >> 1) & 1);
+    mbar_wait(&ufull[b % kNB3], (b / kNB3) & 1);
     __syncwarp();
     CL_TL(b, 2);
     if (!prep) {
       const int64_t r0 = row_lo + (int64_t)b * R;
       const int nr = (int)min((int64_t)R, row_hi - r0);
-      xgroup<K, kNMT>(rg.tiles + (size_t)(b % S) * R * WS, WS, Us + (size_t)(b & 1) * R * kUP,
-                      nr, g8, t4, warp, kNW, nmt, acc, acc8);
+      xgroup<K, kNMT>(rg.tiles + (size_t)(b % S) * R * WS, WS,
+                      Us + (size_t)(b % kNB3) * R * kUP, nr, g8, t4, warp, kNW, nmt, acc, acc8);
     }
     CL_TL(b, 3);
     __syncwarp();
@@ -976,10 +995,10 @@ static void layout(Plan &pl, int S) {
   pl.o_q = take((size_t)pl.WQ * 8, 16);
   pl.o_side = take((size_t)S * pl.R * K * 8, 16);
   if (pl.split == 0) {
-    pl.o_u = take((size_t)2 * kRA * kUP * 8, 16);
+    pl.o_u = take((size_t)kNB3 * kRA * kUP * 8, 16);
     pl.o_vr = take((size_t)2 * pl.cs * kRA * K * 8, 16);
-    pl.o_red = take((size_t)2 * kNW * kRA * K * 8, 16);
-    pl.o_bar = take((size_t)(2 * S + 6) * 8, 8);
+    pl.o_red = take((size_t)kNB3 * kNW * kRA * K * 8, 16);
+    pl.o_bar = take((size_t)(2 * S + 4 + 2 * kNB3) * 8, 8);
   } else {
     pl.o_u = take((size_t)kNW * 8 * kUP * 8, 16);
     pl.o_vr = pl.o_red = 0;
@@ -1049,11 +1068,8 @@ static Plan make_plan(int P, int64_t nrows) {
     pl.R = kRA;
     pl.wc = wc;
     pl.WS = pl.WQ = (wc + 15) / 16 * 16 + 2;
-    int S = 4;
-    for (; S >= 3; --S) {
-      layout<K>(pl, S);
-      if (pl.smem <= cap_a<K>()) break;
-    }
+    int S = 4;  // kLA + 2: V(b + kLA), the tiles waiting for X^T U, one loading
+    layout<K>(pl, S);
     if (pl.smem > cap_a<K>()) continue;
     const int maxcl = max_clusters<K>(cs, pl.smem);
     const int64_t want = nrows > 0 ? (nrows + kRA - 1) / kRA : 1;
