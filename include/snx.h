@@ -189,8 +189,8 @@ int snx_axpby(double a, const double *x, double b, const double *y, int64_t d, d
 int snx_finish_hv(const double *v, double lam, int64_t d, double *out, double *dots,
                   const double *skip, void *stream);
 
-/* Device CG (cg.py:51-98).  state: (max_iters+2)*SNX_CG_SLOT + SNX_DOT_BLOCKS
- * doubles (the tail is reduction scratch); slot t
+/* Device CG (cg.py:51-98).  state: (max_iters+2)*SNX_CG_SLOT + 2*SNX_DOT_BLOCKS
+ * doubles (the tail is reduction scratch: r.r and s.s partials); slot t
  * holds the scalars entering iteration t: [rs, best_norm, done, iters,
  * converged, threshold, err, curvature].  Vectors r, s, p, p_best have d
  * entries.  snx_cg_init sets r = s = -g, p = 0, p_best = -g and slot 0; a
@@ -204,6 +204,19 @@ int snx_cg_init(const double *g, int64_t d, double theta, int32_t max_iters,
 int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
                   const double *dots, double *r, double *s, double *p, double *p_best,
                   double *state, void *stream);
+
+/* One CG iteration t with the one-pass product (fp64, K <= 9: snx_rowpass_fused):
+ * equivalent to snx_hess_apply_rows(s -> Hs, skip = done flag of slot t) +
+ * snx_cg_update(t, ...), with the product's finalize fused into the CG's first
+ * kernel -- the curvature s.Hs = scale * sum_rows V.U + lam * s.s is formed from
+ * per-cluster row sums of the product itself and the s.s partials snx_cg_init /
+ * snx_cg_update leave in the state (so the iterates agree with the unfused
+ * pair to rounding, not bitwise).  rows: NULL for the contiguous sample X. */
+int snx_hess_apply_cg_rows(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                           int64_t nrows, int32_t p, int32_t K, const void *H, double scale,
+                           double lam, int32_t t, int32_t max_iters, double *r, double *s,
+                           double *p_vec, double *p_best, double *Hs, double *state, void *ws,
+                           size_t ws_bytes, void *stream);
 
 /* Address of the "done" field of slot t (pass as snx_hess_apply's skip). */
 const double *snx_cg_done_flag(const double *state, int32_t t);

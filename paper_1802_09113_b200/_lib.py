@@ -45,6 +45,9 @@ SIGNATURES = {
     "snx_hess_apply_rows": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p,
                                      _c_p, _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_size,
                                      _c_p]),
+    "snx_hess_apply_cg_rows": (_c_int, [_c_int, _c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p,
+                                        _c_dbl, _c_dbl, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p,
+                                        _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_tc_ld": (_c_i64, [_c_i32]),
     "snx_hess_prepare_tc": (_c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                      _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_size, _c_p]),

@@ -62,7 +62,8 @@ class CgWorkspace:
         self.d, self.T = d, T
         self.vecs = torch.empty((5, d), **f64)
         self.r, self.s, self.p, self.pb, self.Hs = self.vecs
-        self.state = torch.zeros((T + 2) * _lib.CG_SLOT + _lib.DOT_BLOCKS, **f64)
+        # slots + two scratch rows of block partials (r.r, and s.s for the fused update)
+        self.state = torch.zeros((T + 2) * _lib.CG_SLOT + 2 * _lib.DOT_BLOCKS, **f64)
         self.dots = torch.empty(2 * _lib.DOT_BLOCKS, **f64)
 
     def slot(self, t):
@@ -77,7 +78,10 @@ def enqueue_cg(op, g, theta, T, ws):
     d = ws.d
     _lib.call("snx_cg_init", ptr(g), d, float(theta), T, ptr(ws.r), ptr(ws.s), ptr(ws.p),
               ptr(ws.pb), ptr(ws.state), stream_handle())
+    fused = getattr(op, "apply_cg_into", None)
     for t in range(T):
+        if fused is not None and fused(t, T, ws):  # product + CG update, finalize fused
+            continue
         op.apply_into(ws.s, ws.Hs, dots=ws.dots, skip=ws.done_ptr(t))
         _lib.call("snx_cg_update", t, T, d, ptr(ws.Hs), ptr(ws.dots), ptr(ws.r), ptr(ws.s),
                   ptr(ws.p), ptr(ws.pb), ptr(ws.state), stream_handle())

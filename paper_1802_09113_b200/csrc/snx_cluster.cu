@@ -563,6 +563,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
         const double sm = gsum<4>((vw[0] + vw[1]) + vw[2]);  // softmax.py:207 rowsum(VW)
 #pragma unroll
         for (int j = 0; j < 3; ++j) uo[j] = vw[j] - hv[j] * sm;
+        // curvature pieces: s.(X^T U) = sum over rows of V.U (the fused CG update)
+        if (rv) loss_acc += (z[0] * uo[0] + z[1] * uo[1]) + z[2] * uo[2];
       } else {
         // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
         double M = 0.0;
@@ -610,7 +612,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
       CL_TLX(b, 9);
       mbar_arrive(&ufull[b % kNB3]);  // each lane releases its own U stores
     }
-    if (grad) {
+    if (grad || apply) {  // apply: lossp[cl] = the cluster's sum of V.U (curvature)
       const double l = warp_allsum(loss_acc);
       unsigned long long cc = corr_acc;
 #pragma unroll
@@ -782,6 +784,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
         u0 = w0 - h0 * sm;
         u1 = w1 - h1 * sm;
         u8 = w8 - h8 * sm;
+        if (rv) loss_acc += (z0 * u0 + z1 * u1) + (t == 0 ? z8 * u8 : 0.0);  // V.U
       } else {
         // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
         double M = max_nan(c0v ? z0 : 0.0, c1v ? z1 : 0.0);
@@ -857,7 +860,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
       if (col < a.p) a.gp[(int64_t)cl * d + (int64_t)c * a.p + col] = sm;
     }
   }
-  if (grad) {
+  if (grad || apply) {  // apply: lossp[cl] = the CTA's sum of V.U (curvature)
     const double l = warp_allsum(loss_acc);
     unsigned long long cc = corr_acc;
 #pragma unroll
@@ -944,6 +947,74 @@ __global__ void __launch_bounds__(kFinThreads)
       if (corr_out != nullptr) *corr_out = (long long)cc;
     }
   }
+}
+
+// The CG iteration's first half (cg.py:77-86) fused with the product's
+// finalize: the curvature s.Hs = scale * sum_rows V.U + lam * s.s comes from
+// the kernel's per-cluster V.U sums (lossp) and the s.s partials cg_step2 /
+// cg_init leave in the state's second scratch row, so alpha is known before
+// any element of H s exists; then per element H s = scale * sum_cl gp + lam s
+// (written, for the record), p += alpha s, r -= alpha H s and the r.r block
+// partials cg_step2 reduces.  Same decisions as cg_step1_kernel (curvature test
+// of cg.py:79); the curvature's rounding differs from the dot of s and H s.
+__global__ void __launch_bounds__(kFinThreads)
+    cg_step1_rows_kernel(int t, int T, const double *__restrict__ gp, int ncl, int64_t d,
+                         int64_t epb, int F, double scale, double lam,
+                         const double *__restrict__ vup, const double *__restrict__ s, double *r,
+                         double *p, double *Hs, double *state) {
+  pdl_wait();
+  const double *st = slot(state, t);
+  if (st[kDone] != 0.0) return;
+  __shared__ double sh[kFinThreads / 32];
+  __shared__ double s_alpha;
+  __shared__ int s_bad;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    double v = 0.0;
+    for (int c = tid; c < ncl; c += 32) v += __ldcg(vup + c);
+    v = warp_allsum(v);
+    const double ss = warp_sum_partials(scratch(state, T) + kDotBlocks);
+    if (tid == 0) {
+      const double curv = __dadd_rn(__dmul_rn(scale, v), __dmul_rn(lam, ss));
+      s_bad = curv <= 1e-32 * ss;  // cg.py:16, :79
+      s_alpha = st[kRs] / curv;
+      if (s_bad && blockIdx.x == 0) {
+        slot(state, t + 1)[kErr] = 1.0;
+        slot(state, t + 1)[kCurv] = curv;
+      }
+    }
+  }
+  __syncthreads();
+  if (s_bad) return;
+  const double alpha = s_alpha;
+  const int64_t i = (int64_t)blockIdx.x * epb + tid / F;
+  const int f = tid % F;
+  const bool own = (tid / F) < epb && i < d;
+  double sum = 0.0;
+  if (own) {
+    int c = f;
+    for (; c + 7 * F < ncl; c += 8 * F) {
+      double v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = __ldcg(gp + (int64_t)(c + k * F) * d + i);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) sum += v[k];
+    }
+    for (; c < ncl; c += F) sum += __ldcg(gp + (int64_t)c * d + i);
+  }
+  for (int o = 1; o < F; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  double acc = 0.0;
+  if (own && f == 0) {
+    const double si = s[i];
+    const double o = __dadd_rn(__dmul_rn(scale, sum), __dmul_rn(lam, si));
+    Hs[i] = o;
+    p[i] = np_axpy(p[i], alpha, si);
+    const double ri = np_axmy(r[i], alpha, o);
+    r[i] = ri;
+    acc = ri * ri;
+  }
+  const double b = block_sum<kFinThreads>(acc, sh);
+  if (tid == 0) scratch(state, T)[blockIdx.x] = b;
 }
 
 // ---------------------------------------------------------------- host side
@@ -1277,6 +1348,53 @@ int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows,
                 mode == kGrad ? (const unsigned long long *)cw.corrp : nullptr,
                 mode == kGrad ? loss_out : nullptr, corr_out);
   return check_launch("one-pass finalize");
+}
+
+// One CG iteration t on the sampled Hessian (cg.py:77-96): the one-pass product
+// of s (skipped once the solve is done) without a finalize pass, the fused
+// cg_step1 above, then cg_step2.
+int cluster_cg_iteration(const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+                         int32_t p, int32_t K, const double *h, double scale, double lam, int t,
+                         int T, double *r, double *s, double *pv, double *pb, double *Hs,
+                         double *state, int early, void *ws, size_t ws_bytes, cudaStream_t st) {
+  using namespace clp;
+  const Plan pl = plan_for(SNX_F64, p, K, nrows);
+  if (!pl.ok || nrows < 1) {
+    set_error("snx: no one-pass plan for the fused CG iteration (p=%d K=%d rows=%lld)", p, K,
+              (long long)nrows);
+    return 1;
+  }
+  const ClWs cw = ws_layout(ws, pl, p, K);
+  if (ws == nullptr || ws_bytes < cw.total) {
+    set_error("snx: workspace too small for the one-pass row pass (%zu < %zu)", ws_bytes,
+              cw.total);
+    return 1;
+  }
+  Args a{};
+  a.X = X;
+  a.ldx = ldx;
+  a.rows = rows;
+  a.nrows = nrows;
+  a.p = p;
+  a.K = K;
+  a.mode = kApply;
+  a.w = s;
+  a.h = h;
+  a.gp = cw.gp;
+  a.lossp = cw.lossp;
+  a.corrp = cw.corrp;
+  a.skip = state + (size_t)t * SNX_CG_SLOT + kDone;
+  a.early = early;
+  if (launch_any(pl, K, a, st)) return 1;
+  const int64_t d = (int64_t)K * p;
+  const int64_t epb = (d + kDotBlocks - 1) / kDotBlocks;
+  int F = 1;
+  while (F < 32 && (int64_t)(2 * F) * epb <= kFinThreads) F *= 2;
+  launch_pdl_if(true, cg_step1_rows_kernel, dim3(kDotBlocks), dim3(kFinThreads), 0, st, t, T,
+                cw.gp, pl.ncl, d, epb, F, scale, lam, (const double *)cw.lossp,
+                (const double *)s, r, pv, Hs, state);
+  if (check_launch("cg_step1_rows")) return 1;
+  return launch_cg_step2(t, T, d, r, s, pv, pb, state, st);
 }
 
 }  // namespace snx

@@ -100,7 +100,14 @@ int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows,
                     double *dots, const double *skip, int early, void *ws, size_t ws_bytes,
                     cudaStream_t st);
 
+int cluster_cg_iteration(const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+                         int32_t p, int32_t K, const double *h, double scale, double lam, int t,
+                         int T, double *r, double *s, double *pv, double *pb, double *Hs,
+                         double *state, int early, void *ws, size_t ws_bytes, cudaStream_t st);
+
 // vector kernels (snx_vec.cu)
+int launch_cg_step2(int t, int T, int64_t d, const double *r, double *s, const double *p,
+                    double *pb, double *state, cudaStream_t st);
 int launch_prep_weights(int dtype, const double *w, const double *dir, double alpha, int K,
                         int p, int P, void *Wt, double *wsq_partials, unsigned *counter,
                         double *wsq_out, cudaStream_t st);

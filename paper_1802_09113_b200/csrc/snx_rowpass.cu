@@ -1580,6 +1580,31 @@ int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_
                  (cudaStream_t)stream);
 }
 
+int snx_hess_apply_cg_rows(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                           int64_t nrows, int32_t p, int32_t K, const void *H, double scale,
+                           double lam, int32_t t, int32_t max_iters, double *r, double *s,
+                           double *p_vec, double *p_best, double *Hs, double *state, void *ws,
+                           size_t ws_bytes, void *stream) {
+  if (s == nullptr || Hs == nullptr || state == nullptr || r == nullptr || p_vec == nullptr ||
+      p_best == nullptr || H == nullptr) {
+    set_error("snx_hess_apply_cg_rows: NULL argument");
+    return 1;
+  }
+  if (t < 0 || t >= max_iters) {
+    set_error("snx_hess_apply_cg_rows: iteration %d outside [0, %d)", t, max_iters);
+    return 1;
+  }
+  if (!cluster_supported(dtype, p, K) || nrows < 1) {
+    set_error("snx_hess_apply_cg_rows: fp64 data, K <= 9, nrows >= 1 only (snx_rowpass_fused)");
+    return 1;
+  }
+  if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
+  return cluster_cg_iteration(static_cast<const double *>(X), ldx, rows, nrows, p, K,
+                              static_cast<const double *>(H), scale, lam, t, max_iters, r, s,
+                              p_vec, p_best, Hs, state, gemm1_early_x() ? 1 : 0, ws, ws_bytes,
+                              (cudaStream_t)stream);
+}
+
 int snx_rowpass_fused(int dtype, int32_t p, int32_t K) {
   return cluster_supported(dtype, p, K) ? 1 : 0;
 }

@@ -215,7 +215,10 @@ __global__ void __launch_bounds__(kDotThreads)
     acc += gi * gi;
   }
   const double b = block_sum<kDotThreads>(acc, sh);
-  if (threadIdx.x == 0) scratch(state, max_iters)[blockIdx.x] = b;
+  if (threadIdx.x == 0) {
+    scratch(state, max_iters)[blockIdx.x] = b;
+    scratch(state, max_iters)[kDotBlocks + blockIdx.x] = b;  // s.s of s = -g (fused CG update)
+  }
   // zero every slot's flags (block 0)
   if (blockIdx.x == 0)
     for (int i = threadIdx.x; i < (max_iters + 2) * SNX_CG_SLOT; i += kDotThreads)
@@ -314,11 +317,21 @@ __global__ void __launch_bounds__(kDotThreads)
   const bool best = rn <= st[kBest];
   const bool conv = rn <= st[kThr];
   const double beta = rr / st[kRs];
+  double ss = 0.0;
   for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
        i += (int64_t)kDotBlocks * kDotThreads) {
     if (best) pb[i] = p[i];
-    if (!conv) s[i] = np_axpy(r[i], beta, s[i]);
+    if (!conv) {
+      const double si = np_axpy(r[i], beta, s[i]);
+      s[i] = si;
+      ss += si * si;
+    }
   }
+  // s.s partials of the new direction (the fused CG update's curvature, second
+  // scratch row; every block reaches this point: no early return above here)
+  __shared__ double sh2[kDotThreads / 32];
+  const double bs = block_sum<kDotThreads>(ss, sh2);
+  if (threadIdx.x == 0) scratch(state, max_iters)[kDotBlocks + blockIdx.x] = bs;
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     nx[kRs] = conv ? st[kRs] : rr;
     nx[kBest] = best ? rn : st[kBest];
@@ -654,6 +667,19 @@ int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
   launch_pdl(cg_step2_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, t, max_iters, d, r, s, p, p_best, state);
   return check_launch("cg_step2");
 }
+
+}  // extern "C"
+
+namespace snx {
+int launch_cg_step2(int t, int T, int64_t d, const double *r, double *s, const double *p,
+                    double *pb, double *state, cudaStream_t st) {
+  launch_pdl(cg_step2_kernel, dim3(kDotBlocks), dim3(kDotThreads), 0, st, t, T, d, r, s, p, pb,
+             state);
+  return check_launch("cg_step2");
+}
+}  // namespace snx
+
+extern "C" {
 
 const double *snx_cg_done_flag(const double *state, int32_t t) {
   return state + (size_t)t * SNX_CG_SLOT + kDone;

@@ -14,6 +14,7 @@ Vectors may be numpy arrays (results come back as numpy, the reference's
 contract) or CUDA torch tensors (results stay on the device).
 """
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -24,6 +25,7 @@ from .device import DeviceDataset, DeviceView, as_device, ptr, stream_handle, ve
 from .errors import DataError, DimensionError
 
 BLOCK_ROWS = 8192  # accepted for API parity (softmax.py:25); kernels tile rows themselves
+_UNFUSED = os.environ.get("SNX_CG_UNFUSED") == "1"  # A/B: unfused product + CG update
 
 
 @dataclass(frozen=True)
@@ -192,7 +194,7 @@ class HessianOperator:
         view, base, hb = self.view, self.view.base, self._bufs
         if getattr(base, "is_sparse", False):  # CSR data (csrc/snx_csr.cu)
             sparse.hess_prepare(self)
-        elif hb.fused:  # fp64, K <= 9: gather fused into the one-pass kernel
+        elif getattr(hb, "fused", False):  # fp64, K <= 9: gather fused into the one-pass kernel
             rows = None
             if view.rows is not None:
                 hb.rows[:view.n_rows].copy_(view.rows)  # fixed address: graph replays
@@ -223,7 +225,7 @@ class HessianOperator:
         base, hb = self.view.base, self._bufs
         if getattr(base, "is_sparse", False):
             return sparse.hess_apply(self, v, out, dots, skip)
-        if hb.fused:
+        if getattr(hb, "fused", False):
             rows = hb.rows if self.view.rows is not None else None
             _lib.call("snx_hess_apply_rows", base.code, ptr(base.X), base.ld, ptr(rows),
                       self.view.n_rows, self.p, self.view.K, ptr(hb.h), ptr(v), self.scale,
@@ -237,6 +239,23 @@ class HessianOperator:
                       self.p, self.view.K, ptr(hb.h), ptr(v), self.scale, self.lam, ptr(out),
                       ptr(dots), skip, *_ws(self.view), stream_handle())
         return out
+
+    def apply_cg_into(self, t, T, ws):
+        """CG iteration t on this operator with the product's finalize fused into
+        the CG update (snx_hess_apply_cg_rows; fp64, K <= 9).  False: the caller
+        runs apply_into + snx_cg_update.  SNX_CG_UNFUSED=1 forces the latter."""
+        hb, view = self._bufs, self.view
+        if not getattr(hb, "fused", False) or view.n_rows == 0 or _UNFUSED:
+            return False
+        if hb.owner is not self:
+            self._prepare()
+        base = view.base
+        rows = hb.rows if view.rows is not None else None
+        _lib.call("snx_hess_apply_cg_rows", base.code, ptr(base.X), base.ld, ptr(rows),
+                  view.n_rows, self.p, view.K, ptr(hb.h), self.scale, self.lam, t, T,
+                  ptr(ws.r), ptr(ws.s), ptr(ws.p), ptr(ws.pb), ptr(ws.Hs), ptr(ws.state),
+                  *_ws(view), stream_handle())
+        return True
 
     def apply(self, v):
         if isinstance(v, torch.Tensor) or np.asarray(v).shape == (self.dim,):
