@@ -55,7 +55,13 @@ constexpr int kRR = 8 * kNW;       // rows per block, row split (8 per warp)
 constexpr int kNMT = 12;           // column split: X^T U tiles (8 columns) per warp -> wc <= 768
 constexpr int kUP = 10;            // U row stride: classes 0..8 + pad (bank spread)
 constexpr int kNCH = 6;            // V phase: 16-column chunks per warp (wc <= 768, p <= 64)
-constexpr int kLA = 2;             // column split: logits computed kLA blocks ahead of X^T U
+#ifndef SNX_KLA
+#define SNX_KLA 2
+#endif
+constexpr int kLA = SNX_KLA;       // column split: logits computed kLA blocks ahead of X^T U
+#ifndef SNX_L2_KEEP
+#define SNX_L2_KEEP 1
+#endif
 constexpr int kNB3 = kLA + 1;      // red / U rings (blocks in flight between V and X^T U)
 
 struct Args {
@@ -115,6 +121,14 @@ __device__ __forceinline__ void cp_async4(void *dst, const void *src) {
 __device__ __forceinline__ void cp_async_mbar_arrive(uint64_t *bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
                : "memory");
+}
+// split-phase cluster barrier: arrive now, wait only where a peer's shared
+// memory is first addressed (every thread pairs each arrive with one wait)
+__device__ __forceinline__ void cluster_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -240,6 +254,8 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
                                         int *sh_skip) {
   const int S = a.S, WS = a.WS, WQ = a.WQ;
   const bool apply = a.mode == kApply, grad = a.mode == kGrad;
+  const bool keep = a.mode != kGrad && SNX_L2_KEEP;
+  const uint64_t pol = createpolicy_evict_last();
   constexpr int IPL = (R + 31) / 32;
   auto load_idx = [&](int b, int64_t(&dst)[IPL]) {
     const int64_t r0 = row_lo + (int64_t)b * R;
@@ -262,7 +278,13 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
 #pragma unroll
       for (int j = 0; j < IPL; ++j) {
         const int e = lane + 32 * j;
-        if (e < nr) bulk_g2s(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s]);
+        if (e < nr) {
+          if (keep)  // the sample rows are re-read by every product of the CG solve
+            bulk_g2s_hint(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s],
+                          pol);
+          else
+            bulk_g2s(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s]);
+        }
       }
     }
   };
@@ -328,12 +350,21 @@ __device__ __forceinline__ void load_qfrag(const Args &a, int c0, int wq, int g,
     }
   }
 }
+// class-8 row by cp.async (all copies in flight at once); the caller waits
+// with cp_async_wait_all() before the consumers' barrier
 template <int K>
 __device__ __forceinline__ void load_q8(const Args &a, double *q8, int c0, int wq, int n,
                                         int tid, int nthreads) {
   if constexpr (K == 9)
-    for (int j = tid; j < n; j += nthreads)
-      q8[j] = (j < wq && c0 + j < a.p) ? a.w[(int64_t)8 * a.p + c0 + j] : 0.0;
+    for (int j = tid; j < n; j += nthreads) {
+      if (j < wq && c0 + j < a.p)
+        cp_async8(q8 + j, a.w + (int64_t)8 * a.p + c0 + j);
+      else
+        q8[j] = 0.0;
+    }
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
 }
 
 // V phase of one 8-row group: C = X[8 rows][chunks] Q^T on m8n8k4, the 16
@@ -457,25 +488,41 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     rg.tiles[(size_t)r * WS + wq + j] = 0.0;
   }
   __syncthreads();
+  CL_TL(-1, 6);
   if (tid == 0 && nb > 0) {
     const int nr0 = (int)min((int64_t)R, row_hi - row_lo);
     mbar_arrive_expect_tx(&vfull[0], (unsigned)(cs * nr0 * K * 8));
   }
-  cluster_sync_all();  // peers' barriers initialised before any st.async
+  // peers' barriers must be initialised before any st.async / remote arrive:
+  // arrive here, wait only in the two warps that address peers (the others
+  // pair their wait before the exit barrier)
+  cluster_arrive();
+  CL_TL(-1, 7);
 
   if (warp == kNW) {  // ---------------------------------------- producer
     produce<R, K>(a, rg, row_lo, row_hi, nb, c0, wq, lane, &sh_skip);
+    cluster_wait();
     cluster_sync_all();
     return;
   }
   pdl_wait();  // the weights, h and the skip flag may be the predecessor's outputs
+  CL_TL(-1, 8);
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int nch = (wq + 15) >> 4, nmt = (wq + 7) >> 3;
+  double qf[kNCH][4];
+  if (warp < kNW) {  // weight loads in flight before the skip test
+    load_qfrag<K>(a, c0, wq, g8, t4, warp, kNW, nch, qf);
+    load_q8<K>(a, Q8, c0, wq, a.WQ, tid, kNC);
+  }
   if (a.skip != nullptr && *a.skip != 0.0) {
+    cp_async_wait_all();
+    cluster_wait();
     cluster_sync_all();
     return;
   }
-  const int g8 = lane >> 2, t4 = lane & 3;
 
   if (warp == kNW + 1) {  // ---------------------------------------- send warp
+    cluster_wait();
     // the CTA's partial logits of block b -> every peer's Vr[b & 1][q].  The
     // FP64 pipe is shared with the compute warps' MMA stream, so the dependent
     // FP64 chains here are kept short (independent elements per lane,
@@ -515,6 +562,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   }
 
   if (warp == kNW + 2) {  // ----------------------------- row-algebra warp
+    cluster_wait();
     double loss_acc = 0.0;
     unsigned long long corr_acc = 0;
     for (int b = 0; b < nb; ++b) {
@@ -627,10 +675,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   }
 
   // ---------------------------------------------------------- compute warps
-  const int nch = (wq + 15) >> 4, nmt = (wq + 7) >> 3;
-  double qf[kNCH][4];
-  load_qfrag<K>(a, c0, wq, g8, t4, warp, kNW, nch, qf);
-  load_q8<K>(a, Q8, c0, wq, a.WQ, tid, kNC);
+  CL_TL(-1, 9);
+  cp_async_wait_all();
   consumer_sync(kNC);
   CL_TL(-1, 1);
   double acc[kNMT][2], acc8[kNMT];
@@ -692,6 +738,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     }
   }
   CL_TL(-1, 4);
+  cluster_wait();      // the prologue's arrive
   cluster_sync_all();  // no CTA leaves while a peer may still address its smem
   CL_TL(-1, 5);
 }
@@ -749,6 +796,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
   double qf[kNCH][4];
   load_qfrag<K>(a, 0, wq, g, t, 0, 1, nch, qf);
   load_q8<K>(a, Q8, 0, wq, a.WQ, tid, kNC);
+  cp_async_wait_all();
   consumer_sync(kNC);
   double acc[NMT][2], acc8[NMT];
 #pragma unroll
@@ -964,29 +1012,13 @@ __global__ void __launch_bounds__(kFinThreads)
                          double *p, double *Hs, double *state) {
   pdl_wait();
   const double *st = slot(state, t);
-  if (st[kDone] != 0.0) return;
   __shared__ double sh[kFinThreads / 32];
   __shared__ double s_alpha;
   __shared__ int s_bad;
   const int tid = threadIdx.x;
-  if (tid < 32) {
-    double v = 0.0;
-    for (int c = tid; c < ncl; c += 32) v += __ldcg(vup + c);
-    v = warp_allsum(v);
-    const double ss = warp_sum_partials(scratch(state, T) + kDotBlocks);
-    if (tid == 0) {
-      const double curv = __dadd_rn(__dmul_rn(scale, v), __dmul_rn(lam, ss));
-      s_bad = curv <= 1e-32 * ss;  // cg.py:16, :79
-      s_alpha = st[kRs] / curv;
-      if (s_bad && blockIdx.x == 0) {
-        slot(state, t + 1)[kErr] = 1.0;
-        slot(state, t + 1)[kCurv] = curv;
-      }
-    }
-  }
-  __syncthreads();
-  if (s_bad) return;
-  const double alpha = s_alpha;
+  // every load that does not need alpha goes out first: the partials of H s
+  // and s, p, r overlap the curvature reduction below
+  const double done = st[kDone];
   const int64_t i = (int64_t)blockIdx.x * epb + tid / F;
   const int f = tid % F;
   const bool own = (tid / F) < epb && i < d;
@@ -1002,14 +1034,33 @@ __global__ void __launch_bounds__(kFinThreads)
     }
     for (; c < ncl; c += F) sum += __ldcg(gp + (int64_t)c * d + i);
   }
+  const bool lead = own && f == 0;
+  const double si = lead ? s[i] : 0.0, pi = lead ? p[i] : 0.0, ri0 = lead ? r[i] : 0.0;
+  if (tid < 32) {
+    double v = 0.0;
+    for (int c = tid; c < ncl; c += 32) v += __ldcg(vup + c);
+    v = warp_allsum(v);
+    const double ss = warp_sum_partials(scratch(state, T) + kDotBlocks);
+    if (tid == 0) {
+      const double curv = __dadd_rn(__dmul_rn(scale, v), __dmul_rn(lam, ss));
+      s_bad = curv <= 1e-32 * ss;  // cg.py:16, :79
+      s_alpha = st[kRs] / curv;
+      if (s_bad && blockIdx.x == 0 && done == 0.0) {
+        slot(state, t + 1)[kErr] = 1.0;
+        slot(state, t + 1)[kCurv] = curv;
+      }
+    }
+  }
   for (int o = 1; o < F; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  __syncthreads();
+  if (done != 0.0 || s_bad) return;
+  const double alpha = s_alpha;
   double acc = 0.0;
-  if (own && f == 0) {
-    const double si = s[i];
+  if (lead) {
     const double o = __dadd_rn(__dmul_rn(scale, sum), __dmul_rn(lam, si));
     Hs[i] = o;
-    p[i] = np_axpy(p[i], alpha, si);
-    const double ri = np_axmy(r[i], alpha, o);
+    p[i] = np_axpy(pi, alpha, si);
+    const double ri = np_axmy(ri0, alpha, o);
     r[i] = ri;
     acc = ri * ri;
   }

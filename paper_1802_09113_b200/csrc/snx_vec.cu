@@ -291,11 +291,21 @@ __global__ void __launch_bounds__(kDotThreads)
   if (threadIdx.x == 0) SNX_VTL(1, 0);
   const double *st = slot(state, t);
   double *nx = slot(state, t + 1);
-  if (st[kDone] != 0.0) {
+  // the first element's operands load alongside the flags and the r.r
+  // partials (no dependent round trip before the update)
+  const int64_t i0 = (int64_t)blockIdx.x * kDotThreads + threadIdx.x;
+  const double r0 = i0 < d ? r[i0] : 0.0, s0 = i0 < d ? s[i0] : 0.0, p0 = i0 < d ? p[i0] : 0.0;
+  const double done = st[kDone], err = nx[kErr];
+  __shared__ double s_rr;
+  if (threadIdx.x < 32) {
+    const double rr = warp_sum_partials(scratch(state, max_iters));
+    if (threadIdx.x == 0) s_rr = rr;
+  }
+  if (done != 0.0) {
     if (blockIdx.x == 0 && threadIdx.x < SNX_CG_SLOT) nx[threadIdx.x] = st[threadIdx.x];
     return;
   }
-  if (nx[kErr] != 0.0) {
+  if (err != 0.0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) {
       nx[kRs] = st[kRs];
       nx[kBest] = st[kBest];
@@ -306,11 +316,6 @@ __global__ void __launch_bounds__(kDotThreads)
     }
     return;
   }
-  __shared__ double s_rr;
-  if (threadIdx.x < 32) {
-    const double rr = warp_sum_partials(scratch(state, max_iters));
-    if (threadIdx.x == 0) s_rr = rr;
-  }
   __syncthreads();
   const double rr = s_rr;
   const double rn = sqrt(rr);
@@ -318,11 +323,11 @@ __global__ void __launch_bounds__(kDotThreads)
   const bool conv = rn <= st[kThr];
   const double beta = rr / st[kRs];
   double ss = 0.0;
-  for (int64_t i = (int64_t)blockIdx.x * kDotThreads + threadIdx.x; i < d;
-       i += (int64_t)kDotBlocks * kDotThreads) {
-    if (best) pb[i] = p[i];
+  for (int64_t i = i0; i < d; i += (int64_t)kDotBlocks * kDotThreads) {
+    const bool first = i == i0;
+    if (best) pb[i] = first ? p0 : p[i];
     if (!conv) {
-      const double si = np_axpy(r[i], beta, s[i]);
+      const double si = np_axpy(first ? r0 : r[i], beta, first ? s0 : s[i]);
       s[i] = si;
       ss += si * si;
     }

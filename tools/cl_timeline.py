@@ -6,8 +6,9 @@
 Events per block, compute thread 0: 0 loop top, 1 next block's V done,
 2 U(b) ready (waited), 3 X^T U(b) done; exchange-warp lane 0: 6 warp partials
 ready, 7 sent to the peers, 8 peers' partials in, 9 U rows written.  Kernel
-row (-1): 0 entry, 1 weights loaded, 2 first V done, 3 loop end, 4 partial
-written, 5 exit."""
+row (-1): 0 entry, 6 shared memory zeroed, 7 cluster barrier, 8 PDL wait
+done, 9 weight fragments in registers, 1 weights loaded, 2 first V done, 3 loop
+end, 4 partial written, 5 exit."""
 import ctypes
 import os
 import sys
@@ -56,9 +57,10 @@ if not used:
     sys.exit(f'{name}: no stamps (kernel not used for this shape?)')
 t0 = min(t[c, 0, 0] for c in used)
 rel = lambda v: (v - t0) / 1e3 if v else float("nan")  # noqa: E731
-print(f"{name}: {len(used)} CTAs; kernel rows: entry / Q loaded / first V / loop end / partial out / exit (us)")
+print(f"{name}: {len(used)} CTAs; kernel rows: entry / smem zeroed / cluster sync / pdl wait / "
+      "Q frags / Q loaded / first V / loop end / partial out / exit (us)")
 for c in used[:6] + used[-2:]:
-    print(f"cta {c:3d}: " + " ".join(f"{rel(t[c, 0, e]):7.2f}" for e in range(6)))
+    print(f"cta {c:3d}: " + " ".join(f"{rel(t[c, 0, e]):7.2f}" for e in (0, 6, 7, 8, 9, 1, 2, 3, 4, 5)))
 print("per block (cta 0): compute top / V(b+1) done / U(b) ready / XtU done | xchg red in / sent / peers in / U out")
 for b in range(NB - 1):
     if t[used[0], b + 1, 0] == 0 or t[used[0], b + 1, 0] < t0:

@@ -30,7 +30,24 @@ def timed(fn, reps, warm=3):
     return e0.elapsed_time(e1) / reps * 1e3
 
 
+def persist_l2():
+    """SNX_PERSIST=1: set aside the maximum persisting-L2 carve-out (what the
+    kernels' evict_last bulk copies need to stay resident)."""
+    import ctypes
+    import glob
+    torch.zeros(1, device="cuda")
+    lib = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "cuda_runtime",
+                                 "lib", "libcudart.so.*"))[0]
+    rt = ctypes.CDLL(lib)
+    v = ctypes.c_int()
+    rt.cudaDeviceGetAttribute(ctypes.byref(v), 108, 0)  # cudaDevAttrMaxPersistingL2CacheSize
+    rc = rt.cudaDeviceSetLimit(6, ctypes.c_size_t(v.value))  # cudaLimitPersistingL2CacheSize
+    print(f"persisting L2 carve-out {v.value / 2**20:.1f} MiB (rc {rc})")
+
+
 def main():
+    if os.environ.get("SNX_PERSIST"):
+        persist_l2()
     names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(SHAPES)
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
     tag = "two-pass" if os.environ.get("SNX_TWO_PASS") else "cluster"
