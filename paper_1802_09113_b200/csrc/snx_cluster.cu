@@ -59,9 +59,6 @@ constexpr int kNCH = 6;            // V phase: 16-column chunks per warp (wc <= 
 #define SNX_KLA 2
 #endif
 constexpr int kLA = SNX_KLA;       // column split: logits computed kLA blocks ahead of X^T U
-#ifndef SNX_L2_KEEP
-#define SNX_L2_KEEP 1
-#endif
 constexpr int kNB3 = kLA + 1;      // red / U rings (blocks in flight between V and X^T U)
 
 struct Args {
@@ -129,6 +126,12 @@ __device__ __forceinline__ void cluster_arrive() {
 }
 __device__ __forceinline__ void cluster_wait() {
   asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+// exit barrier of warps that issued no remote shared-memory operation: the
+// arrive need not order their (global) stores, so no GPU-scope fence
+__device__ __forceinline__ void cluster_sync_relaxed() {
+  asm volatile("barrier.cluster.arrive.relaxed.aligned;\n" ::: "memory");
+  asm volatile("barrier.cluster.wait.aligned;\n" ::: "memory");
 }
 __device__ __forceinline__ void cluster_sync_all() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
@@ -254,8 +257,6 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
                                         int *sh_skip) {
   const int S = a.S, WS = a.WS, WQ = a.WQ;
   const bool apply = a.mode == kApply, grad = a.mode == kGrad;
-  const bool keep = a.mode != kGrad && SNX_L2_KEEP;
-  const uint64_t pol = createpolicy_evict_last();
   constexpr int IPL = (R + 31) / 32;
   auto load_idx = [&](int b, int64_t(&dst)[IPL]) {
     const int64_t r0 = row_lo + (int64_t)b * R;
@@ -278,13 +279,7 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
 #pragma unroll
       for (int j = 0; j < IPL; ++j) {
         const int e = lane + 32 * j;
-        if (e < nr) {
-          if (keep)  // the sample rows are re-read by every product of the CG solve
-            bulk_g2s_hint(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s],
-                          pol);
-          else
-            bulk_g2s(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s]);
-        }
+        if (e < nr) bulk_g2s(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s]);
       }
     }
   };
@@ -502,7 +497,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   if (warp == kNW) {  // ---------------------------------------- producer
     produce<R, K>(a, rg, row_lo, row_hi, nb, c0, wq, lane, &sh_skip);
     cluster_wait();
-    cluster_sync_all();
+    cluster_sync_relaxed();
     return;
   }
   pdl_wait();  // the weights, h and the skip flag may be the predecessor's outputs
@@ -517,7 +512,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   if (a.skip != nullptr && *a.skip != 0.0) {
     cp_async_wait_all();
     cluster_wait();
-    cluster_sync_all();
+    cluster_sync_relaxed();
     return;
   }
 
@@ -701,7 +696,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
 
   // logits run kLA blocks ahead of X^T U: the exchange (warp sums, DSMEM
   // push, peers' partials, row algebra) of a block has kLA blocks of compute
-  // to hide behind
+  // to hide behind.  (Compile-time full-slice variants of the two MMA streams,
+  // without the per-chunk / per-tile bounds tests, measured 1 us slower.)
   for (int b = 0; b < kLA && b < nb; ++b) vphase(b);
   CL_TL(-1, 2);
   for (int b = 0; b < nb; ++b) {
@@ -738,8 +734,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     }
   }
   CL_TL(-1, 4);
-  cluster_wait();      // the prologue's arrive
-  cluster_sync_all();  // no CTA leaves while a peer may still address its smem
+  cluster_wait();          // the prologue's arrive
+  cluster_sync_relaxed();  // no CTA leaves while a peer may still address its smem
   CL_TL(-1, 5);
 }
 

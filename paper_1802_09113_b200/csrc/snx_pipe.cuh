@@ -65,21 +65,6 @@ __device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned by
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
-// the same with an L2 eviction-priority policy (createpolicy_evict_last())
-__device__ __forceinline__ void bulk_g2s_hint(void *dst, const void *src, unsigned bytes,
-                                              uint64_t *bar, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-      "[%0], [%1], %2, [%3], %4;\n" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t createpolicy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
-
 // named barrier over the `n` consumer threads (id 1; id 0 is __syncthreads)
 __device__ __forceinline__ void consumer_sync(unsigned n) {
   asm volatile("bar.sync 1, %0;\n" ::"r"(n) : "memory");
