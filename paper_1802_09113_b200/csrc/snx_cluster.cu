@@ -142,6 +142,12 @@ __device__ __forceinline__ void mbar_remote_arrive(unsigned raddr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr)
                : "memory");
 }
+// Relaxed remote arrive (no GPU-scope fence): for a credit that releases only
+// shared-memory reads whose values the caller has already consumed.
+__device__ __forceinline__ void mbar_remote_arrive_relaxed(unsigned raddr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(raddr)
+               : "memory");
+}
 // spin on a phase (test_wait polls: a thread parked in try_wait is not woken
 // promptly by remote complete-tx).  The phase completes only once the peers'
 // st.async bytes have landed in this CTA's shared memory.
@@ -587,13 +593,12 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
 #pragma unroll
           for (int pq = 0; pq < 4; ++pq)
             if (pq < cs) pz[pq] = vr[(pq * R + row) * K + c];
-          for (int pq = 4; pq < cs; ++pq) pz[pq & 3] += vr[(pq * R + row) * K + c];
+#pragma unroll
+          for (int pq = 4; pq < 8; ++pq)
+            if (pq < cs) pz[pq - 4] += vr[(pq * R + row) * K + c];
         }
         z[j] = (pz[0] + pz[1]) + (pz[2] + pz[3]);
       }
-      // this CTA's receive slot (b & 1) is read: hand the credit to every sender
-      __syncwarp();
-      if (lane < cs) mbar_remote_arrive(mapa(smem_u32(&credit[b & 1]), (unsigned)lane));
       double uo[3] = {0.0, 0.0, 0.0};
       if (apply) {
         double hv[3], vw[3];
@@ -654,6 +659,11 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
       }
       CL_TLX(b, 9);
       mbar_arrive(&ufull[b % kNB3]);  // each lane releases its own U stores
+      // this CTA's receive slot (b & 1) is read -- the U stores above consumed
+      // every value read, so those loads have completed: hand the credit to
+      // every sender with a relaxed arrive (no GPU-scope fence per block)
+      __syncwarp();
+      if (lane < cs) mbar_remote_arrive_relaxed(mapa(smem_u32(&credit[b & 1]), (unsigned)lane));
     }
     if (grad || apply) {  // apply: lossp[cl] = the cluster's sum of V.U (curvature)
       const double l = warp_allsum(loss_acc);
@@ -940,6 +950,7 @@ __global__ void __launch_bounds__(kFinThreads)
                     double *__restrict__ out, double *dots, const double *skip,
                     const double *lossp, const unsigned long long *corrp, double *loss_out,
                     long long *corr_out) {
+  pdl_trigger();  // the next row pass may start staging its X tiles (it waits for this grid)
   pdl_wait();
   if (skip != nullptr && *skip != 0.0) return;
   __shared__ double sh[kFinThreads / 32];
@@ -1006,6 +1017,7 @@ __global__ void __launch_bounds__(kFinThreads)
                          int64_t epb, int F, double scale, double lam,
                          const double *__restrict__ vup, const double *__restrict__ s, double *r,
                          double *p, double *Hs, double *state) {
+  pdl_trigger();  // cg_step2, then the next row pass, may launch early (both wait)
   pdl_wait();
   const double *st = slot(state, t);
   __shared__ double sh[kFinThreads / 32];
