@@ -47,7 +47,6 @@ enum Mode { kPrep = 0, kApply = 1, kGrad = 2 };
 
 constexpr int kNW = 8;             // compute warps (2 per SM sub-partition)
 constexpr int kNC = kNW * 32;      // compute threads
-constexpr int kNTA = kNC + 96;     // column split: + producer + send warp + row-algebra warp
 constexpr int kNTR = kNC + 32;     // row split: + producer warp
 constexpr int kMaxK = 9;
 constexpr int kRA = 8;             // rows per block, column split
@@ -55,6 +54,12 @@ constexpr int kRR = 8 * kNW;       // rows per block, row split (8 per warp)
 constexpr int kNMT = 12;           // column split: X^T U tiles (8 columns) per warp -> wc <= 768
 constexpr int kUP = 10;            // U row stride: classes 0..8 + pad (bank spread)
 constexpr int kNCH = 6;            // V phase: 16-column chunks per warp (wc <= 768, p <= 64)
+constexpr int kNWA = 8;            // column split: compute warps (16 measured slower: the
+                                   // larger partial ring forces 8-CTA clusters at p = 3072)
+constexpr int kNCA = kNWA * 32;
+constexpr int kNMTA = 96 / kNWA;   // column split: X^T U tiles per warp (wc <= 768)
+constexpr int kNCHA = 48 / kNWA;   // column split: V chunks per warp
+constexpr int kNTA = kNCA + 96;    // column split: + producer + send warp + row-algebra warp
 #ifndef SNX_KLA
 #define SNX_KLA 2
 #endif
@@ -234,7 +239,7 @@ __device__ __forceinline__ void cl_stamp(int b, int ev) {
   } while (0)
 #define CL_TLX(b, ev)                                                  \
   do {                                                                 \
-    if (threadIdx.x == kNC + 32 || threadIdx.x == kNC + 64) cl_stamp((b), (ev)); \
+    if (threadIdx.x == kNCA + 32 || threadIdx.x == kNCA + 64) cl_stamp((b), (ev)); \
   } while (0)
 #else
 #define CL_TL(b, ev) \
@@ -338,11 +343,11 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
 // w[g][16 ch + 4 t + s] (s = 0..3) of its NCH chunks (zero past the slice, past
 // p, or for classes >= K).  Class 8 (K = 9) is a shared-memory row (smem
 // broadcasts: the four lanes of a group read one 16-B pair).
-template <int K>
+template <int K, int NCH>
 __device__ __forceinline__ void load_qfrag(const Args &a, int c0, int wq, int g, int t, int ch0,
-                                           int step, int nch, double (&qf)[kNCH][4]) {
+                                           int step, int nch, double (&qf)[NCH][4]) {
 #pragma unroll
-  for (int i = 0; i < kNCH; ++i) {
+  for (int i = 0; i < NCH; ++i) {
     const int ch = ch0 + step * i;
 #pragma unroll
     for (int s = 0; s < 4; ++s) {
@@ -373,14 +378,14 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // lane's A and B values are 2 contiguous 16-B loads each).  Returns the lane's
 // C = (V[g][2t], V[g][2t+1]) and v8 = the row's class-8 logit partial (summed
 // over the 4 lanes of the group, K == 9).
-template <int K>
+template <int K, int NCH>
 __device__ __forceinline__ void vgroup(const double *xrow, const double *q8row,
-                                       const double (&qf)[kNCH][4], int ch0, int step, int nch,
+                                       const double (&qf)[NCH][4], int ch0, int step, int nch,
                                        double (&c2)[2], double &v8) {
   // two independent accumulator chains (steps 0,1 and 2,3), added at the end
   double ca[2] = {0.0, 0.0}, cb[2] = {0.0, 0.0}, va = 0.0, vb = 0.0;
 #pragma unroll
-  for (int i = 0; i < kNCH; ++i) {
+  for (int i = 0; i < NCH; ++i) {
     const int ch = ch0 + step * i;
     if (ch < nch) {
       const double2 xa = *reinterpret_cast<const double2 *>(xrow + 16 * ch);
@@ -471,14 +476,14 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   if (tid == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&rg.full[s], 32);
-      mbar_init(&rg.empty[s], kNW);
+      mbar_init(&rg.empty[s], kNWA);
     }
     for (int j = 0; j < 2; ++j) {
       mbar_init(&vfull[j], 1);
       mbar_init(&credit[j], a.cs);
     }
     for (int j = 0; j < kNB3; ++j) {
-      mbar_init(&redfull[j], kNW);
+      mbar_init(&redfull[j], kNWA);
       mbar_init(&ufull[j], 32);
     }
     mbar_fence_init();
@@ -500,7 +505,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   cluster_arrive();
   CL_TL(-1, 7);
 
-  if (warp == kNW) {  // ---------------------------------------- producer
+  if (warp == kNWA) {  // ---------------------------------------- producer
     produce<R, K>(a, rg, row_lo, row_hi, nb, c0, wq, lane, &sh_skip);
     cluster_wait();
     cluster_sync_relaxed();
@@ -510,10 +515,10 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   CL_TL(-1, 8);
   const int g8 = lane >> 2, t4 = lane & 3;
   const int nch = (wq + 15) >> 4, nmt = (wq + 7) >> 3;
-  double qf[kNCH][4];
-  if (warp < kNW) {  // weight loads in flight before the skip test
-    load_qfrag<K>(a, c0, wq, g8, t4, warp, kNW, nch, qf);
-    load_q8<K>(a, Q8, c0, wq, a.WQ, tid, kNC);
+  double qf[kNCHA][4];
+  if (warp < kNWA) {  // weight loads in flight before the skip test
+    load_qfrag<K, kNCHA>(a, c0, wq, g8, t4, warp, kNWA, nch, qf);
+    load_q8<K>(a, Q8, c0, wq, a.WQ, tid, kNCA);
   }
   if (a.skip != nullptr && *a.skip != 0.0) {
     cp_async_wait_all();
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     return;
   }
 
-  if (warp == kNW + 1) {  // ---------------------------------------- send warp
+  if (warp == kNWA + 1) {  // ---------------------------------------- send warp
     cluster_wait();
     // the CTA's partial logits of block b -> every peer's Vr[b & 1][q].  The
     // FP64 pipe is shared with the compute warps' MMA stream, so the dependent
@@ -537,21 +542,27 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
       if (b >= 2) mbar_wait(&credit[b & 1], ((b >> 1) - 1) & 1);
       __syncwarp();  // lanes leave a polling loop one by one: reconverge
       CL_TLX(b, 6);
-      const double *rb = red + (size_t)(b % kNB3) * kNW * R * K;
+      const double *rb = red + (size_t)(b % kNB3) * kNWA * R * K;
       const unsigned vr_local = smem_u32(Vr + ((size_t)(b & 1) * cs + q) * R * K);
       const unsigned bar_local = smem_u32(&vfull[b & 1]);
       constexpr int EPL = (R * K + 31) / 32;
-      double v[EPL][kNW];
+      double tot[EPL];
 #pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        const int e = lane + 32 * j;
+      for (int h = 0; h < kNWA / 8; ++h) {  // eight warps' partials at a time
+        double v[EPL][8];
 #pragma unroll
-        for (int w = 0; w < kNW; ++w) v[j][w] = e < nr * K ? rb[w * R * K + e] : 0.0;
+        for (int j = 0; j < EPL; ++j) {
+          const int e = lane + 32 * j;
+#pragma unroll
+          for (int w = 0; w < 8; ++w) v[j][w] = e < nr * K ? rb[(8 * h + w) * R * K + e] : 0.0;
+        }
+#pragma unroll
+        for (int j = 0; j < EPL; ++j) tot[j] = h == 0 ? tree_sum<0, 8>(v[j]) : tot[j] + tree_sum<0, 8>(v[j]);
       }
 #pragma unroll
       for (int j = 0; j < EPL; ++j) {
         const int e = lane + 32 * j;
-        const double sm = tree_sum<0, kNW>(v[j]);
+        const double sm = tot[j];
         if (e < nr * K)
           for (int pq = 0; pq < cs; ++pq)
             st_async(mapa(vr_local + e * 8, pq), sm, mapa(bar_local, pq));
@@ -562,7 +573,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     return;
   }
 
-  if (warp == kNW + 2) {  // ----------------------------- row-algebra warp
+  if (warp == kNWA + 2) {  // ----------------------------- row-algebra warp
     cluster_wait();
     double loss_acc = 0.0;
     unsigned long long corr_acc = 0;
@@ -682,11 +693,11 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   // ---------------------------------------------------------- compute warps
   CL_TL(-1, 9);
   cp_async_wait_all();
-  consumer_sync(kNC);
+  consumer_sync(kNCA);
   CL_TL(-1, 1);
-  double acc[kNMT][2], acc8[kNMT];
+  double acc[kNMTA][2], acc8[kNMTA];
 #pragma unroll
-  for (int m = 0; m < kNMT; ++m) acc[m][0] = acc[m][1] = acc8[m] = 0.0;
+  for (int m = 0; m < kNMTA; ++m) acc[m][0] = acc[m][1] = acc8[m] = 0.0;
 
   // partial logits of block b (k split over the warps) -> red[b & 1][warp]
   auto vphase = [&](int b) {
@@ -695,8 +706,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     __syncwarp();  // reconverge before the warp-wide MMAs
     const double *tile = rg.tiles + (size_t)s * R * WS;
     double c2[2], v8;
-    vgroup<K>(tile + (size_t)g8 * WS + 4 * t4, Q8 + 4 * t4, qf, warp, kNW, nch, c2, v8);
-    double *rbw = red + (size_t)(b % kNB3) * kNW * R * K + (size_t)warp * R * K + g8 * K;
+    vgroup<K, kNCHA>(tile + (size_t)g8 * WS + 4 * t4, Q8 + 4 * t4, qf, warp, kNWA, nch, c2, v8);
+    double *rbw = red + (size_t)(b % kNB3) * kNWA * R * K + (size_t)warp * R * K + g8 * K;
     if (2 * t4 < K) rbw[2 * t4] = c2[0];
     if (2 * t4 + 1 < K) rbw[2 * t4 + 1] = c2[1];
     if (K == 9 && t4 == 0) rbw[8] = v8;
@@ -720,8 +731,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     if (!prep) {
       const int64_t r0 = row_lo + (int64_t)b * R;
       const int nr = (int)min((int64_t)R, row_hi - r0);
-      xgroup<K, kNMT>(rg.tiles + (size_t)(b % S) * R * WS, WS,
-                      Us + (size_t)(b % kNB3) * R * kUP, nr, g8, t4, warp, kNW, nmt, acc, acc8);
+      xgroup<K, kNMTA>(rg.tiles + (size_t)(b % S) * R * WS, WS,
+                      Us + (size_t)(b % kNB3) * R * kUP, nr, g8, t4, warp, kNWA, nmt, acc, acc8);
     }
     CL_TL(b, 3);
     __syncwarp();
@@ -732,8 +743,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     const int64_t d = (int64_t)K * a.p;
     double *gq = a.gp + (int64_t)cl * d;
 #pragma unroll
-    for (int m = 0; m < kNMT; ++m) {
-      const int mt = warp + kNW * m;
+    for (int m = 0; m < kNMTA; ++m) {
+      const int mt = warp + kNWA * m;
       const double s8 = K == 9 ? gsum<4>(acc8[m]) : 0.0;
       const int col = 8 * mt + g8, gc = c0 + col;
       if (mt < nmt && col < wq && gc < a.p) {
@@ -800,7 +811,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
   const int g = lane >> 2, t = lane & 3;
   const int nch = (wq + 15) >> 4, nmt = (wq + 7) >> 3;
   double qf[kNCH][4];
-  load_qfrag<K>(a, 0, wq, g, t, 0, 1, nch, qf);
+  load_qfrag<K, kNCH>(a, 0, wq, g, t, 0, 1, nch, qf);
   load_q8<K>(a, Q8, 0, wq, a.WQ, tid, kNC);
   cp_async_wait_all();
   consumer_sync(kNC);
@@ -823,7 +834,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
     if (ng > 0) {
       const double *tile = rg.tiles + (size_t)s * R * WS + (size_t)gr0 * WS;
       double c2[2], v8;
-      vgroup<K>(tile + (size_t)g * WS + 4 * t, Q8 + 4 * t, qf, 0, 1, nch, c2, v8);
+      vgroup<K, kNCH>(tile + (size_t)g * WS + 4 * t, Q8 + 4 * t, qf, 0, 1, nch, c2, v8);
       // row algebra: lane (g, t) holds classes 2t, 2t+1 of row g (+ class 8)
       const int row = gr0 + g;
       const bool rv = g < ng;
@@ -1127,7 +1138,7 @@ static void layout(Plan &pl, int S) {
   if (pl.split == 0) {
     pl.o_u = take((size_t)kNB3 * kRA * kUP * 8, 16);
     pl.o_vr = take((size_t)2 * pl.cs * kRA * K * 8, 16);
-    pl.o_red = take((size_t)kNB3 * kNW * kRA * K * 8, 16);
+    pl.o_red = take((size_t)kNB3 * kNWA * kRA * K * 8, 16);
     pl.o_bar = take((size_t)(2 * S + 4 + 2 * kNB3) * 8, 8);
   } else {
     pl.o_u = take((size_t)kNW * 8 * kUP * 8, 16);
@@ -1191,7 +1202,7 @@ static Plan make_plan(int P, int64_t nrows) {
   }
   for (int cs : {1, 2, 4, 8}) {
     const int wc = ((P + cs - 1) / cs + 1) & ~1;
-    if ((wc + 7) / 8 > kNW * kNMT) continue;  // > 768 columns per CTA
+    if ((wc + 7) / 8 > kNWA * kNMTA) continue;  // > 768 columns per CTA
     pl = Plan{};
     pl.split = 0;
     pl.cs = cs;
