@@ -65,6 +65,8 @@ constexpr int kNTA = kNCA + 96;    // column split: + producer + send warp + row
 #endif
 constexpr int kLA = SNX_KLA;       // column split: logits computed kLA blocks ahead of X^T U
 constexpr int kNB3 = kLA + 1;      // red / U rings (blocks in flight between V and X^T U)
+constexpr int kSA = kLA + 2;       // column split: ring stages (V(b + kLA), the tiles waiting
+                                   // for X^T U, one loading)
 
 struct Args {
   const double *X;
@@ -439,6 +441,140 @@ __device__ __forceinline__ void xgroup(const double *x0, int WS, const double *u
   }
 }
 
+// Send warp, one block: the CTA's partial logits (the compute warps' partials
+// summed in a fixed tree) -> every peer's Vr[B & 1][q] by st.async, counted on
+// the peer's vfull[B & 1].  B: the block's position in the CTA's ring sequence.
+template <int K>
+__device__ __forceinline__ void send_block(const double *red, double *Vr, uint64_t *vfull,
+                                           unsigned q, int cs, int lane, int64_t B, int nr) {
+  constexpr int R = kRA;
+  const double *rb = red + (size_t)(B % kNB3) * kNWA * R * K;
+  const unsigned vr_local = smem_u32(Vr + ((size_t)(B & 1) * cs + q) * R * K);
+  const unsigned bar_local = smem_u32(&vfull[B & 1]);
+  constexpr int EPL = (R * K + 31) / 32;
+  double tot[EPL];
+#pragma unroll
+  for (int h = 0; h < kNWA / 8; ++h) {  // eight warps' partials at a time
+    double v[EPL][8];
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) {
+      const int e = lane + 32 * j;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) v[j][w] = e < nr * K ? rb[(8 * h + w) * R * K + e] : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < EPL; ++j) tot[j] = h == 0 ? tree_sum<0, 8>(v[j]) : tot[j] + tree_sum<0, 8>(v[j]);
+  }
+#pragma unroll
+  for (int j = 0; j < EPL; ++j) {
+    const int e = lane + 32 * j;
+    const double sm = tot[j];
+    if (e < nr * K)
+      for (int pq = 0; pq < cs; ++pq)
+        st_async(mapa(vr_local + e * 8, pq), sm, mapa(bar_local, pq));
+  }
+}
+
+// Row-algebra warp, one block (lanes: 4 per row): z = the peers' partial
+// logits summed in rank order, then the mode's row algebra (apply: U =
+// diag(h) z - h (h.z), the V.U curvature sum; prep: h; grad: residual, loss,
+// accuracy), U rows -> Us[B % 3], ufull[B % 3], and the credit for Vr[B & 1]
+// to every peer.
+template <int K>
+__device__ __forceinline__ void rows_block(const Args &a, const Ring &rg, const double *Vr,
+                                           double *Us, uint64_t *ufull, uint64_t *credit,
+                                           unsigned q, int cs, int lane, int64_t B, int s,
+                                           int64_t r0, int nr, double &loss_acc,
+                                           unsigned long long &corr_acc) {
+  constexpr int R = kRA;
+  const bool apply = a.mode == kApply, prep = a.mode == kPrep;
+  // all 8 rows at once: 4 lanes per row, lane `sub` owns classes sub,
+  // sub + 4, sub + 8
+  const double *vr = Vr + (size_t)(B & 1) * cs * R * K;
+  double *u = Us + (size_t)(B % kNB3) * R * kUP;
+  const int row = lane >> 2, sub = lane & 3;
+  const bool rv = row < nr;
+  double z[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int c = sub + 4 * j;
+    double pz[4] = {0.0, 0.0, 0.0, 0.0};
+    if (rv && c < K) {
+#pragma unroll
+      for (int pq = 0; pq < 4; ++pq)
+        if (pq < cs) pz[pq] = vr[(pq * R + row) * K + c];
+#pragma unroll
+      for (int pq = 4; pq < 8; ++pq)
+        if (pq < cs) pz[pq - 4] += vr[(pq * R + row) * K + c];
+    }
+    z[j] = (pz[0] + pz[1]) + (pz[2] + pz[3]);
+  }
+  double uo[3] = {0.0, 0.0, 0.0};
+  if (apply) {
+    double hv[3], vw[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const int c = sub + 4 * j;
+      hv[j] = (rv && c < K) ? rg.side[((size_t)s * R + row) * K + c] : 0.0;
+      vw[j] = z[j] * hv[j];
+    }
+    const double sm = gsum<4>((vw[0] + vw[1]) + vw[2]);  // softmax.py:207 rowsum(VW)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) uo[j] = vw[j] - hv[j] * sm;
+    // curvature pieces: s.(X^T U) = sum over rows of V.U (the fused CG update)
+    if (rv) loss_acc += (z[0] * uo[0] + z[1] * uo[1]) + z[2] * uo[2];
+  } else {
+    // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
+    double M = 0.0;
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      if (sub + 4 * j < K) M = max_nan(M, z[j]);
+    M = gmax_nan<4>(M);
+    double E[3];
+#pragma unroll
+    for (int j = 0; j < 3; ++j) E[j] = (sub + 4 * j < K) ? exp(z[j] - M) : 0.0;
+    const double eM = exp(-M);
+    const double alpha = eM + gsum<4>((E[0] + E[1]) + E[2]);
+    if (prep) {
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (rv && sub + 4 * j < K && q == 0) a.hout[(r0 + row) * K + sub + 4 * j] = E[j] / alpha;
+    } else {
+      // grad: residual (softmax.py:157-161), loss (:134), accuracy (:224-247)
+      const int y = rv ? reinterpret_cast<const int *>(rg.side)[s * R + row] : -1;
+      double pr[3], lin = 0.0;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const int c = sub + 4 * j;
+        pr[j] = E[j] / alpha;
+        uo[j] = pr[j] - (c == y ? 1.0 : 0.0);
+        if (c < K && c == y) lin = z[j];
+      }
+      lin = gsum<4>(lin);
+      if (rv && sub == 0 && q == 0) loss_acc += (M + log(alpha)) - lin;
+      double bv = -INFINITY;
+      int bi = K + 1;
+#pragma unroll
+      for (int j = 0; j < 3; ++j)
+        if (sub + 4 * j < K) amax_take(bv, bi, pr[j], sub + 4 * j);
+      gargmax<4>(bv, bi);
+      amax_take(bv, bi, eM / alpha, K);  // the reference class
+      if (rv && sub == 0 && q == 0 && bi == y) corr_acc += 1ull;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    const int c = sub + 4 * j;
+    if (c < kUP) u[row * kUP + c] = (rv && c < K) ? uo[j] : 0.0;
+  }
+  mbar_arrive(&ufull[B % kNB3]);  // each lane releases its own U stores
+  // this CTA's receive slot (B & 1) is read -- the U stores above consumed
+  // every value read, so those loads have completed: hand the credit to
+  // every sender with a relaxed arrive (no GPU-scope fence per block)
+  __syncwarp();
+  if (lane < cs) mbar_remote_arrive_relaxed(mapa(smem_u32(&credit[B & 1]), (unsigned)lane));
+}
+
 // ---------------------------------------------------------------- column split
 template <int K>
 __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_constant__ Args a) {
@@ -463,7 +599,8 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
   // the warp index through a shuffle: provably warp-uniform for the compiler
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
-  const int S = a.S, WS = a.WS, cs = a.cs;
+  constexpr int S = kSA;
+  const int WS = a.WS, cs = a.cs;
   CL_TL(-1, 0);
   const unsigned q = cluster_rank();
   const int cl = (int)cluster_id();
@@ -542,31 +679,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
       if (b >= 2) mbar_wait(&credit[b & 1], ((b >> 1) - 1) & 1);
       __syncwarp();  // lanes leave a polling loop one by one: reconverge
       CL_TLX(b, 6);
-      const double *rb = red + (size_t)(b % kNB3) * kNWA * R * K;
-      const unsigned vr_local = smem_u32(Vr + ((size_t)(b & 1) * cs + q) * R * K);
-      const unsigned bar_local = smem_u32(&vfull[b & 1]);
-      constexpr int EPL = (R * K + 31) / 32;
-      double tot[EPL];
-#pragma unroll
-      for (int h = 0; h < kNWA / 8; ++h) {  // eight warps' partials at a time
-        double v[EPL][8];
-#pragma unroll
-        for (int j = 0; j < EPL; ++j) {
-          const int e = lane + 32 * j;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) v[j][w] = e < nr * K ? rb[(8 * h + w) * R * K + e] : 0.0;
-        }
-#pragma unroll
-        for (int j = 0; j < EPL; ++j) tot[j] = h == 0 ? tree_sum<0, 8>(v[j]) : tot[j] + tree_sum<0, 8>(v[j]);
-      }
-#pragma unroll
-      for (int j = 0; j < EPL; ++j) {
-        const int e = lane + 32 * j;
-        const double sm = tot[j];
-        if (e < nr * K)
-          for (int pq = 0; pq < cs; ++pq)
-            st_async(mapa(vr_local + e * 8, pq), sm, mapa(bar_local, pq));
-      }
+      send_block<K>(red, Vr, vfull, q, cs, lane, b, nr);
       CL_TLX(b, 7);
     }
     cluster_sync_all();
@@ -589,92 +702,7 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
         const int nr1 = (int)min((int64_t)R, row_hi - (r0 + R));
         mbar_arrive_expect_tx(&vfull[(b + 1) & 1], (unsigned)(cs * nr1 * K * 8));
       }
-      // all 8 rows at once: 4 lanes per row, lane `sub` owns classes sub,
-      // sub + 4, sub + 8
-      const double *vr = Vr + (size_t)(b & 1) * cs * R * K;
-      double *u = Us + (size_t)(b % kNB3) * R * kUP;
-      const int row = lane >> 2, sub = lane & 3;
-      const bool rv = row < nr;
-      double z[3];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int c = sub + 4 * j;
-        double pz[4] = {0.0, 0.0, 0.0, 0.0};
-        if (rv && c < K) {
-#pragma unroll
-          for (int pq = 0; pq < 4; ++pq)
-            if (pq < cs) pz[pq] = vr[(pq * R + row) * K + c];
-#pragma unroll
-          for (int pq = 4; pq < 8; ++pq)
-            if (pq < cs) pz[pq - 4] += vr[(pq * R + row) * K + c];
-        }
-        z[j] = (pz[0] + pz[1]) + (pz[2] + pz[3]);
-      }
-      double uo[3] = {0.0, 0.0, 0.0};
-      if (apply) {
-        double hv[3], vw[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) {
-          const int c = sub + 4 * j;
-          hv[j] = (rv && c < K) ? rg.side[((size_t)s * R + row) * K + c] : 0.0;
-          vw[j] = z[j] * hv[j];
-        }
-        const double sm = gsum<4>((vw[0] + vw[1]) + vw[2]);  // softmax.py:207 rowsum(VW)
-#pragma unroll
-        for (int j = 0; j < 3; ++j) uo[j] = vw[j] - hv[j] * sm;
-        // curvature pieces: s.(X^T U) = sum over rows of V.U (the fused CG update)
-        if (rv) loss_acc += (z[0] * uo[0] + z[1] * uo[1]) + z[2] * uo[2];
-      } else {
-        // softmax.py:91-98: M = max(0, max_c z); E = exp(z - M); alpha = e^-M + sum E
-        double M = 0.0;
-#pragma unroll
-        for (int j = 0; j < 3; ++j)
-          if (sub + 4 * j < K) M = max_nan(M, z[j]);
-        M = gmax_nan<4>(M);
-        double E[3];
-#pragma unroll
-        for (int j = 0; j < 3; ++j) E[j] = (sub + 4 * j < K) ? exp(z[j] - M) : 0.0;
-        const double eM = exp(-M);
-        const double alpha = eM + gsum<4>((E[0] + E[1]) + E[2]);
-        if (prep) {
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            if (rv && sub + 4 * j < K && q == 0) a.hout[(r0 + row) * K + sub + 4 * j] = E[j] / alpha;
-        } else {
-          // grad: residual (softmax.py:157-161), loss (:134), accuracy (:224-247)
-          const int y = rv ? reinterpret_cast<const int *>(rg.side)[s * R + row] : -1;
-          double pr[3], lin = 0.0;
-#pragma unroll
-          for (int j = 0; j < 3; ++j) {
-            const int c = sub + 4 * j;
-            pr[j] = E[j] / alpha;
-            uo[j] = pr[j] - (c == y ? 1.0 : 0.0);
-            if (c < K && c == y) lin = z[j];
-          }
-          lin = gsum<4>(lin);
-          if (rv && sub == 0 && q == 0) loss_acc += (M + log(alpha)) - lin;
-          double bv = -INFINITY;
-          int bi = K + 1;
-#pragma unroll
-          for (int j = 0; j < 3; ++j)
-            if (sub + 4 * j < K) amax_take(bv, bi, pr[j], sub + 4 * j);
-          gargmax<4>(bv, bi);
-          amax_take(bv, bi, eM / alpha, K);  // the reference class
-          if (rv && sub == 0 && q == 0 && bi == y) corr_acc += 1ull;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < 3; ++j) {
-        const int c = sub + 4 * j;
-        if (c < kUP) u[row * kUP + c] = (rv && c < K) ? uo[j] : 0.0;
-      }
-      CL_TLX(b, 9);
-      mbar_arrive(&ufull[b % kNB3]);  // each lane releases its own U stores
-      // this CTA's receive slot (b & 1) is read -- the U stores above consumed
-      // every value read, so those loads have completed: hand the credit to
-      // every sender with a relaxed arrive (no GPU-scope fence per block)
-      __syncwarp();
-      if (lane < cs) mbar_remote_arrive_relaxed(mapa(smem_u32(&credit[b & 1]), (unsigned)lane));
+      rows_block<K>(a, rg, Vr, Us, ufull, credit, q, cs, lane, b, s, r0, nr, loss_acc, corr_acc);
     }
     if (grad || apply) {  // apply: lossp[cl] = the cluster's sum of V.U (curvature)
       const double l = warp_allsum(loss_acc);
@@ -1209,8 +1237,7 @@ static Plan make_plan(int P, int64_t nrows) {
     pl.R = kRA;
     pl.wc = wc;
     pl.WS = pl.WQ = (wc + 15) / 16 * 16 + 2;
-    int S = 4;  // kLA + 2: V(b + kLA), the tiles waiting for X^T U, one loading
-    layout<K>(pl, S);
+    layout<K>(pl, kSA);
     if (pl.smem > cap_a<K>()) continue;
     const int maxcl = max_clusters<K>(cs, pl.smem);
     const int64_t want = nrows > 0 ? (nrows + kRA - 1) / kRA : 1;
@@ -1466,6 +1493,7 @@ int cluster_cg_iteration(const double *X, int64_t ldx, const int64_t *rows, int6
   if (check_launch("cg_step1_rows")) return 1;
   return launch_cg_step2(t, T, d, r, s, pv, pb, state, st);
 }
+
 
 }  // namespace snx
 
