@@ -268,7 +268,8 @@ template <int R, int K>
 __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t row_lo,
                                         int64_t row_hi, int nb, int c0, int wq, int lane,
                                         int *sh_skip) {
-  const int S = a.S, WS = a.WS, WQ = a.WQ;
+  const int S = R == kRA ? kSA : a.S;  // column split: compile-time ring depth
+  const int WS = a.WS;
   const bool apply = a.mode == kApply, grad = a.mode == kGrad;
   constexpr int IPL = (R + 31) / 32;
   auto load_idx = [&](int b, int64_t(&dst)[IPL]) {
@@ -851,13 +852,14 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
   double *u = Uw + (size_t)warp * 8 * kUP;
   const bool c0v = 2 * t < K, c1v = 2 * t + 1 < K;
 
+  int s = 0;         // ring stage of block b (S is a runtime 2..4: no division per block)
+  unsigned ph = 0;   // its phase parity
   for (int b = 0; b < nb; ++b) {
-    const int s = b % S;
     const int64_t r0 = row_lo + (int64_t)b * R;
     const int nr = (int)min((int64_t)R, row_hi - r0);
     const int gr0 = 8 * warp;          // the warp's first row in the block
     const int ng = min(8, nr - gr0);   // its valid rows (warp-uniform)
-    mbar_wait(&rg.full[s], (b / S) & 1);
+    mbar_wait(&rg.full[s], ph);
     __syncwarp();  // reconverge before the warp-wide MMAs
     if (ng > 0) {
       const double *tile = rg.tiles + (size_t)s * R * WS + (size_t)gr0 * WS;
@@ -930,6 +932,10 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
       __syncwarp();
     }
     if (lane == 0) mbar_arrive(&rg.empty[s]);
+    if (++s == S) {
+      s = 0;
+      ph ^= 1u;
+    }
   }
   // the CTA's partial: warps reduced in order through shared memory (the tiles)
   consumer_sync(kNC);
