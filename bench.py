@@ -516,6 +516,118 @@ def trust_region_config4(snx, torch, rank, world, skip_cpu):
     return res
 
 
+def sharded_extras(snx, torch, rank, world, dev, with_c100=True):
+    """The N > 1 extras: newton_solve_sharded time-to-tolerance on
+    the planted CIFAR-shape problem (rows sharded over the ranks: strong
+    scaling), and BASELINE config #5 -- 1M x 3072 f32 rows per rank, C = 100,
+    the wide tensor-core product -- as sharded Hessian products, a 10-product
+    CG solve and outer iterations (weak scaling: per-rank rows fixed).  Times
+    are the max over ranks."""
+    import torch.distributed as dist
+
+    from paper_1802_09113_b200 import cg as cgmod, distributed as sd
+
+    def tmax(v):
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    out = {}
+    # ---- time to tolerance, newton_solve_sharded (planted labels, eps = 1e-6 |grad F(0)|)
+    A, y = planted_problem(N, P, C)
+    sp = sd.ShardedProblem.from_global(A, y, C, LAM)
+    del A, y
+    x0 = torch.zeros(sp.dim, dtype=torch.float64, device=dev)
+    g0 = sd.ShardedOracle(sp, snx.SampleConfig(1.0, 1.0), 0).gradient_device(x0)
+    eps = 1e-6 * math.sqrt(float(torch.dot(g0, g0)))
+    ncfg = snx.make_variant("subsampled-100", snx.NewtonConfig(epsilon=eps, max_outer_iters=100))
+    sd.newton_solve_sharded(sp, replace(ncfg, max_outer_iters=1), x0=x0.clone())  # warm-up
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    tr = sd.newton_solve_sharded(sp, ncfg, x0=x0.clone())
+    torch.cuda.synchronize()
+    dt = tmax(time.perf_counter() - t0)
+    out["time_to_tolerance_sharded"] = {
+        "workload": f"cifar10-shape 50000x3072 C=10 planted labels, rows sharded over {world} "
+                    "rank(s), newton_solve_sharded subsampled-100, eps = 1e-6 |grad F(0)|, <= 100 "
+                    "outer iterations", "scaling": "strong", "epsilon": eps,
+        "time_to_tol_s": dt, "outer_iters": tr.iterations, "reason": tr.reason,
+        "ms_per_outer_iter": 1e3 * dt / max(tr.iterations, 1),
+        "final_objective": tr.final_objective}
+    del sp, x0, g0
+    torch.cuda.empty_cache()
+    if not with_c100:
+        return out
+    # ---- BASELINE config #5: 1M x 3072 f32 rows per rank, C = 100
+    n_loc, p5, c5 = 1_000_000, 3072, 100
+    gen = torch.Generator(device=dev).manual_seed(1000 + rank)
+    X = torch.randn((n_loc, p5), generator=gen, device=dev, dtype=torch.float32)
+    X.mul_(1.0 / math.sqrt(n_loc * world))
+    labels = torch.randint(0, c5, (n_loc,), generator=gen, device=dev, dtype=torch.int32)
+    local = snx.DeviceDataset(X, labels, c5, p5, dtype="f32")
+    sp5 = sd.ShardedProblem(local, n_loc * world, n_loc * rank, LAM)
+    gx = torch.Generator(device=dev).manual_seed(7)  # the same x on every rank
+    x = 0.05 * torch.randn(sp5.dim, generator=gx, device=dev, dtype=torch.float64)
+    samples = snx.SampleConfig(1.0, F_H)
+    g = sd.ShardedOracle(sp5, samples, 0).gradient_device(x)
+    cgws = cgmod.CgWorkspace(sp5.dim, T_CG, dev)
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+
+    def cg_step(k):
+        op = sd.ShardedOracle(sp5, samples, k).hessian_operator(x)
+        cgmod.enqueue_cg(op, g, THETA, T_CG, cgws)
+        return op
+
+    for k in range(2):
+        op = cg_step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    steps = 3
+    e0.record(st)
+    hv = 0
+    for k in range(2, 2 + steps):
+        op = cg_step(k)
+        hv += int(cgws.slot(T_CG)[3])
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = tmax(e0.elapsed_time(e1))
+    v = g.clone()
+    o = torch.empty_like(v)
+    for _ in range(2):
+        op.apply_into(v, o)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(5):
+        op.apply_into(v, o)
+    e1.record(st)
+    torch.cuda.synchronize()
+    hv_ms = tmax(e0.elapsed_time(e1) / 5)
+    ncfg5 = snx.make_variant("subsampled-100", snx.NewtonConfig(max_outer_iters=3))
+    sd.newton_solve_sharded(sp5, replace(ncfg5, max_outer_iters=1))  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    tr5 = sd.newton_solve_sharded(sp5, ncfg5)
+    torch.cuda.synchronize()
+    dt5 = tmax(time.perf_counter() - t0)
+    out["config5_sharded"] = {
+        "workload": f"BASELINE config #5: {n_loc} x {p5} f32 rows per rank ({n_loc * world} "
+                    f"global), C = {c5}, 5% S_H, tensor-core (bf16 two-term split) products, "
+                    "one all-reduce per product", "scaling": "weak",
+        "hv_per_s": hv / (ms / 1e3), "ms_per_cg_step": ms / steps, "cg_products": hv,
+        "hess_apply_ms": hv_ms,
+        "newton": {"outer_iters": tr5.iterations, "seconds": dt5,
+                   "ms_per_outer_iter": 1e3 * dt5 / max(tr5.iterations, 1),
+                   "reason": tr5.reason, "objective": [r.objective for r in tr5.records]}}
+    del X, labels, local, sp5, op, cgws
+    torch.cuda.empty_cache()
+    return out
+
+
 def cg_kernel_rate(torch, ws, d, reps=50):
     """Achieved GB/s of the CG vector kernels (snx_cg_update = cg_step1 + cg_step2,
     cg.py:77-96): d-vector bytes per update (step1 reads p s r Hs, writes p r;
@@ -735,10 +847,12 @@ def run_ours(args):
         A, y = make_problem()
     cpu = cpu_baseline(A, y, x_host) if (rank == 0 and world == 1 and not args.skip_cpu) \
         else None
-    shapes = None
+    shapes = extras = None
     if world == 1 and not args.skip_shapes:
         del A, y
         shapes = secondary(snx, torch, args)
+    if sharded and not args.skip_solve:
+        extras = sharded_extras(snx, torch, rank, world, dev, with_c100=not args.skip_shapes)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -749,12 +863,13 @@ def run_ours(args):
             "parallelism": (f"rows sharded over {world} GPU(s), one all-reduce per Hv"
                             if sharded else "1 GPU"),
             "hv_applied": hv_count, "gpu_launches": args.steps * (
-                # per step: the H2D index copy, prepare (1 kernel), cg_init x2, T x
-                # (product + finalize, cg_step1, cg_step2) [+ snx_finish_hv when sharded]
-                1 + 2 + T_CG * (4 + (1 if sharded else 0))),
+                # per step: prepare (1 kernel, gather fused), cg_init x2, then T x
+                # (one-pass product, fused finalize + cg_step1, cg_step2); sharded:
+                # T x (product, finalize, snx_finish_hv, cg_step1, cg_step2)
+                1 + 2 + T_CG * (5 if sharded else 3)),
             "clocks": clk.summary(), "roofline": roofline, "cg_kernels": cg_rate, "e2e": e2e,
             "cpu_baseline": cpu, "time_to_tolerance": solve, "trust_region_config4": tr4,
-            "other_shapes": shapes,
+            "other_shapes": shapes, "sharded_extras": extras,
         }
         print(json.dumps(line))
     if world > 1:
