@@ -106,8 +106,9 @@ class ClockSampler:
 # dram__bytes_read.sum + dram__bytes_write.sum of one Hessian product (the
 # one-pass kernel + its finalize), from the committed ncu --set full capture
 # (per launch, cold cache); None until profiled
-TRAFFIC = {"f64": 61.967616e6 + 1.257472e6 + 7.529984e6}  # main kernel read + write, finalize
-TRAFFIC_SOURCE = "profiles/r02_onepass_ncu_full.txt"
+# main kernel dram read + write (r02b capture) + the finalize kernel's (r02 capture)
+TRAFFIC = {"f64": 61.931008e6 + 1.38496e6 + 7.529984e6}
+TRAFFIC_SOURCE = "profiles/r02b_onepass_ncu_full.txt (+ finalize_kernel: profiles/r02_onepass_ncu_full.txt)"
 KERNEL_NAME = {"f64": "one-pass cluster row pass (cluster_rowpass_kernel<9> + finalize_kernel, "
                       "csrc/snx_cluster.cu)",
                "f32": "tcgen05 tc_gemm1 + tc_gemm2 (csrc/snx_tc.cu)"}
@@ -376,7 +377,7 @@ def secondary(snx, torch, args):
     t0 = time.perf_counter()
     oracle.estimate_lipschitz(A, y, C, iters=5)
     cpu5 = time.perf_counter() - t0
-    full_bytes = 2 * N * P * 8  # X streamed twice per product (V = X Q, X^T U)
+    full_bytes = N * P * 8  # X streamed once per product (the one-pass row pass)
     out["lipschitz_cifar10"] = {
         "seconds": dt, "iters": 200, "L": L, "ms_per_iter": dt / 200 * 1e3,
         "x_stream_gb_s": full_bytes / (dt / 200) / 1e9,
@@ -798,9 +799,9 @@ def run_ours(args):
                 # product, and the tcgen05 bf16 pipe of the declared f32 path (C = 10:
                 # N = 9 columns, memory-bound by construction; C = 100: config #5)
                 "tensor_pipe": {
-                    "fp64_dmma_ops_pct_of_peak_elapsed": 21.8,
-                    "fp64_dmma_cycles_active_pct": 28.6,
-                    "source_fp64": "profiles/r02_onepass_ncu_full.txt (cluster_rowpass_kernel<9>)",
+                    "fp64_dmma_ops_pct_of_peak_elapsed": 25.0,
+                    "fp64_dmma_cycles_active_pct": 33.7,
+                    "source_fp64": "profiles/r02b_onepass_ncu_full.txt (cluster_rowpass_kernel<9>)",
                     "tcgen05_c10_pct_elapsed": [1.7, 2.0],
                     "source_c10": "profiles/r02_tc_ncu_full.txt (tc_gemm1 / tc_gemm2)",
                     "tcgen05_c100_pct_active": [23.0, 31.0],
