@@ -163,7 +163,10 @@ class DeviceDataset:
         owner = getattr(self, "_ws_owner", None)
         if owner is not None:  # a materialised view shares its parent's workspace
             return owner.workspace(nrows)
-        need = _lib.workspace_bytes(self.code, nrows, self.n_features, self.K)
+        cache = self.__dict__.setdefault("_ws_need", {})
+        need = cache.get(nrows)
+        if need is None:
+            need = cache[nrows] = _lib.workspace_bytes(self.code, nrows, self.n_features, self.K)
         if self._ws is None or self._ws.numel() < need:
             floor = _lib.workspace_bytes(self.code, self.n_rows, self.n_features, self.K)
             self._ws = torch.zeros(max(need, floor), dtype=torch.uint8, device=self.X.device)
