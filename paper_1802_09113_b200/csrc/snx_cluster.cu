@@ -59,7 +59,12 @@ constexpr int kNWA = 8;            // column split: compute warps (16 measured s
 constexpr int kNCA = kNWA * 32;
 constexpr int kNMTA = 96 / kNWA;   // column split: X^T U tiles per warp (wc <= 768)
 constexpr int kNCHA = 48 / kNWA;   // column split: V chunks per warp
-constexpr int kNTA = kNCA + 96;    // column split: + producer + send warp + row-algebra warp
+// column split block: compute warps + producer + send warp + NRW row-algebra
+// warps (1 for the Hessian passes; 2 for the gradient pass, whose exp / log row
+// algebra would otherwise bound the block rate -- they take alternate blocks)
+template <int NRW>
+constexpr int nta() { return kNCA + 32 * (2 + NRW); }
+constexpr int kNTA = nta<2>();     // the larger block (occupancy queries)
 #ifndef SNX_KLA
 #define SNX_KLA 2
 #endif
@@ -577,8 +582,9 @@ __device__ __forceinline__ void rows_block(const Args &a, const Ring &rg, const 
 }
 
 // ---------------------------------------------------------------- column split
-template <int K>
-__global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_constant__ Args a) {
+template <int K, int NRW>
+__global__ void __launch_bounds__(nta<NRW>(), 1)
+    cluster_rowpass_kernel(const __grid_constant__ Args a) {
   constexpr int R = kRA;
   pdl_trigger();  // the finalize kernel may launch now (it waits for this grid)
   extern __shared__ __align__(1024) unsigned char smem[];
@@ -627,15 +633,17 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     mbar_fence_init();
   }
   // zero the tile columns no bulk copy writes (the chunks / tiles read them)
-  for (int i = tid; i < S * R * (WS - wq); i += kNTA) {
+  for (int i = tid; i < S * R * (WS - wq); i += nta<NRW>()) {
     const int r = i / (WS - wq), j = i - r * (WS - wq);
     rg.tiles[(size_t)r * WS + wq + j] = 0.0;
   }
   __syncthreads();
   CL_TL(-1, 6);
-  if (tid == 0 && nb > 0) {
-    const int nr0 = (int)min((int64_t)R, row_hi - row_lo);
-    mbar_arrive_expect_tx(&vfull[0], (unsigned)(cs * nr0 * K * 8));
+  if (tid == 0) {  // the first block of each row-algebra warp
+    for (int b = 0; b < NRW && b < nb; ++b) {
+      const int nr0 = (int)min((int64_t)R, row_hi - (row_lo + (int64_t)b * R));
+      mbar_arrive_expect_tx(&vfull[b & 1], (unsigned)(cs * nr0 * K * 8));
+    }
   }
   // peers' barriers must be initialised before any st.async / remote arrive:
   // arrive here, wait only in the two warps that address peers (the others
@@ -687,11 +695,15 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
     return;
   }
 
-  if (warp == kNWA + 2) {  // ----------------------------- row-algebra warp
+  if (warp >= kNWA + 2) {  // --------------------------- row-algebra warps
+    // warp j takes blocks j, j + NRW, ...; block b's receive slot is vfull[b & 1],
+    // re-armed for block b + NRW once this block's phase is done
+    static_assert(NRW == 1 || NRW == 2, "two receive slots");
     cluster_wait();
+    const int j = warp - (kNWA + 2);
     double loss_acc = 0.0;
     unsigned long long corr_acc = 0;
-    for (int b = 0; b < nb; ++b) {
+    for (int b = j; b < nb; b += NRW) {
       const int s = b % S;
       const int64_t r0 = row_lo + (int64_t)b * R;
       const int nr = (int)min((int64_t)R, row_hi - r0);
@@ -699,18 +711,29 @@ __global__ void __launch_bounds__(kNTA, 1) cluster_rowpass_kernel(const __grid_c
       mbar_poll(&vfull[b & 1], (b >> 1) & 1);
       __syncwarp();
       CL_TLX(b, 8);
-      if (lane == 0 && b + 1 < nb) {  // arm the other buffer for block b + 1
-        const int nr1 = (int)min((int64_t)R, row_hi - (r0 + R));
-        mbar_arrive_expect_tx(&vfull[(b + 1) & 1], (unsigned)(cs * nr1 * K * 8));
+      if (lane == 0 && b + NRW < nb) {  // arm slot (b + NRW) & 1 for block b + NRW
+        const int nrn = (int)min((int64_t)R, row_hi - (r0 + NRW * R));
+        mbar_arrive_expect_tx(&vfull[(b + NRW) & 1], (unsigned)(cs * nrn * K * 8));
       }
       rows_block<K>(a, rg, Vr, Us, ufull, credit, q, cs, lane, b, s, r0, nr, loss_acc, corr_acc);
     }
     if (grad || apply) {  // apply: lossp[cl] = the cluster's sum of V.U (curvature)
-      const double l = warp_allsum(loss_acc);
+      double l = warp_allsum(loss_acc);
       unsigned long long cc = corr_acc;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) cc += __shfl_xor_sync(0xffffffffu, cc, o);
-      if (lane == 0 && q == 0) {
+      if constexpr (NRW == 2) {  // fixed order: warp 0's sum + warp 1's
+        __shared__ double sh_rl;
+        __shared__ unsigned long long sh_rc;
+        if (j == 1 && lane == 0) {
+          sh_rl = l;
+          sh_rc = cc;
+        }
+        asm volatile("bar.sync 2, 64;\n" ::: "memory");  // the two row-algebra warps
+        l += sh_rl;
+        cc += sh_rc;
+      }
+      if (j == 0 && lane == 0 && q == 0) {
         a.lossp[cl] = l;
         a.corrp[cl] = cc;
       }
@@ -1147,7 +1170,7 @@ static size_t smem_cap(KernT kern) {
 template <int K>
 static size_t cap_a() {
   static size_t c = 0;
-  if (!c) c = smem_cap(cluster_rowpass_kernel<K>);
+  if (!c) c = smem_cap(cluster_rowpass_kernel<K, 2>);
   return c;
 }
 template <int K>
@@ -1191,7 +1214,7 @@ static int max_clusters(int cs, size_t smem) {
   static size_t cache_smem[4] = {0, 0, 0, 0};
   const int ci = cs == 1 ? 0 : cs == 2 ? 1 : cs == 4 ? 2 : 3;
   if (cache[ci] >= 0 && cache_smem[ci] == smem) return cache[ci];
-  auto kern = cluster_rowpass_kernel<K>;
+  auto kern = cluster_rowpass_kernel<K, 2>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_a<K>());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs * 64);
@@ -1316,16 +1339,20 @@ static int launch_k(const Plan &pl, Args &a, cudaStream_t st) {
   cfg.numAttrs = na;
   if (pl.split == 0) {
     static bool attr = false;
-    auto kern = cluster_rowpass_kernel<K>;
+    auto k1 = cluster_rowpass_kernel<K, 1>;
+    auto k2 = cluster_rowpass_kernel<K, 2>;
     if (!attr) {
-      if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)cap_a<K>()) != cudaSuccess ||
+          cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)cap_a<K>()) != cudaSuccess)
         return check_launch("cluster_rowpass attributes");
       attr = true;
     }
-    carveout(kern);
-    cfg.blockDim = dim3(kNTA);
-    cudaLaunchKernelEx(&cfg, kern, a);
+    const bool two = a.mode == kGrad;  // exp / log row algebra: two row warps
+    carveout(two ? k2 : k1);
+    cfg.blockDim = dim3(two ? nta<2>() : nta<1>());
+    cudaLaunchKernelEx(&cfg, two ? k2 : k1, a);
     return check_launch("cluster_rowpass");
   }
   static bool attr = false;
@@ -1385,15 +1412,15 @@ bool cluster_supported(int dtype, int32_t p, int32_t K) {
   return clp::plan_for(dtype, p, K, 1).ok != 0;
 }
 
-// The full-data objective + gradient pass takes the one-pass kernel where it
-// measured faster than the two GEMMs of snx_rowpass.cu: the row split (p <= 64).
-// The column split streams X from HBM once, but its row algebra (exp / log per
-// row) on the shared FP64 pipe makes it slower than the two-pass kernels at
-// MNIST / CIFAR shape (SNX_ONEPASS_GRAD=1 forces it, for A/B runs).
+// The full-data objective + gradient pass runs on the one-pass kernel (X read
+// once): the row split at p <= 64, the column split with two row-algebra warps
+// otherwise (CIFAR 365 vs 415 us for the two GEMMs of snx_rowpass.cu, which read
+// X twice; with one row-algebra warp the exp / log per row bounded it at 522 us).
+// SNX_TWO_PASS_GRAD=1 selects the two GEMMs, for A/B runs.
 bool cluster_grad_preferred(int dtype, int32_t p, int32_t K) {
-  static const bool force = getenv("SNX_ONEPASS_GRAD") != nullptr;
+  static const bool off = getenv("SNX_TWO_PASS_GRAD") != nullptr;  // A/B: snx_rowpass.cu
   const clp::Plan pl = clp::plan_for(dtype, p, K, 1);
-  return pl.ok && (pl.split == 1 || force);
+  return pl.ok && !off;
 }
 
 size_t cluster_ws_bytes(int dtype, int64_t nrows, int32_t p, int32_t K) {
