@@ -601,6 +601,7 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
   uint64_t *credit = vfull + 2;      // [2] every peer has consumed this CTA's slot (b & 1)
   uint64_t *redfull = credit + 2;    // [3] compute warps' partials written
   uint64_t *ufull = redfull + kNB3;  // [3] U rows ready
+  uint64_t *redfree = ufull + kNB3;  // [3] prep: the send warp has read red[b % 3]
   __shared__ int sh_skip;
 
   // the warp index through a shuffle: provably warp-uniform for the compiler
@@ -629,6 +630,7 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
     for (int j = 0; j < kNB3; ++j) {
       mbar_init(&redfull[j], kNWA);
       mbar_init(&ufull[j], 32);
+      mbar_init(&redfree[j], 1);
     }
     mbar_fence_init();
   }
@@ -689,6 +691,10 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
       __syncwarp();  // lanes leave a polling loop one by one: reconverge
       CL_TLX(b, 6);
       send_block<K>(red, Vr, vfull, q, cs, lane, b, nr);
+      // prep: the compute warps do not wait for U, so red[b % 3] is handed
+      // back explicitly (the sums above consumed every value read)
+      __syncwarp();
+      if (prep && lane == 0) mbar_arrive(&redfree[b % kNB3]);
       CL_TLX(b, 7);
     }
     cluster_sync_all();
@@ -771,6 +777,19 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
   // push, peers' partials, row algebra) of a block has kLA blocks of compute
   // to hide behind.  (Compile-time full-slice variants of the two MMA streams,
   // without the per-chunk / per-tile bounds tests, measured 1 us slower.)
+  if (prep) {
+    // h only: no X^T U, so a stage is released right after its logits and the
+    // logits stream at the rate the exchange and the row algebra drain them
+    for (int b = 0; b < nb; ++b) {
+      if (b >= kNB3) mbar_wait(&redfree[b % kNB3], ((b / kNB3) - 1) & 1);
+      __syncwarp();
+      vphase(b);
+      if (lane == 0) mbar_arrive(&rg.empty[b % S]);
+    }
+    cluster_wait();          // the prologue's arrive
+    cluster_sync_relaxed();  // no CTA leaves while a peer may still address its smem
+    return;
+  }
   for (int b = 0; b < kLA && b < nb; ++b) vphase(b);
   CL_TL(-1, 2);
   for (int b = 0; b < nb; ++b) {
@@ -1196,7 +1215,7 @@ static void layout(Plan &pl, int S) {
     pl.o_u = take((size_t)kNB3 * kRA * kUP * 8, 16);
     pl.o_vr = take((size_t)2 * pl.cs * kRA * K * 8, 16);
     pl.o_red = take((size_t)kNB3 * kNWA * kRA * K * 8, 16);
-    pl.o_bar = take((size_t)(2 * S + 4 + 2 * kNB3) * 8, 8);
+    pl.o_bar = take((size_t)(2 * S + 4 + 3 * kNB3) * 8, 8);
   } else {
     pl.o_u = take((size_t)kNW * 8 * kUP * 8, 16);
     pl.o_vr = pl.o_red = 0;
@@ -1349,7 +1368,7 @@ static int launch_k(const Plan &pl, Args &a, cudaStream_t st) {
         return check_launch("cluster_rowpass attributes");
       attr = true;
     }
-    const bool two = a.mode == kGrad;  // exp / log row algebra: two row warps
+    const bool two = a.mode != kApply;  // exp / log row algebra: two row warps
     carveout(two ? k2 : k1);
     cfg.blockDim = dim3(two ? nta<2>() : nta<1>());
     cudaLaunchKernelEx(&cfg, two ? k2 : k1, a);
