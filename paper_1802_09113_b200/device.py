@@ -30,7 +30,14 @@ def cuda_device():
     return torch.device("cuda", torch.cuda.current_device())
 
 
+_RAW_STREAM = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def stream_handle():
+    """cudaStream_t of the current stream (the raw getter skips building a
+    torch Stream object: ~0.5 instead of ~6 us per kernel-launching call)."""
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(torch.cuda.current_device())
     return torch.cuda.current_stream().cuda_stream
 
 

@@ -32,3 +32,17 @@ device.upload = pinned
 run("pinned staging per call")
 device.upload = orig
 run("device.upload again")
+
+# downloads: pinned buffers + one synchronisation (device.download) vs pageable .cpu()
+orig_d = device.download
+
+
+def pageable_download(*ts):
+    torch.cuda.current_stream().synchronize()
+    return [t.cpu().numpy() for t in ts]
+
+
+device.download = pageable_download
+run("download via pageable .cpu()")
+device.download = orig_d
+run("device.download (pinned)")
