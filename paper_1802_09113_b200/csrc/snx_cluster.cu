@@ -447,6 +447,41 @@ __device__ __forceinline__ void xgroup(const double *x0, int WS, const double *u
   }
 }
 
+// X^T U of one 8-row block on m16n8k8: tile m covers columns 16 mt .. +15
+// (mt = m0 + mstep m); lane (g, t) holds A = X^T values of columns g, g + 8 at
+// rows t, t + 4, B = U rows t, t + 4 at class g, C = (columns g, g + 8) x
+// (classes 2t, 2t + 1); class 8 by DFMA (per lane: rows t, t + 4 of columns g,
+// g + 8; the four lanes of a group cover the 8 rows).
+template <int K, int NMT>
+__device__ __forceinline__ void xgroup16(const double *x0, int WS, const double *u, int nr, int g,
+                                         int t, int m0, int mstep, int nmt16,
+                                         double (&acc)[NMT][4], double (&acc8)[NMT][2]) {
+  const double b0 = u[t * kUP + g], b1 = u[(t + 4) * kUP + g];
+  const double u8a = K == 9 ? u[t * kUP + 8] : 0.0, u8b = K == 9 ? u[(t + 4) * kUP + 8] : 0.0;
+  const bool okt = t < nr, okt4 = t + 4 < nr;
+  const double *xa = x0 + (size_t)t * WS + g;
+  const double *xb = xa + 4 * (size_t)WS;
+#pragma unroll
+  for (int m = 0; m < NMT; ++m) {
+    const int mt = m0 + mstep * m;
+    if (mt < nmt16) {
+      const double a0 = okt ? xa[16 * mt] : 0.0, a1 = okt ? xa[16 * mt + 8] : 0.0;
+      const double a2 = okt4 ? xb[16 * mt] : 0.0, a3 = okt4 ? xb[16 * mt + 8] : 0.0;
+      asm volatile(
+          "mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+          "{%8,%9}, {%0,%1,%2,%3};"
+          : "+d"(acc[m][0]), "+d"(acc[m][1]), "+d"(acc[m][2]), "+d"(acc[m][3])
+          : "d"(a0), "d"(a1), "d"(a2), "d"(a3), "d"(b0), "d"(b1));
+      if constexpr (K == 9) {
+        acc8[m][0] = fma(a0, u8a, acc8[m][0]);
+        acc8[m][1] = fma(a1, u8a, acc8[m][1]);
+        acc8[m][0] = fma(a2, u8b, acc8[m][0]);
+        acc8[m][1] = fma(a3, u8b, acc8[m][1]);
+      }
+    }
+  }
+}
+
 // Send warp, one block: the CTA's partial logits (the compute warps' partials
 // summed in a fixed tree) -> every peer's Vr[B & 1][q] by st.async, counted on
 // the peer's vfull[B & 1].  B: the block's position in the CTA's ring sequence.
@@ -753,9 +788,12 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
   cp_async_wait_all();
   consumer_sync(kNCA);
   CL_TL(-1, 1);
-  double acc[kNMTA][2], acc8[kNMTA];
+  constexpr int NM16 = kNMTA / 2;  // 16-column X^T U tiles per warp
+  const int nmt16 = (wq + 15) >> 4;
+  double acc[NM16][4], acc8[NM16][2];
 #pragma unroll
-  for (int m = 0; m < kNMTA; ++m) acc[m][0] = acc[m][1] = acc8[m] = 0.0;
+  for (int m = 0; m < NM16; ++m) acc[m][0] = acc[m][1] = acc[m][2] = acc[m][3] = acc8[m][0] =
+      acc8[m][1] = 0.0;
 
   // partial logits of block b (k split over the warps) -> red[b & 1][warp]
   auto vphase = [&](int b) {
@@ -802,8 +840,9 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
     if (!prep) {
       const int64_t r0 = row_lo + (int64_t)b * R;
       const int nr = (int)min((int64_t)R, row_hi - r0);
-      xgroup<K, kNMTA>(rg.tiles + (size_t)(b % S) * R * WS, WS,
-                      Us + (size_t)(b % kNB3) * R * kUP, nr, g8, t4, warp, kNWA, nmt, acc, acc8);
+      xgroup16<K, NM16>(rg.tiles + (size_t)(b % S) * R * WS, WS,
+                        Us + (size_t)(b % kNB3) * R * kUP, nr, g8, t4, warp, kNWA, nmt16, acc,
+                        acc8);
     }
     CL_TL(b, 3);
     __syncwarp();
@@ -814,14 +853,17 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
     const int64_t d = (int64_t)K * a.p;
     double *gq = a.gp + (int64_t)cl * d;
 #pragma unroll
-    for (int m = 0; m < kNMTA; ++m) {
+    for (int m = 0; m < NM16; ++m) {
       const int mt = warp + kNWA * m;
-      const double s8 = K == 9 ? gsum<4>(acc8[m]) : 0.0;
-      const int col = 8 * mt + g8, gc = c0 + col;
-      if (mt < nmt && col < wq && gc < a.p) {
-        if (2 * t4 < K) gq[(int64_t)(2 * t4) * a.p + gc] = acc[m][0];
-        if (2 * t4 + 1 < K) gq[(int64_t)(2 * t4 + 1) * a.p + gc] = acc[m][1];
-        if (K == 9 && t4 == 0) gq[(int64_t)8 * a.p + gc] = s8;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {  // columns g (c0, c1) and g + 8 (c2, c3)
+        const double s8 = K == 9 ? gsum<4>(acc8[m][h]) : 0.0;
+        const int col = 16 * mt + g8 + 8 * h, gc = c0 + col;
+        if (mt < nmt16 && col < wq && gc < a.p) {
+          if (2 * t4 < K) gq[(int64_t)(2 * t4) * a.p + gc] = acc[m][2 * h];
+          if (2 * t4 + 1 < K) gq[(int64_t)(2 * t4 + 1) * a.p + gc] = acc[m][2 * h + 1];
+          if (K == 9 && t4 == 0) gq[(int64_t)8 * a.p + gc] = s8;
+        }
       }
     }
   }
