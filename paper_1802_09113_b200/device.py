@@ -41,6 +41,10 @@ def stream_handle():
     return torch.cuda.current_stream().cuda_stream
 
 
+def _out_of_range(idx, n):
+    return bool(idx.min() < 0 or idx.max() >= n)
+
+
 def ptr(t):
     return None if t is None else t.data_ptr()
 
@@ -130,13 +134,15 @@ class DeviceDataset:
         return self
 
     # ------------------------------------------------------------ views
-    def take(self, indices):
-        """Row gather (dataset.py:90-97, 180-185); identity returns self."""
+    def take(self, indices, _sorted=False):
+        """Row gather (dataset.py:90-97, 180-185); identity returns self.
+        `_sorted`: the indices are ascending (the sampler's sets): the range
+        check reads the two ends only."""
         idx = np.asarray(indices, dtype=np.int64)
         n = self.n_rows
         if len(idx) == n and np.array_equal(idx, np.arange(n)):
             return self
-        if len(idx) and (idx.min() < 0 or idx.max() >= n):
+        if len(idx) and (_out_of_range(idx, n) if not _sorted else idx[0] < 0 or idx[-1] >= n):
             raise DimensionError("row index out of range")
         return DeviceView(self, upload(idx, self.X.device), len(idx))
 
@@ -242,7 +248,7 @@ class DeviceView:
             self._dense._ws_owner = b
         return self._dense
 
-    def take(self, indices):
+    def take(self, indices, _sorted=False):
         """Rows `indices` of this view (a view of the base's rows[indices]):
         sampling from a train split works as on the reference's materialised
         LabeledDataset (dataset.py:180-185)."""
@@ -250,7 +256,7 @@ class DeviceView:
         n = self._n
         if len(idx) == n and np.array_equal(idx, np.arange(n)):
             return self
-        if len(idx) and (idx.min() < 0 or idx.max() >= n):
+        if len(idx) and (_out_of_range(idx, n) if not _sorted else idx[0] < 0 or idx[-1] >= n):
             raise DimensionError("row index out of range")
         return DeviceView(self.base, self.rows[upload(idx, self.rows.device)], len(idx))
 

@@ -96,13 +96,15 @@ class CsrDataset:
         return self
 
     # ------------------------------------------------------------ views
-    def take(self, indices):
-        """Row gather (dataset.py:90-97); identity returns self."""
+    def take(self, indices, _sorted=False):
+        """Row gather (dataset.py:90-97); identity returns self (`_sorted`: see
+        DeviceDataset.take)."""
         idx = np.asarray(indices, dtype=np.int64)
         n = self.n_rows
         if len(idx) == n and np.array_equal(idx, np.arange(n)):
             return self
-        if len(idx) and (idx.min() < 0 or idx.max() >= n):
+        if len(idx) and (idx.min() < 0 or idx.max() >= n if not _sorted
+                         else idx[0] < 0 or idx[-1] >= n):
             raise DimensionError("row index out of range")
         return CsrView(self, idx)
 
