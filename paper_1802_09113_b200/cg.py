@@ -106,7 +106,10 @@ class CgGraph:
         enqueue_cg(self.op, self.g, self.theta, self.T, self.ws)
 
     def run(self, g):
-        self.g.copy_(g)
+        """g: the right-hand side (device tensor), or None when self.g already
+        holds it."""
+        if g is not None:
+            self.g.copy_(g)
         ws_now = self.op.view.workspace(self.op.view.n_rows).data_ptr()
         if self.graph is not None and ws_now != self._ws_ptr:
             self.graph = None  # the dataset workspace moved: recapture
@@ -190,6 +193,13 @@ def report_from(ws, t_final, as_torch, slot_values=None):
 
 def cg_solve(apply_H, g, cfg):
     """Approximately solve H p = -g to ||H p + g|| <= theta ||g|| (cg.py:51-98)."""
+    if getattr(apply_H, "_bufs", None) is not None and not isinstance(g, torch.Tensor):
+        a = np.ascontiguousarray(g, dtype=np.float64)
+        cg = cg_graph_for(apply_H, cfg.max_iters, cfg.theta)
+        if a.ndim == 1 and a.shape[0] == cg.g.numel():
+            # numpy g straight into the captured graph's input (one async copy)
+            cg.g.copy_(torch.from_numpy(a), non_blocking=True)
+            return report_from(cg.run(None), cfg.max_iters, False)
     gd, as_t = vec_in(g, np.asarray(g).shape[0] if not isinstance(g, torch.Tensor)
                       else g.numel(), "gradient")
     if getattr(apply_H, "_bufs", None) is not None:  # our operator: graph-captured solve
