@@ -608,6 +608,7 @@ __device__ __forceinline__ void rows_block(const Args &a, const Ring &rg, const 
     const int c = sub + 4 * j;
     if (c < kUP) u[row * kUP + c] = (rv && c < K) ? uo[j] : 0.0;
   }
+  CL_TLX((int)B, 9);
   mbar_arrive(&ufull[B % kNB3]);  // each lane releases its own U stores
   // this CTA's receive slot (B & 1) is read -- the U stores above consumed
   // every value read, so those loads have completed: hand the credit to
