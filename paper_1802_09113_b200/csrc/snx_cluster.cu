@@ -474,18 +474,22 @@ __device__ __forceinline__ void xgroup(const double *x0, int WS, const double *u
 
 // X^T U of one 8-row block on m16n8k8: tile m covers columns 16 mt .. +15
 // (mt = m0 + mstep m); lane (g, t) holds A = X^T values of columns g, g + 8 at
-// rows t, t + 4, B = U rows t, t + 4 at class g, C = (columns g, g + 8) x
-// (classes 2t, 2t + 1); class 8 by DFMA (per lane: rows t, t + 4 of columns g,
-// g + 8; the four lanes of a group cover the 8 rows).
+// rows 2t, 2t + 1, B = U rows 2t, 2t + 1 at class g, C = (columns g, g + 8) x
+// (classes 2t, 2t + 1); class 8 by DFMA (per lane: rows 2t, 2t + 1 of columns
+// g, g + 8; the four lanes of a group cover the 8 rows).
 template <int K, int NMT>
 __device__ __forceinline__ void xgroup16(const double *x0, int WS, const double *u, int nr, int g,
                                          int t, int m0, int mstep, int nmt16,
                                          double (&acc)[NMT][4], double (&acc8)[NMT][2]) {
-  const double b0 = u[t * kUP + g], b1 = u[(t + 4) * kUP + g];
-  const double u8a = K == 9 ? u[t * kUP + 8] : 0.0, u8b = K == 9 ? u[(t + 4) * kUP + 8] : 0.0;
-  const bool okt = t < nr, okt4 = t + 4 < nr;
-  const double *xa = x0 + (size_t)t * WS + g;
-  const double *xb = xa + 4 * (size_t)WS;
+  // the MMA's k index runs over the block's rows permuted (k = t -> row 2t,
+  // k = t + 4 -> row 2t + 1), the same for A and B: a warp's A loads then hit
+  // every bank pair exactly twice (rows 4 x WS = 2 mod 16 apart)
+  const double b0 = u[(2 * t) * kUP + g], b1 = u[(2 * t + 1) * kUP + g];
+  const double u8a = K == 9 ? u[(2 * t) * kUP + 8] : 0.0;
+  const double u8b = K == 9 ? u[(2 * t + 1) * kUP + 8] : 0.0;
+  const bool okt = 2 * t < nr, okt4 = 2 * t + 1 < nr;
+  const double *xa = x0 + (size_t)(2 * t) * WS + g;
+  const double *xb = xa + WS;
 #pragma unroll
   for (int m = 0; m < NMT; ++m) {
     const int mt = m0 + mstep * m;
