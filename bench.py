@@ -107,7 +107,7 @@ class ClockSampler:
 # one-pass kernel + its finalize), from the committed ncu --set full capture
 # (per launch, cold cache); None until profiled
 # main kernel dram read + write (r02b capture) + the finalize kernel's (r02 capture)
-TRAFFIC = {"f64": 61.931008e6 + 1.38496e6 + 7.529984e6}
+TRAFFIC = {"f64": 61.933568e6 + 1.92128e6 + 7.529984e6}
 TRAFFIC_SOURCE = "profiles/r02b_onepass_ncu_full.txt (+ finalize_kernel: profiles/r02_onepass_ncu_full.txt)"
 KERNEL_NAME = {"f64": "one-pass cluster row pass (cluster_rowpass_kernel<9> + finalize_kernel, "
                       "csrc/snx_cluster.cu)",
@@ -799,8 +799,8 @@ def run_ours(args):
                 # product, and the tcgen05 bf16 pipe of the declared f32 path (C = 10:
                 # N = 9 columns, memory-bound by construction; C = 100: config #5)
                 "tensor_pipe": {
-                    "fp64_dmma_ops_pct_of_peak_elapsed": 25.0,
-                    "fp64_dmma_cycles_active_pct": 33.7,
+                    "fp64_dmma_ops_pct_of_peak_elapsed": 26.8,
+                    "fp64_dmma_cycles_active_pct": 36.1,
                     "source_fp64": "profiles/r02b_onepass_ncu_full.txt (cluster_rowpass_kernel<9>)",
                     "tcgen05_c10_pct_elapsed": [1.7, 2.0],
                     "source_c10": "profiles/r02_tc_ncu_full.txt (tc_gemm1 / tc_gemm2)",
