@@ -1,7 +1,7 @@
 """Per-CTA, per-block timeline of the one-pass cluster kernel (debug build).
 
     python -c "from paper_1802_09113_b200 import _build; _build.build_timeline('tools/libsnx_cltl.so', ['-DSNX_CL_TIMELINE'])"
-    SNX_LIB=tools/libsnx_cltl.so python tools/cl_timeline.py [cifar|mnist|covertype] [b2b|sync|prep]
+    SNX_LIB=tools/libsnx_cltl.so python tools/cl_timeline.py [cifar|mnist|covertype] [b2b|sync|prep|cg]
 
 Events per block, compute thread 0: 0 loop top, 1 next block's V done,
 2 U(b) ready (waited), 3 X^T U(b) done; exchange-warp lane 0: 6 warp partials
@@ -36,7 +36,13 @@ out = torch.empty_like(g)
 mode = sys.argv[2] if len(sys.argv) > 2 else "b2b"
 st = torch.cuda.current_stream()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-run = (lambda: orc.hessian_operator(x)) if mode == "prep" else (lambda: op.apply_into(g, out))
+if mode == "prep":
+    run = lambda: orc.hessian_operator(x)  # noqa: E731
+elif mode == "cg":  # the products of a captured CG solve (the stamps: its last product)
+    from paper_1802_09113_b200 import cg as cgmod
+    run = lambda: cgmod.cg_graph_for(op, 10, 1e-12).run(g)  # noqa: E731
+else:
+    run = lambda: op.apply_into(g, out)  # noqa: E731
 for _ in range(5):
     run()
 torch.cuda.synchronize()
@@ -47,6 +53,8 @@ e1.record(st)
 torch.cuda.synchronize()
 print(f"20 back-to-back {'prepares' if mode == 'prep' else 'products'}: "
       f"{e0.elapsed_time(e1) / 20 * 1e3:.1f} us each (events)")
+if mode == "cg":
+    torch.cuda.synchronize()
 if mode == "sync":  # the stamps below: one product on an idle GPU
     op.apply_into(g, out)
     torch.cuda.synchronize()
