@@ -1096,6 +1096,22 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
   }
 }
 
+#ifdef SNX_CL_TIMELINE
+__device__ unsigned long long g_cgr_tl[256][3];  // cg_step1_rows: entry, dependency met, exit
+#define CGR_TL(ev)                                                   \
+  do {                                                               \
+    if (threadIdx.x == 0) {                                          \
+      unsigned long long t_;                                         \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));         \
+      g_cgr_tl[blockIdx.x][(ev)] = t_;                               \
+    }                                                                \
+  } while (0)
+#else
+#define CGR_TL(ev) \
+  do {             \
+  } while (0)
+#endif
+
 // ---------------------------------------------------------------- finalize
 // out[i] = scale * sum_cl gp[cl][i] + lam * base[i] (fixed order: F lanes per
 // element sum the partials cl = f (mod F) in order, then an xor butterfly),
@@ -1176,8 +1192,10 @@ __global__ void __launch_bounds__(kFinThreads)
                          int64_t epb, int F, double scale, double lam,
                          const double *__restrict__ vup, const double *__restrict__ s, double *r,
                          double *p, double *Hs, double *state) {
+  CGR_TL(0);
   pdl_trigger();  // cg_step2, then the next row pass, may launch early (both wait)
   pdl_wait();
+  CGR_TL(1);
   const double *st = slot(state, t);
   __shared__ double sh[kFinThreads / 32];
   __shared__ double s_alpha;
@@ -1189,25 +1207,36 @@ __global__ void __launch_bounds__(kFinThreads)
   const int64_t i = (int64_t)blockIdx.x * epb + tid / F;
   const int f = tid % F;
   const bool own = (tid / F) < epb && i < d;
-  double sum = 0.0;
-  if (own) {
-    int c = f;
-    for (; c + 7 * F < ncl; c += 8 * F) {
-      double v[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldcg(gp + (int64_t)(c + k * F) * d + i);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) sum += v[k];
-    }
-    for (; c < ncl; c += F) sum += __ldcg(gp + (int64_t)c * d + i);
-  }
   const bool lead = own && f == 0;
   const double si = lead ? s[i] : 0.0, pi = lead ? p[i] : 0.0, ri0 = lead ? r[i] : 0.0;
+  // lane f's partials cl = f, f + F, ...: all in flight at once (one L2 round
+  // trip), summed in that order
+  constexpr int kML = 16;
+  double sum = 0.0;
+  {
+    double v[kML];
+#pragma unroll
+    for (int k = 0; k < kML; ++k) {
+      const int c = f + k * F;
+      v[k] = own && c < ncl ? __ldcg(gp + (int64_t)c * d + i) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < kML; ++k)
+      if (f + k * F < ncl) sum += v[k];
+    if (own)
+      for (int c = f + kML * F; c < ncl; c += F) sum += __ldcg(gp + (int64_t)c * d + i);
+  }
   if (tid < 32) {
+    double vv[8];  // the clusters' V.U sums: lane-strided, loads first
+#pragma unroll
+    for (int k = 0; k < 8; ++k) vv[k] = tid + 32 * k < ncl ? __ldcg(vup + tid + 32 * k) : 0.0;
     double v = 0.0;
-    for (int c = tid; c < ncl; c += 32) v += __ldcg(vup + c);
+#pragma unroll
+    for (int k = 0; k < 8; ++k)
+      if (tid + 32 * k < ncl) v += vv[k];
+    for (int c = tid + 256; c < ncl; c += 32) v += __ldcg(vup + c);
     v = warp_allsum(v);
-    const double ss = warp_sum_partials(scratch(state, T) + kDotBlocks);
+    const double ss = warp_sum_partials_cg(scratch(state, T) + kDotBlocks);
     if (tid == 0) {
       const double curv = __dadd_rn(__dmul_rn(scale, v), __dmul_rn(lam, ss));
       s_bad = curv <= 1e-32 * ss;  // cg.py:16, :79
@@ -1233,6 +1262,7 @@ __global__ void __launch_bounds__(kFinThreads)
   }
   const double b = block_sum<kFinThreads>(acc, sh);
   if (tid == 0) scratch(state, T)[blockIdx.x] = b;
+  CGR_TL(2);
 }
 
 // ---------------------------------------------------------------- host side
@@ -1622,6 +1652,12 @@ int cluster_cg_iteration(const double *X, int64_t ldx, const int64_t *rows, int6
 }  // namespace snx
 
 #ifdef SNX_CL_TIMELINE
+extern "C" int snx_debug_cgr_timeline(unsigned long long *host_out) {
+  return cudaMemcpyFromSymbol(host_out, snx::clp::g_cgr_tl, sizeof(snx::clp::g_cgr_tl)) ==
+                 cudaSuccess
+             ? 0
+             : 1;
+}
 extern "C" int snx_debug_cl_timeline(unsigned long long *host_out) {
   return cudaMemcpyFromSymbol(host_out, snx::clp::g_cl_tl, sizeof(snx::clp::g_cl_tl)) ==
                  cudaSuccess
