@@ -1097,7 +1097,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
 }
 
 #ifdef SNX_CL_TIMELINE
-__device__ unsigned long long g_cgr_tl[256][3];  // cg_step1_rows: entry, dependency met, exit
+__device__ unsigned long long g_cgr_tl[256][6];  // cg_step1_rows: entry, dependency met, exit, loads, alpha, stores
 #define CGR_TL(ev)                                                   \
   do {                                                               \
     if (threadIdx.x == 0) {                                          \
@@ -1204,15 +1204,17 @@ __global__ void __launch_bounds__(kFinThreads)
   // every load that does not need alpha goes out first: the partials of H s
   // and s, p, r overlap the curvature reduction below
   const double done = st[kDone];
-  const int64_t i = (int64_t)blockIdx.x * epb + tid / F;
-  const int f = tid % F;
-  const bool own = (tid / F) < epb && i < d;
-  const bool lead = own && f == 0;
-  const double si = lead ? s[i] : 0.0, pi = lead ? p[i] : 0.0, ri0 = lead ? r[i] : 0.0;
-  // lane f's partials cl = f, f + F, ...: all in flight at once (one L2 round
-  // trip), summed in that order
+  // thread (f, e): element e of the block, partials cl = f, f + F, ...; a warp
+  // covers consecutive elements of one partial row (coalesced); the F sums of
+  // an element meet in shared memory and its lead thread adds them in f order
+  const int e = tid % (int)epb, f = tid / (int)epb;
+  const int64_t i = (int64_t)blockIdx.x * epb + e;
+  const bool own = f < F && i < d;
+  const int64_t il = (int64_t)blockIdx.x * epb + tid;
+  const bool lead = tid < epb && il < d;
+  const double si = lead ? s[il] : 0.0, pi = lead ? p[il] : 0.0, ri0 = lead ? r[il] : 0.0;
+  __shared__ double part[kFinThreads];
   constexpr int kML = 16;
-  double sum = 0.0;
   {
     double v[kML];
 #pragma unroll
@@ -1220,11 +1222,13 @@ __global__ void __launch_bounds__(kFinThreads)
       const int c = f + k * F;
       v[k] = own && c < ncl ? __ldcg(gp + (int64_t)c * d + i) : 0.0;
     }
+    double sum = 0.0;
 #pragma unroll
     for (int k = 0; k < kML; ++k)
       if (f + k * F < ncl) sum += v[k];
     if (own)
       for (int c = f + kML * F; c < ncl; c += F) sum += __ldcg(gp + (int64_t)c * d + i);
+    if (own) part[f * epb + e] = sum;
   }
   if (tid < 32) {
     double vv[8];  // the clusters' V.U sums: lane-strided, loads first
@@ -1247,19 +1251,23 @@ __global__ void __launch_bounds__(kFinThreads)
       }
     }
   }
-  for (int o = 1; o < F; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+  CGR_TL(3);
   __syncthreads();
+  CGR_TL(4);
   if (done != 0.0 || s_bad) return;
   const double alpha = s_alpha;
   double acc = 0.0;
   if (lead) {
+    double sum = 0.0;
+    for (int ff = 0; ff < F; ++ff) sum += part[ff * epb + tid];
     const double o = __dadd_rn(__dmul_rn(scale, sum), __dmul_rn(lam, si));
-    Hs[i] = o;
-    p[i] = np_axpy(pi, alpha, si);
+    Hs[il] = o;
+    p[il] = np_axpy(pi, alpha, si);
     const double ri = np_axmy(ri0, alpha, o);
-    r[i] = ri;
+    r[il] = ri;
     acc = ri * ri;
   }
+  CGR_TL(5);
   const double b = block_sum<kFinThreads>(acc, sh);
   if (tid == 0) scratch(state, T)[blockIdx.x] = b;
   CGR_TL(2);

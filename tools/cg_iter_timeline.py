@@ -35,9 +35,9 @@ NB = 26
 cl = (ctypes.c_ulonglong * (160 * NB * 10))()
 lib.snx_debug_cl_timeline(cl)
 cl = np.frombuffer(cl, dtype=np.uint64).reshape(160, NB, 10).astype(np.int64)
-cr = (ctypes.c_ulonglong * (256 * 3))()
+cr = (ctypes.c_ulonglong * (256 * 6))()
 lib.snx_debug_cgr_timeline(cr)
-cr = np.frombuffer(cr, dtype=np.uint64).reshape(256, 3).astype(np.int64)
+cr = np.frombuffer(cr, dtype=np.uint64).reshape(256, 6).astype(np.int64)
 vb = (ctypes.c_ulonglong * (2 * 256 * 2))()
 lib.snx_debug_vec_timeline(vb)
 v = np.frombuffer(vb, dtype=np.uint64).reshape(2, 256, 2).astype(np.int64)
@@ -52,5 +52,7 @@ print(f"{name}: product CTAs entry {us(ent.min()):6.2f}..{us(ent.max()):6.2f}  d
 print(f"cg_step1_rows   entry {us(cr[:, 0].min()):6.2f}..{us(cr[:, 0].max()):6.2f}  dependency met "
       f"{us(np.median(cr[:, 1])):6.2f}  exit med {us(np.median(cr[:, 2])):6.2f} max "
       f"{us(cr[:, 2].max()):6.2f}")
+print("cg_step1_rows medians: loads+F-reduce " + f"{us(np.median(cr[:, 3])):6.2f}, alpha shared "
+      f"{us(np.median(cr[:, 4])):6.2f}, element updates {us(np.median(cr[:, 5])):6.2f}")
 print(f"cg_step2        dependency met {us(v[1, :, 0].min()):6.2f}..{us(np.median(v[1, :, 0])):6.2f}"
       f"  exit med {us(np.median(v[1, :, 1])):6.2f} max {us(v[1, :, 1].max()):6.2f}")
