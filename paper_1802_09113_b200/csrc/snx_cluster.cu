@@ -1129,28 +1129,39 @@ __global__ void __launch_bounds__(kFinThreads)
   pdl_wait();
   if (skip != nullptr && *skip != 0.0) return;
   __shared__ double sh[kFinThreads / 32];
+  __shared__ double part[kFinThreads];
   const int t = threadIdx.x;
-  const int64_t i = (int64_t)blockIdx.x * epb + t / F;
-  const int f = t % F;
-  const bool own = (t / F) < epb && i < d;
-  double s = 0.0;
-  if (own) {
-    int c = f;
-    for (; c + 7 * F < ncl; c += 8 * F) {
-      double v[8];
+  // thread (f, e) as in cg_step1_rows_kernel: coalesced partial rows, the F sums
+  // of an element added in f order by its lead thread
+  const int e = t % (int)epb, f = t / (int)epb;
+  const int64_t i = (int64_t)blockIdx.x * epb + e;
+  const bool own = f < F && i < d;
+  const int64_t il = (int64_t)blockIdx.x * epb + t;
+  const bool lead = t < epb && il < d;
+  const double b = lead ? base[il] : 0.0;
+  {
+    constexpr int kML = 16;
+    double v[kML];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = __ldcg(gp + (int64_t)(c + k * F) * d + i);
-#pragma unroll
-      for (int k = 0; k < 8; ++k) s += v[k];
+    for (int k = 0; k < kML; ++k) {
+      const int c = f + k * F;
+      v[k] = own && c < ncl ? __ldcg(gp + (int64_t)c * d + i) : 0.0;
     }
-    for (; c < ncl; c += F) s += __ldcg(gp + (int64_t)c * d + i);
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < kML; ++k)
+      if (f + k * F < ncl) s += v[k];
+    if (own)
+      for (int c = f + kML * F; c < ncl; c += F) s += __ldcg(gp + (int64_t)c * d + i);
+    if (own) part[f * epb + e] = s;
   }
-  for (int o = 1; o < F; o <<= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __syncthreads();
   double bo = 0.0, bb = 0.0;
-  if (own && f == 0) {
-    const double b = base[i];
+  if (lead) {
+    double s = 0.0;
+    for (int ff = 0; ff < F; ++ff) s += part[ff * epb + t];
     const double o = __dadd_rn(__dmul_rn(scale, s), __dmul_rn(lam, b));
-    out[i] = o;
+    out[il] = o;
     bo = b * o;
     bb = b * b;
   }
