@@ -848,14 +848,21 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
   if (prep) {
     // h only: no X^T U, so a stage is released right after its logits and the
     // logits stream at the rate the exchange and the row algebra drain them
+    CL_TL(-1, 2);
     for (int b = 0; b < nb; ++b) {
+      CL_TL(b, 0);
       if (b >= kNB3) mbar_wait(&redfree[b % kNB3], ((b / kNB3) - 1) & 1);
       __syncwarp();
+      CL_TL(b, 2);
       vphase(b);
+      CL_TL(b, 1);
       if (lane == 0) mbar_arrive(&rg.empty[b % S]);
     }
+    CL_TL(-1, 3);
+    CL_TL(-1, 4);
     cluster_wait();          // the prologue's arrive
     cluster_sync_relaxed();  // no CTA leaves while a peer may still address its smem
+    CL_TL(-1, 5);
     return;
   }
   for (int b = 0; b < kLA && b < nb; ++b) vphase(b);
