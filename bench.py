@@ -360,10 +360,18 @@ def secondary(snx, torch, args):
         out[name]["workload"] = f"{name}-shape {n}x{p} C={nC}, 5% S_H, fp64"
         del A, y
     if args.dtype == "f64":
+        from paper_1802_09113_b200 import device as snx_device
+
         A, y = make_problem()
+        out["cifar10_f32"] = shape_rate(snx, torch, A, y, C, "f32")
+        out["cifar10_f32"]["workload"] = (
+            "cifar10-shape, f32 data: the one-pass kernel on f32 rows widened to fp64 "
+            "(half the bytes of X_S, fp64 arithmetic)")
+        snx_device.F32_TENSOR_CORES = True  # the tcgen05 pair on the same data, for comparison
         out["cifar10_f32_tensor_core"] = shape_rate(snx, torch, A, y, C, "f32")
         out["cifar10_f32_tensor_core"]["workload"] = (
             "cifar10-shape, f32 data, Hessian GEMMs on tcgen05 (bf16 two-term split), 1e-4 path")
+        snx_device.F32_TENSOR_CORES = False
     # estimate_lipschitz (bench.py:116-138 of the reference): 200 power
     # iterations of the full-data (50k x 3072) Hessian product at x = 0
     A, y = make_problem()

@@ -121,9 +121,10 @@ int snx_hess_apply(int dtype, const void *Xs, int64_t ldx, int64_t nrows, int32_
 /* The gather-fused form of snx_hess_apply: the sample is rows[0..nrows) of X
  * (sorted int64 indices, duplicates allowed), read in place -- no X_S copy.
  * H comes from snx_hess_prepare(..., rows, ..., Xs_out = NULL, ...), which
- * fuses the same gather.  fp64 data with K <= 9 (snx_rowpass_fused != 0):
- * the one-pass cluster kernel (csrc/snx_cluster.cu) streams every sample row
- * once per product. */
+ * fuses the same gather.  K <= 9 (snx_rowpass_fused != 0): the one-pass
+ * cluster kernel (csrc/snx_cluster.cu) streams every sample row once per
+ * product -- fp64 data, or f32 data widened to fp64 in shared memory (fp64
+ * arithmetic); H is fp64 for both (rows may be NULL: all nrows rows). */
 int snx_rowpass_fused(int dtype, int32_t p, int32_t K);
 int snx_hess_apply_rows(int dtype, const void *X, int64_t ldx, const int64_t *rows,
                         int64_t nrows, int32_t p, int32_t K, const void *H, const double *v,
@@ -205,7 +206,7 @@ int snx_cg_update(int32_t t, int32_t max_iters, int64_t d, const double *Hs,
                   const double *dots, double *r, double *s, double *p, double *p_best,
                   double *state, void *stream);
 
-/* One CG iteration t with the one-pass product (fp64, K <= 9: snx_rowpass_fused):
+/* One CG iteration t with the one-pass product (K <= 9: snx_rowpass_fused):
  * equivalent to snx_hess_apply_rows(s -> Hs, skip = done flag of slot t) +
  * snx_cg_update(t, ...), with the product's finalize fused into the CG's first
  * kernel -- the curvature s.Hs = scale * sum_rows V.U + lam * s.s is formed from

@@ -74,7 +74,7 @@ constexpr int kSA = kLA + 2;       // column split: ring stages (V(b + kLA), the
                                    // for X^T U, one loading)
 
 struct Args {
-  const double *X;
+  const void *X;          // [n][ldx] fp64 or f32 (the kernels' element type T)
   int64_t ldx;
   const int64_t *rows;    // nullable: sample position -> source row
   int64_t nrows;
@@ -266,9 +266,20 @@ __device__ __forceinline__ void cl_stamp(int b, int ev) {
 
 // ---------------------------------------------------------------- shared pieces
 struct Ring {
-  double *tiles, *Qs, *side;
+  void *tiles;  // [S][R][WS] elements of the data type
+  double *Qs, *side;
   uint64_t *full, *empty;
 };
+
+// X elements of either data type, widened to fp64 for the fp64 MMAs (f32 data:
+// exact conversion, the arithmetic stays fp64)
+__device__ __forceinline__ double2 ld2d(const double *p) {
+  return *reinterpret_cast<const double2 *>(p);
+}
+__device__ __forceinline__ double2 ld2d(const float *p) {
+  const float2 v = *reinterpret_cast<const float2 *>(p);
+  return make_double2((double)v.x, (double)v.y);
+}
 
 // Producer warp: row indices prefetched one block ahead; X slices by TMA bulk
 // copies (one per row); side data (h rows / labels) by cp.async; each lane
@@ -276,12 +287,13 @@ struct Ring {
 // `early` the first stages' X copies go out before the predecessor grid has
 // finished (X and the row indices are older than it); everything the
 // predecessor may write (weights, h, labels, the skip flag) waits.
-template <int R, int K>
+template <int R, int K, typename T>
 __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t row_lo,
                                         int64_t row_hi, int nb, int c0, int wq, int lane,
                                         int *sh_skip) {
   const int S = R == kRA ? kSA : a.S;  // column split: compile-time ring depth
   const int WS = a.WS;
+  const T *X = static_cast<const T *>(a.X);
   const bool apply = a.mode == kApply, grad = a.mode == kGrad;
   constexpr int IPL = (R + 31) / 32;
   auto load_idx = [&](int b, int64_t(&dst)[IPL]) {
@@ -298,8 +310,8 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
     if (b >= S) mbar_wait(&rg.empty[s], ((b / S) - 1) & 1);
     const int64_t r0 = row_lo + (int64_t)b * R;
     const int nr = (int)min((int64_t)R, row_hi - r0);
-    double *tile = rg.tiles + (size_t)s * R * WS;
-    const unsigned bytes = (unsigned)wq * 8u;
+    T *tile = static_cast<T *>(rg.tiles) + (size_t)s * R * WS;
+    const unsigned bytes = (unsigned)(wq * sizeof(T));
     if (R == kRR && !grad) {
       // row split (p <= 64), Hessian passes: rows of a few hundred bytes -- one
       // TMA request per row serialises on the copy engine (covertype product
@@ -311,9 +323,9 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
       for (int j = 0; j < IPL; ++j) {
         const int e = lane + 32 * j;
         if (e < nr) {
-          const double *src = a.X + idx[j] * a.ldx + c0;
-          double *dst = tile + (size_t)e * WS;
-          for (int c = 0; c < pieces; ++c) cp_async16(dst + 2 * c, src + 2 * c);
+          const char *src = reinterpret_cast<const char *>(X + idx[j] * a.ldx + c0);
+          char *dst = reinterpret_cast<char *>(tile + (size_t)e * WS);
+          for (int c = 0; c < pieces; ++c) cp_async16(dst + 16 * c, src + 16 * c);
         }
       }
     } else {
@@ -323,7 +335,7 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
         for (int j = 0; j < IPL; ++j) {
           const int e = lane + 32 * j;
           if (e < nr)
-            bulk_g2s(tile + (size_t)e * WS, a.X + idx[j] * a.ldx + c0, bytes, &rg.full[s]);
+            bulk_g2s(tile + (size_t)e * WS, X + idx[j] * a.ldx + c0, bytes, &rg.full[s]);
         }
       }
     }
@@ -411,8 +423,8 @@ __device__ __forceinline__ void load_q8(const Args &a, double *q8, int c0, int w
 // lane's A and B values are 2 contiguous 16-B loads each).  Returns the lane's
 // C = (V[g][2t], V[g][2t+1]) and v8 = the row's class-8 logit partial (summed
 // over the 4 lanes of the group, K == 9).
-template <int K, int NCH>
-__device__ __forceinline__ void vgroup(const double *xrow, const double *q8row,
+template <int K, int NCH, typename T>
+__device__ __forceinline__ void vgroup(const T *xrow, const double *q8row,
                                        const double (&qf)[NCH][4], int ch0, int step, int nch,
                                        double (&c2)[2], double &v8) {
   // two independent accumulator chains (steps 0,1 and 2,3), added at the end
@@ -421,8 +433,8 @@ __device__ __forceinline__ void vgroup(const double *xrow, const double *q8row,
   for (int i = 0; i < NCH; ++i) {
     const int ch = ch0 + step * i;
     if (ch < nch) {
-      const double2 xa = *reinterpret_cast<const double2 *>(xrow + 16 * ch);
-      const double2 xb = *reinterpret_cast<const double2 *>(xrow + 16 * ch + 2);
+      const double2 xa = ld2d(xrow + 16 * ch);
+      const double2 xb = ld2d(xrow + 16 * ch + 2);
       dmma(ca, xa.x, qf[i][0]);
       dmma(cb, xb.x, qf[i][2]);
       dmma(ca, xa.y, qf[i][1]);
@@ -446,16 +458,16 @@ __device__ __forceinline__ void vgroup(const double *xrow, const double *q8row,
 // X^T U of one 8-row group into the warp's column tiles: tile m covers
 // columns 8 (m0 + mstep m) .. +7; rows of step s, lane t: 2t + s (each bank
 // hit by two of the four rows).  u points at the group's U rows (stride kUP).
-template <int K, int NMT>
-__device__ __forceinline__ void xgroup(const double *x0, int WS, const double *u, int nr, int g,
+template <int K, int NMT, typename T>
+__device__ __forceinline__ void xgroup(const T *x0, int WS, const double *u, int nr, int g,
                                        int t, int m0, int mstep, int nmt, double (&acc)[NMT][2],
                                        double (&acc8)[NMT]) {
   const double ua0 = u[(2 * t) * kUP + g], ua1 = u[(2 * t + 1) * kUP + g];
   const double u80 = K == 9 ? u[(2 * t) * kUP + 8] : 0.0;
   const double u81 = K == 9 ? u[(2 * t + 1) * kUP + 8] : 0.0;
   const bool ok0 = 2 * t < nr, ok1 = 2 * t + 1 < nr;
-  const double *xa = x0 + (size_t)(2 * t) * WS + g;
-  const double *xb = xa + WS;
+  const T *xa = x0 + (size_t)(2 * t) * WS + g;
+  const T *xb = xa + WS;
 #pragma unroll
   for (int m = 0; m < NMT; ++m) {
     const int mt = m0 + mstep * m;
@@ -477,8 +489,8 @@ __device__ __forceinline__ void xgroup(const double *x0, int WS, const double *u
 // rows 2t, 2t + 1, B = U rows 2t, 2t + 1 at class g, C = (columns g, g + 8) x
 // (classes 2t, 2t + 1); class 8 by DFMA (per lane: rows 2t, 2t + 1 of columns
 // g, g + 8; the four lanes of a group cover the 8 rows).
-template <int K, int NMT>
-__device__ __forceinline__ void xgroup16(const double *x0, int WS, const double *u, int nr, int g,
+template <int K, int NMT, typename T>
+__device__ __forceinline__ void xgroup16(const T *x0, int WS, const double *u, int nr, int g,
                                          int t, int m0, int mstep, int nmt16,
                                          double (&acc)[NMT][4], double (&acc8)[NMT][2]) {
   // the MMA's k index runs over the block's rows permuted (k = t -> row 2t,
@@ -488,8 +500,8 @@ __device__ __forceinline__ void xgroup16(const double *x0, int WS, const double 
   const double u8a = K == 9 ? u[(2 * t) * kUP + 8] : 0.0;
   const double u8b = K == 9 ? u[(2 * t + 1) * kUP + 8] : 0.0;
   const bool okt = 2 * t < nr, okt4 = 2 * t + 1 < nr;
-  const double *xa = x0 + (size_t)(2 * t) * WS + g;
-  const double *xb = xa + WS;
+  const T *xa = x0 + (size_t)(2 * t) * WS + g;
+  const T *xb = xa + WS;
 #pragma unroll
   for (int m = 0; m < NMT; ++m) {
     const int mt = m0 + mstep * m;
@@ -647,14 +659,15 @@ __device__ __forceinline__ void rows_block(const Args &a, const Ring &rg, const 
 }
 
 // ---------------------------------------------------------------- column split
-template <int K, int NRW>
+template <int K, int NRW, typename T>
 __global__ void __launch_bounds__(nta<NRW>(), 1)
     cluster_rowpass_kernel(const __grid_constant__ Args a) {
   constexpr int R = kRA;
   pdl_trigger();  // the finalize kernel may launch now (it waits for this grid)
   extern __shared__ __align__(1024) unsigned char smem[];
   Ring rg;
-  rg.tiles = reinterpret_cast<double *>(smem + a.o_tiles);          // [S][R][WS]
+  rg.tiles = smem + a.o_tiles;                                       // [S][R][WS] T
+  T *tiles = static_cast<T *>(rg.tiles);
   rg.side = reinterpret_cast<double *>(smem + a.o_side);            // [S][R][K] h | [S][R] int
   double *Q8 = reinterpret_cast<double *>(smem + a.o_q);            // [WQ] class-8 weights
   double *Us = reinterpret_cast<double *>(smem + a.o_u);            // [3][R][kUP]
@@ -702,7 +715,7 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
   // zero the tile columns no bulk copy writes (the chunks / tiles read them)
   for (int i = tid; i < S * R * (WS - wq); i += nta<NRW>()) {
     const int r = i / (WS - wq), j = i - r * (WS - wq);
-    rg.tiles[(size_t)r * WS + wq + j] = 0.0;
+    tiles[(size_t)r * WS + wq + j] = T(0);
   }
   __syncthreads();
   CL_TL(-1, 6);
@@ -719,7 +732,7 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
   CL_TL(-1, 7);
 
   if (warp == kNWA) {  // ---------------------------------------- producer
-    produce<R, K>(a, rg, row_lo, row_hi, nb, c0, wq, lane, &sh_skip);
+    produce<R, K, T>(a, rg, row_lo, row_hi, nb, c0, wq, lane, &sh_skip);
     cluster_wait();
     cluster_sync_relaxed();
     return;
@@ -830,9 +843,9 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
     const int s = b % S;
     mbar_wait(&rg.full[s], (b / S) & 1);
     __syncwarp();  // reconverge before the warp-wide MMAs
-    const double *tile = rg.tiles + (size_t)s * R * WS;
+    const T *tile = tiles + (size_t)s * R * WS;
     double c2[2], v8;
-    vgroup<K, kNCHA>(tile + (size_t)g8 * WS + 4 * t4, Q8 + 4 * t4, qf, warp, kNWA, nch, c2, v8);
+    vgroup<K, kNCHA, T>(tile + (size_t)g8 * WS + 4 * t4, Q8 + 4 * t4, qf, warp, kNWA, nch, c2, v8);
     double *rbw = red + (size_t)(b % kNB3) * kNWA * R * K + (size_t)warp * R * K + g8 * K;
     if (2 * t4 < K) rbw[2 * t4] = c2[0];
     if (2 * t4 + 1 < K) rbw[2 * t4 + 1] = c2[1];
@@ -877,7 +890,7 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
     if (!prep) {
       const int64_t r0 = row_lo + (int64_t)b * R;
       const int nr = (int)min((int64_t)R, row_hi - r0);
-      xgroup16<K, NM16>(rg.tiles + (size_t)(b % S) * R * WS, WS,
+      xgroup16<K, NM16, T>(tiles + (size_t)(b % S) * R * WS, WS,
                         Us + (size_t)(b % kNB3) * R * kUP, nr, g8, t4, warp, kNWA, nmt16, acc,
                         acc8);
     }
@@ -914,14 +927,15 @@ __global__ void __launch_bounds__(nta<NRW>(), 1)
 // p <= 64: warp w owns rows 8w..8w+7 of every 64-row block completely (V over
 // all columns, the row algebra in registers, X^T U of its rows); the CTA's
 // K x p partial is reduced over the warps once at the end.
-template <int K>
+template <int K, typename T>
 __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant__ Args a) {
   constexpr int R = kRR;
   constexpr int NMT = 8;  // column tiles: p <= 64
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem[];
   Ring rg;
-  rg.tiles = reinterpret_cast<double *>(smem + a.o_tiles);  // [S][R][WS]
+  rg.tiles = smem + a.o_tiles;  // [S][R][WS] T
+  T *tiles = static_cast<T *>(rg.tiles);
   rg.side = reinterpret_cast<double *>(smem + a.o_side);    // [S][R][K] h | [S][R] int
   double *Q8 = reinterpret_cast<double *>(smem + a.o_q);    // [WQ] class-8 weights
   double *Uw = reinterpret_cast<double *>(smem + a.o_u);    // [NW][8][kUP] per warp
@@ -949,11 +963,11 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
   }
   for (int i = tid; i < S * R * (WS - wq); i += kNTR) {
     const int r = i / (WS - wq), j = i - r * (WS - wq);
-    rg.tiles[(size_t)r * WS + wq + j] = 0.0;
+    tiles[(size_t)r * WS + wq + j] = T(0);
   }
   __syncthreads();
   if (warp == kNW) {
-    produce<R, K>(a, rg, row_lo, row_hi, nb, 0, wq, lane, &sh_skip);
+    produce<R, K, T>(a, rg, row_lo, row_hi, nb, 0, wq, lane, &sh_skip);
     return;
   }
   pdl_wait();
@@ -983,9 +997,9 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
     mbar_wait(&rg.full[s], ph);
     __syncwarp();  // reconverge before the warp-wide MMAs
     if (ng > 0) {
-      const double *tile = rg.tiles + (size_t)s * R * WS + (size_t)gr0 * WS;
+      const T *tile = tiles + (size_t)s * R * WS + (size_t)gr0 * WS;
       double c2[2], v8;
-      vgroup<K, kNCH>(tile + (size_t)g * WS + 4 * t, Q8 + 4 * t, qf, 0, 1, nch, c2, v8);
+      vgroup<K, kNCH, T>(tile + (size_t)g * WS + 4 * t, Q8 + 4 * t, qf, 0, 1, nch, c2, v8);
       // row algebra: lane (g, t) holds classes 2t, 2t+1 of row g (+ class 8)
       const int row = gr0 + g;
       const bool rv = g < ng;
@@ -1048,7 +1062,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
       }
       __syncwarp();
       if (!prep)
-        xgroup<K, NMT>(rg.tiles + (size_t)s * R * WS + (size_t)gr0 * WS, WS, u, ng, g, t, 0, 1,
+        xgroup<K, NMT, T>(tiles + (size_t)s * R * WS + (size_t)gr0 * WS, WS, u, ng, g, t, 0, 1,
                        nmt, acc, acc8);
       __syncwarp();
     }
@@ -1061,7 +1075,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
   // the CTA's partial: warps reduced in order through shared memory (the tiles)
   consumer_sync(kNC);
   if (!prep) {
-    double *comb = rg.tiles;  // [NW][64 columns][kUP]
+    double *comb = static_cast<double *>(rg.tiles);  // [NW][64 columns][kUP] (over the tiles)
 #pragma unroll
     for (int m = 0; m < NMT; ++m) {
       const double s8 = K == 9 ? gsum<4>(acc8[m]) : 0.0;
@@ -1314,20 +1328,20 @@ static size_t smem_cap(KernT kern) {
   return (size_t)optin - fa.sharedSizeBytes;
 }
 
-template <int K>
+template <int K, typename T>
 static size_t cap_a() {
   static size_t c = 0;
-  if (!c) c = smem_cap(cluster_rowpass_kernel<K, 2>);
+  if (!c) c = smem_cap(cluster_rowpass_kernel<K, 2, T>);
   return c;
 }
-template <int K>
+template <int K, typename T>
 static size_t cap_r() {
   static size_t c = 0;
-  if (!c) c = smem_cap(rowsplit_kernel<K>);
+  if (!c) c = smem_cap(rowsplit_kernel<K, T>);
   return c;
 }
 
-template <int K>
+template <int K, typename T>
 static void layout(Plan &pl, int S) {
   size_t off = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -1336,7 +1350,7 @@ static void layout(Plan &pl, int S) {
     off += bytes;
     return (int)o;
   };
-  pl.o_tiles = take((size_t)S * pl.R * pl.WS * 8, 1024);
+  pl.o_tiles = take((size_t)S * pl.R * pl.WS * sizeof(T), 1024);
   pl.o_q = take((size_t)pl.WQ * 8, 16);
   pl.o_side = take((size_t)S * pl.R * K * 8, 16);
   if (pl.split == 0) {
@@ -1349,20 +1363,20 @@ static void layout(Plan &pl, int S) {
     pl.o_vr = pl.o_red = 0;
     pl.o_bar = take((size_t)(2 * S) * 8, 8);
     // the final warp reduction reuses the tiles: [NW][64][kUP] doubles
-    if ((size_t)S * pl.R * pl.WS * 8 < (size_t)kNW * 64 * kUP * 8) off = (size_t)1 << 30;
+    if ((size_t)S * pl.R * pl.WS * sizeof(T) < (size_t)kNW * 64 * kUP * 8) off = (size_t)1 << 30;
   }
   pl.smem = off;
   pl.S = S;
 }
 
-template <int K>
+template <int K, typename T>
 static int max_clusters(int cs, size_t smem) {
   static int cache[4] = {-1, -1, -1, -1};
   static size_t cache_smem[4] = {0, 0, 0, 0};
   const int ci = cs == 1 ? 0 : cs == 2 ? 1 : cs == 4 ? 2 : 3;
   if (cache[ci] >= 0 && cache_smem[ci] == smem) return cache[ci];
-  auto kern = cluster_rowpass_kernel<K, 2>;
-  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_a<K>());
+  auto kern = cluster_rowpass_kernel<K, 2, T>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap_a<K, T>());
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(cs * 64);
   cfg.blockDim = dim3(kNTA);
@@ -1384,7 +1398,7 @@ static int max_clusters(int cs, size_t smem) {
   return n;
 }
 
-template <int K>
+template <int K, typename T>
 static Plan make_plan(int P, int64_t nrows) {
   Plan pl{};
   if (P <= 64) {  // row split: the whole row in one CTA
@@ -1392,30 +1406,33 @@ static Plan make_plan(int P, int64_t nrows) {
     pl.cs = 1;
     pl.R = kRR;
     pl.wc = P;
-    pl.WS = pl.WQ = (P + 15) / 16 * 16 + 2;  // = 2 (mod 16): fragment loads spread over banks
+    // = 2 (mod 16) doubles: fragment loads spread over banks; f32 rows: = 4
+    // (mod 16) floats (16-B aligned for the copies)
+    pl.WS = pl.WQ = (P + 15) / 16 * 16 + (sizeof(T) == 8 ? 2 : 4);
     int S = 4;
     for (; S >= 2; --S) {
-      layout<K>(pl, S);
-      if (pl.smem <= cap_r<K>()) break;
+      layout<K, T>(pl, S);
+      if (pl.smem <= cap_r<K, T>()) break;
     }
-    if (pl.smem > cap_r<K>()) return Plan{};
+    if (pl.smem > cap_r<K, T>()) return Plan{};
     const int64_t want = nrows > 0 ? (nrows + kRR - 1) / kRR : 1;
     pl.ncl = (int)(want < sm_count() ? want : sm_count());
     pl.ok = 1;
     return pl;
   }
   for (int cs : {1, 2, 4, 8}) {
-    const int wc = ((P + cs - 1) / cs + 1) & ~1;
+    // slice width: even (fp64: 16-B aligned slices), a multiple of 4 for f32
+    const int wc = sizeof(T) == 8 ? ((P + cs - 1) / cs + 1) & ~1 : ((P + cs - 1) / cs + 3) & ~3;
     if ((wc + 7) / 8 > kNWA * kNMTA) continue;  // > 768 columns per CTA
     pl = Plan{};
     pl.split = 0;
     pl.cs = cs;
     pl.R = kRA;
     pl.wc = wc;
-    pl.WS = pl.WQ = (wc + 15) / 16 * 16 + 2;
-    layout<K>(pl, kSA);
-    if (pl.smem > cap_a<K>()) continue;
-    const int maxcl = max_clusters<K>(cs, pl.smem);
+    pl.WS = pl.WQ = (wc + 15) / 16 * 16 + (sizeof(T) == 8 ? 2 : 4);
+    layout<K, T>(pl, kSA);
+    if (pl.smem > cap_a<K, T>()) continue;
+    const int maxcl = max_clusters<K, T>(cs, pl.smem);
     const int64_t want = nrows > 0 ? (nrows + kRA - 1) / kRA : 1;
     pl.ncl = (int)(want < maxcl ? want : maxcl);
     if (pl.ncl < 1) pl.ncl = 1;
@@ -1430,13 +1447,16 @@ static bool disabled() {
   return off != 0;
 }
 
+// fp64 data, or f32 data widened to fp64 in shared memory (the arithmetic is
+// the fp64 path's either way)
 static Plan plan_for(int dtype, int p, int K, int64_t nrows) {
-  if (dtype != SNX_F64 || K < 1 || K > kMaxK || disabled()) return Plan{};
+  if ((dtype != SNX_F64 && dtype != SNX_F32) || K < 1 || K > kMaxK || disabled()) return Plan{};
   const int P = padded(p);
+  const bool f32 = dtype == SNX_F32;
   switch (K) {
 #define SNX_CL_K(KK) \
   case KK:           \
-    return make_plan<KK>(P, nrows);
+    return f32 ? make_plan<KK, float>(P, nrows) : make_plan<KK, double>(P, nrows);
     SNX_CL_K(1) SNX_CL_K(2) SNX_CL_K(3) SNX_CL_K(4) SNX_CL_K(5) SNX_CL_K(6) SNX_CL_K(7)
     SNX_CL_K(8) SNX_CL_K(9)
 #undef SNX_CL_K
@@ -1461,7 +1481,7 @@ static void fill(Args &a, const Plan &pl) {
   a.o_bar = pl.o_bar;
 }
 
-template <int K>
+template <int K, typename T>
 static int launch_k(const Plan &pl, Args &a, cudaStream_t st) {
   fill(a, pl);
   cudaLaunchConfig_t cfg = {};
@@ -1486,13 +1506,13 @@ static int launch_k(const Plan &pl, Args &a, cudaStream_t st) {
   cfg.numAttrs = na;
   if (pl.split == 0) {
     static bool attr = false;
-    auto k1 = cluster_rowpass_kernel<K, 1>;
-    auto k2 = cluster_rowpass_kernel<K, 2>;
+    auto k1 = cluster_rowpass_kernel<K, 1, T>;
+    auto k2 = cluster_rowpass_kernel<K, 2, T>;
     if (!attr) {
       if (cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)cap_a<K>()) != cudaSuccess ||
+                               (int)cap_a<K, T>()) != cudaSuccess ||
           cudaFuncSetAttribute(k2, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                               (int)cap_a<K>()) != cudaSuccess)
+                               (int)cap_a<K, T>()) != cudaSuccess)
         return check_launch("cluster_rowpass attributes");
       attr = true;
     }
@@ -1503,10 +1523,10 @@ static int launch_k(const Plan &pl, Args &a, cudaStream_t st) {
     return check_launch("cluster_rowpass");
   }
   static bool attr = false;
-  auto kern = rowsplit_kernel<K>;
+  auto kern = rowsplit_kernel<K, T>;
   if (!attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)cap_r<K>()) != cudaSuccess)
+                             (int)cap_r<K, T>()) != cudaSuccess)
       return check_launch("rowsplit attributes");
     attr = true;
   }
@@ -1516,11 +1536,12 @@ static int launch_k(const Plan &pl, Args &a, cudaStream_t st) {
   return check_launch("rowsplit_rowpass");
 }
 
-static int launch_any(const Plan &pl, int K, Args &a, cudaStream_t st) {
+static int launch_any(const Plan &pl, int K, int dtype, Args &a, cudaStream_t st) {
+  const bool f32 = dtype == SNX_F32;
   switch (K) {
 #define SNX_CL_K(KK) \
   case KK:           \
-    return launch_k<KK>(pl, a, st);
+    return f32 ? launch_k<KK, float>(pl, a, st) : launch_k<KK, double>(pl, a, st);
     SNX_CL_K(1) SNX_CL_K(2) SNX_CL_K(3) SNX_CL_K(4) SNX_CL_K(5) SNX_CL_K(6) SNX_CL_K(7)
     SNX_CL_K(8) SNX_CL_K(9)
 #undef SNX_CL_K
@@ -1578,14 +1599,15 @@ size_t cluster_ws_bytes(int dtype, int64_t nrows, int32_t p, int32_t K) {
 }
 
 // mode: 0 prep (hout), 1 apply (h, skip, dots -> out), 2 grad (labels, loss/corr -> out)
-int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+int cluster_rowpass(int mode, int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                    int64_t nrows,
                     int32_t p, int32_t K, const int32_t *labels, const double *w,
                     const double *h, double *hout, double scale, double lam,
                     const double *base, double *out, double *loss_out, long long *corr_out,
                     double *dots, const double *skip, int early, void *ws, size_t ws_bytes,
                     cudaStream_t st) {
   using namespace clp;
-  const Plan pl = plan_for(SNX_F64, p, K, nrows);
+  const Plan pl = plan_for(dtype, p, K, nrows);
   if (!pl.ok) {
     set_error("snx: no one-pass row-pass plan for p=%d K=%d", p, K);
     return 1;
@@ -1613,7 +1635,7 @@ int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows,
   a.corrp = cw.corrp;
   a.skip = skip;
   a.early = early;
-  if (launch_any(pl, K, a, st)) return 1;
+  if (launch_any(pl, K, dtype, a, st)) return 1;
   if (mode == kPrep) return 0;
   const int64_t d = (int64_t)K * p;
   const int64_t epb = (d + kDotBlocks - 1) / kDotBlocks;
@@ -1630,12 +1652,13 @@ int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows,
 // One CG iteration t on the sampled Hessian (cg.py:77-96): the one-pass product
 // of s (skipped once the solve is done) without a finalize pass, the fused
 // cg_step1 above, then cg_step2.
-int cluster_cg_iteration(const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+int cluster_cg_iteration(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                         int64_t nrows,
                          int32_t p, int32_t K, const double *h, double scale, double lam, int t,
                          int T, double *r, double *s, double *pv, double *pb, double *Hs,
                          double *state, int early, void *ws, size_t ws_bytes, cudaStream_t st) {
   using namespace clp;
-  const Plan pl = plan_for(SNX_F64, p, K, nrows);
+  const Plan pl = plan_for(dtype, p, K, nrows);
   if (!pl.ok || nrows < 1) {
     set_error("snx: no one-pass plan for the fused CG iteration (p=%d K=%d rows=%lld)", p, K,
               (long long)nrows);
@@ -1662,7 +1685,7 @@ int cluster_cg_iteration(const double *X, int64_t ldx, const int64_t *rows, int6
   a.corrp = cw.corrp;
   a.skip = state + (size_t)t * SNX_CG_SLOT + kDone;
   a.early = early;
-  if (launch_any(pl, K, a, st)) return 1;
+  if (launch_any(pl, K, dtype, a, st)) return 1;
   const int64_t d = (int64_t)K * p;
   const int64_t epb = (d + kDotBlocks - 1) / kDotBlocks;
   int F = 1;

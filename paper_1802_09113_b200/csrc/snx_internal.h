@@ -93,14 +93,16 @@ size_t rowpass_counter_bytes();  // the zero-at-rest counter block at workspace 
 bool cluster_supported(int dtype, int32_t p, int32_t K);
 bool cluster_grad_preferred(int dtype, int32_t p, int32_t K);
 size_t cluster_ws_bytes(int dtype, int64_t nrows, int32_t p, int32_t K);
-int cluster_rowpass(int mode, const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+int cluster_rowpass(int mode, int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                    int64_t nrows,
                     int32_t p, int32_t K, const int32_t *labels, const double *w,
                     const double *h, double *hout, double scale, double lam,
                     const double *base, double *out, double *loss_out, long long *corr_out,
                     double *dots, const double *skip, int early, void *ws, size_t ws_bytes,
                     cudaStream_t st);
 
-int cluster_cg_iteration(const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+int cluster_cg_iteration(int dtype, const void *X, int64_t ldx, const int64_t *rows,
+                         int64_t nrows,
                          int32_t p, int32_t K, const double *h, double scale, double lam, int t,
                          int T, double *r, double *s, double *pv, double *pb, double *Hs,
                          double *state, int early, void *ws, size_t ws_bytes, cudaStream_t st);

@@ -1326,14 +1326,16 @@ static int rowpass(int mode, int dtype, const void *X, int64_t ldx, int64_t nrow
   double *dotp = reinterpret_cast<double *>(wsb + lay.dot_part);
 
   // fp64, K <= 9: the one-pass cluster kernel (X streamed once per product)
+  // (f32 data: the gradient; its Hessian passes take the one-pass kernel only
+  // through the row-index entry points, whose h is fp64)
   if (nrows > 0 &&
-      ((mode == kHessApply && cluster_supported(dtype, p, K)) ||
+      ((mode == kHessApply && dtype == SNX_F64 && cluster_supported(dtype, p, K)) ||
        (mode == kGradient && cluster_grad_preferred(dtype, p, K)))) {
     if (mode == kGradient && out != nullptr &&
         launch_prep_weights(dtype, w, nullptr, 0.0, K, p, P, nullptr, dotp, counters + 15,
                             out + 1, st))
       return 1;
-    return cluster_rowpass(mode == kHessApply ? 1 : 2, static_cast<const double *>(X), ldx,
+    return cluster_rowpass(mode == kHessApply ? 1 : 2, dtype, X, ldx,
                            nullptr, nrows, p, K, labels, w, static_cast<const double *>(H),
                            nullptr, scale, lam, base, vec_out, out, corr_out, dots, skip,
                            (mode == kHessApply && gemm1_early_x()) ? 1 : 0, ws, ws_bytes, st);
@@ -1545,14 +1547,15 @@ int snx_hess_prepare(int dtype, const void *X, int64_t ldx, const int64_t *rows,
     return 1;
   }
   cudaStream_t st = (cudaStream_t)stream;
-  if (nrows > 0 && cluster_supported(dtype, p, K)) {
+  if (nrows > 0 && cluster_supported(dtype, p, K) && (dtype == SNX_F64 || Xs_out == nullptr)) {
     // one pass over X[rows]: the row gather is fused into the TMA loads; X_S is
-    // materialised only if the caller asks for it (Xs_out != NULL)
+    // materialised only if the caller asks for it (Xs_out != NULL).  f32 data:
+    // only without X_S (the fused path), and H_out is fp64
     if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
     if (rows != nullptr && Xs_out != nullptr &&
         gather(dtype, X, ldx, nullptr, rows, nrows, Xs_out, ld_out, nullptr, st))
       return 1;
-    return cluster_rowpass(0, static_cast<const double *>(X), ldx, rows, nrows, p, K, nullptr, w,
+    return cluster_rowpass(0, dtype, X, ldx, rows, nrows, p, K, nullptr, w,
                            nullptr, static_cast<double *>(H_out), 1.0, 0.0, nullptr, nullptr,
                            nullptr, nullptr, nullptr, nullptr, 0, ws, ws_bytes, st);
   }
@@ -1595,11 +1598,11 @@ int snx_hess_apply_cg_rows(int dtype, const void *X, int64_t ldx, const int64_t 
     return 1;
   }
   if (!cluster_supported(dtype, p, K) || nrows < 1) {
-    set_error("snx_hess_apply_cg_rows: fp64 data, K <= 9, nrows >= 1 only (snx_rowpass_fused)");
+    set_error("snx_hess_apply_cg_rows: K <= 9 and nrows >= 1 only (snx_rowpass_fused)");
     return 1;
   }
   if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
-  return cluster_cg_iteration(static_cast<const double *>(X), ldx, rows, nrows, p, K,
+  return cluster_cg_iteration(dtype, X, ldx, rows, nrows, p, K,
                               static_cast<const double *>(H), scale, lam, t, max_iters, r, s,
                               p_vec, p_best, Hs, state, gemm1_early_x() ? 1 : 0, ws, ws_bytes,
                               (cudaStream_t)stream);
@@ -1617,15 +1620,15 @@ int snx_hess_apply_rows(int dtype, const void *X, int64_t ldx, const int64_t *ro
     set_error("snx_hess_apply_rows: NULL v/Hv_out/H");
     return 1;
   }
-  if (rows == nullptr || nrows == 0)
+  if (nrows == 0 || (rows == nullptr && dtype == SNX_F64))
     return snx_hess_apply(dtype, X, ldx, nrows, p, K, H, v, scale, lam, Hv_out, dots, skip, ws,
                           ws_bytes, stream);
   if (!cluster_supported(dtype, p, K)) {
-    set_error("snx_hess_apply_rows: fp64 data with K <= 9 only (snx_rowpass_fused)");
+    set_error("snx_hess_apply_rows: K <= 9 only (snx_rowpass_fused)");
     return 1;
   }
   if (validate(dtype, X, ldx, nrows, p, K, ws, ws_bytes)) return 1;
-  return cluster_rowpass(1, static_cast<const double *>(X), ldx, rows, nrows, p, K, nullptr, v,
+  return cluster_rowpass(1, dtype, X, ldx, rows, nrows, p, K, nullptr, v,
                          static_cast<const double *>(H), nullptr, scale, lam, v, Hv_out, nullptr,
                          nullptr, dots, skip, gemm1_early_x() ? 1 : 0, ws, ws_bytes,
                          (cudaStream_t)stream);

@@ -12,6 +12,7 @@ itself, as the reference does, so full-sample runs use the unsampled path.
 torch owns the device memory; all arithmetic is done by libsnx kernels.
 """
 
+import os
 import weakref
 
 import numpy as np
@@ -186,6 +187,11 @@ class DeviceDataset:
         return self._ws
 
 
+# f32 data with K <= 9 takes the one-pass kernel (rows widened to fp64); True
+# sends it to the tcgen05 pair instead (A/B measurements: bench.py)
+F32_TENSOR_CORES = os.environ.get("SNX_F32_TC") == "1"
+
+
 class HessBuffers:
     """HBM buffers of one sampled Hessian (the sample's rows and h probabilities).
 
@@ -194,16 +200,17 @@ class HessBuffers:
     loop (cg.CgGraph) stays valid.  `owner` is the operator whose sample is
     currently prepared; any other operator re-prepares before use.
 
-    fp64 data with K <= 9 (`fused`): the kernels read the sample in place
-    through its row indices (a fixed-address copy in `rows`), nothing else is
-    materialised.  Otherwise the rows are gathered into `xs` (and, for f32, the
-    bf16 split X1 + X2 the tensor-core product reads)."""
+    K <= 9 (`fused`, fp64 or f32 data): the one-pass kernels read the sample in
+    place through its row indices (a fixed-address copy in `rows`); h is fp64
+    and nothing else is materialised (f32 rows are widened to fp64 in shared
+    memory).  Otherwise the rows are gathered into `xs` (and, for f32, the bf16
+    split X1 + X2 the tensor-core product reads)."""
 
     def __init__(self, base, m, gathered):
         dev = base.X.device
         mm = max(m, 1)
-        self.fused = base.code == _lib.F64 and bool(
-            _lib.load().snx_rowpass_fused(base.code, base.n_features, base.K))
+        self.fused = bool(_lib.load().snx_rowpass_fused(base.code, base.n_features, base.K)) \
+            and not (base.code == _lib.F32 and F32_TENSOR_CORES)
         self.rows = None
         self.xs = None
         if self.fused:
@@ -212,10 +219,11 @@ class HessBuffers:
         else:
             self.xs = torch.empty((mm, base.ld), dtype=base.X.dtype, device=dev) if gathered \
                 else base.X
-        self.h = torch.empty((mm, base.K), dtype=base.X.dtype, device=dev)
+        self.h = torch.empty((mm, base.K), dtype=torch.float64 if self.fused else base.X.dtype,
+                             device=dev)
         # f32: bf16 split X1 + X2 of the sample rows for the tensor-core product
         self.xs_tc = None
-        if base.code == _lib.F32:
+        if base.code == _lib.F32 and not self.fused:
             self.ldb = int(_lib.load().snx_tc_ld(base.n_features))
             rows = mm if gathered else max(base.X.shape[0], 1)
             self.xs_tc = torch.empty((2, rows, self.ldb), dtype=torch.bfloat16, device=dev)

@@ -1,7 +1,8 @@
-"""Tensor-core (tcgen05 kind::f16, two-term bf16 split) Hessian product of the f32 path
-against the fp64 oracle: ragged row / column counts around the 128-row,
-32-column and 128-column tile edges, every class count K = 1..16, sampled
-and unsampled operators, bit-identical reruns."""
+"""The f32 Hessian product against the fp64 oracle: for K = 10..16 the
+tensor-core pair (tcgen05 kind::f16, two-term bf16 split), for K <= 9 the
+one-pass kernel on f32 rows widened to fp64; ragged row / column counts around
+the tile edges, every class count K = 1..16, sampled and unsampled operators,
+bit-identical reruns."""
 
 import numpy as np
 import pytest
@@ -34,7 +35,9 @@ def test_tc_hess_apply_vs_oracle(n, p, C):
     ds = snx.DeviceDataset.from_numpy(A, y, C, dtype="f32")
     lam = 1e-3
     op = snx.HessianOperator(ds, x, lam, scale=1.7)
-    assert op._bufs.xs_tc is not None  # the tensor-core path is the one under test
+    # K <= 9: the one-pass kernel (f32 rows widened to fp64); K = 10..16: tcgen05
+    assert op._bufs.fused != (op._bufs.xs_tc is not None)
+    assert C - 1 <= 9 or op._bufs.xs_tc is not None
     h = oracle.hess_probs(A, y, C, x)
     ref = oracle.hess_apply(A, h, C, v, 1.7, lam)
     got = op.apply(v)
