@@ -97,3 +97,30 @@ def test_tiny_samples(m):
     h = oracle.hess_probs(A[rows], y[rows], C, x)
     ref = oracle.hess_apply(A[rows], h, C, v, n / m, 1e-3)
     assert rel_err(op.apply(v), ref) <= 1e-10
+
+
+@pytest.mark.parametrize("n,p,C", [(2000, 40, 10), (3000, 900, 5), (2500, 2000, 10)])
+def test_f32_rows_widened(n, p, C):
+    """f32 data on the one-pass kernel (rows copied as f32, widened to fp64 in
+    shared memory): the fp64 arithmetic on the f32-rounded data, so the product
+    and the gradient match the oracle on the rounded data to 1e-10 and the
+    original data to the declared 1e-4."""
+    A, y = oracle.synthetic_problem(n, p, C, seed=p)
+    A32 = A.astype(np.float32).astype(np.float64)
+    rng = np.random.default_rng(C)
+    x = 0.1 * rng.standard_normal((C - 1) * p)
+    v = rng.standard_normal((C - 1) * p)
+    lam = 1e-3
+    ds = snx.DeviceDataset.from_numpy(A, y, C, dtype="f32")
+    prob = snx.SoftmaxProblem(ds, lam)
+    orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, 0.2), 1)
+    op = orc.hessian_operator(x)
+    assert op._bufs.fused and op._bufs.xs_tc is None
+    s_h = orc.s_h
+    h = oracle.hess_probs(A32[s_h], y[s_h], C, x)
+    ref = oracle.hess_apply(A32[s_h], h, C, v, n / len(s_h), lam)
+    hv = op.apply(v)
+    assert rel_err(hv, ref) <= 1e-10
+    assert rel_err(hv, oracle.hess_apply(A[s_h], oracle.hess_probs(A[s_h], y[s_h], C, x), C, v,
+                                         n / len(s_h), lam)) <= 1e-4
+    assert rel_err(snx.gradient(prob, x), oracle.grad(A32, y, C, x, lam)) <= 1e-10
