@@ -255,7 +255,14 @@ __device__ __forceinline__ void cl_stamp(int b, int ev) {
   do {                                                                 \
     if (threadIdx.x == kNCA + 32 || threadIdx.x == kNCA + 64) cl_stamp((b), (ev)); \
   } while (0)
+#define CL_TLP(b, ev)                               \
+  do {                                              \
+    if (R == kRR && threadIdx.x == kNC) cl_stamp((b), (ev)); \
+  } while (0)
 #else
+#define CL_TLP(b, ev) \
+  do {                \
+  } while (0)
 #define CL_TL(b, ev) \
   do {               \
   } while (0)
@@ -281,12 +288,15 @@ __device__ __forceinline__ double2 ld2d(const float *p) {
   return make_double2((double)v.x, (double)v.y);
 }
 
-// Producer warp: row indices prefetched one block ahead; X slices by TMA bulk
-// copies (one per row); side data (h rows / labels) by cp.async; each lane
-// arrives on the stage's full barrier once its copies have landed.  With
-// `early` the first stages' X copies go out before the predecessor grid has
-// finished (X and the row indices are older than it); everything the
-// predecessor may write (weights, h, labels, the skip flag) waits.
+// Producer warp: the row indices of the first S blocks are loaded at once and
+// later ones one block ahead (registers: the ping-pong below keeps every array
+// index compile-time); X slices by TMA bulk copies (one per row), or by 16-B
+// cp.async pieces in the row split's Hessian passes; side data (h rows /
+// labels) by cp.async; each lane arrives on the stage's full barrier once its
+// copies have landed.  The first S stages' X copies go out before
+// griddepcontrol.wait (X and the row indices are older than the predecessor
+// grid); everything the predecessor may write (weights, h, labels, the skip
+// flag) waits.
 template <int R, int K, typename T>
 __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t row_lo,
                                         int64_t row_hi, int nb, int c0, int wq, int lane,
@@ -295,7 +305,11 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
   const int WS = a.WS;
   const T *X = static_cast<const T *>(a.X);
   const bool apply = a.mode == kApply, grad = a.mode == kGrad;
+  // row split, Hessian passes: X by cp.async pieces with the lane's own arrive
+  // per block; the consumers read h themselves (no side data)
+  const bool pieces_path = R == kRR && !grad;
   constexpr int IPL = (R + 31) / 32;
+  constexpr int kSMax = 4;
   auto load_idx = [&](int b, int64_t(&dst)[IPL]) {
     const int64_t r0 = row_lo + (int64_t)b * R;
     const int nr = (int)min((int64_t)R, row_hi - r0);
@@ -312,12 +326,13 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
     const int nr = (int)min((int64_t)R, row_hi - r0);
     T *tile = static_cast<T *>(rg.tiles) + (size_t)s * R * WS;
     const unsigned bytes = (unsigned)(wq * sizeof(T));
-    if (R == kRR && !grad) {
-      // row split (p <= 64), Hessian passes: rows of a few hundred bytes -- one
-      // TMA request per row serialises on the copy engine (covertype product
-      // 18.2 -> 15.9 us), so 16-B cp.async pieces, each lane its own rows;
-      // completion through the lane's noinc arrive (issue_side).  The streaming
-      // gradient pass keeps the bulk copies (measured 5 % faster there).
+    if (pieces_path) {
+      // rows of a few hundred bytes: one TMA request per row serialises on the
+      // copy engine (covertype product 18.2 -> 15.9 us), so 16-B cp.async
+      // pieces, each lane its own rows (a lane-contiguous mapping costs a
+      // division and two shuffles per piece: 4x slower to issue); each lane's
+      // noinc arrive covers this block and the earlier ones only.  The
+      // streaming gradient pass keeps the bulk copies (5 % faster there).
       const int pieces = (int)(bytes / 16u);
 #pragma unroll
       for (int j = 0; j < IPL; ++j) {
@@ -328,6 +343,7 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
           for (int c = 0; c < pieces; ++c) cp_async16(dst + 16 * c, src + 16 * c);
         }
       }
+      cp_async_mbar_arrive(&rg.full[s]);
     } else {
       if (lane == 0) mbar_expect_tx(&rg.full[s], bytes * (unsigned)nr);
       if (bytes > 0) {
@@ -341,6 +357,7 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
     }
   };
   auto issue_side = [&](int b, const int64_t(&idx)[IPL]) {
+    if (pieces_path) return;
     const int s = b % S;
     const int64_t r0 = row_lo + (int64_t)b * R;
     const int nr = (int)min((int64_t)R, row_hi - r0);
@@ -357,13 +374,21 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
     }
     cp_async_mbar_arrive(&rg.full[s]);
   };
-  int64_t idx[2][IPL];
-  int b = 0;
-  if (nb > 0) load_idx(0, idx[0]);
-  if (a.early) {
-    for (; b < nb && b < S; ++b) {
-      if (b + 1 < nb) load_idx(b + 1, idx[(b + 1) & 1]);
-      issue_x(b, idx[b & 1]);
+  // A programmatic dependent (apply) stages the first min(S, nb) blocks' X
+  // before griddepcontrol.wait, all their indices in flight at once; the side
+  // data (h) follows the wait.  Otherwise each block's side data goes right
+  // behind its X.  (grad is never launched early: its labels need the indices.)
+  const bool early = a.early && !grad;
+  const int nb0 = early ? min(nb, S) : 0;
+  if (early) {
+    int64_t e_idx[kSMax][IPL];
+#pragma unroll
+    for (int k = 0; k < kSMax; ++k)
+      if (k < nb0) load_idx(k, e_idx[k]);
+#pragma unroll
+    for (int k = 0; k < kSMax; ++k) {
+      if (k < nb0) issue_x(k, e_idx[k]);
+      CL_TLP(k, 2);
     }
   }
   pdl_wait();
@@ -371,17 +396,26 @@ __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t r
   __syncwarp();
   if (*sh_skip) {  // complete the staged phases (no copy left in flight), then leave
     cp_async_wait_all();
-    for (int bb = 0; bb < b; ++bb) {
-      mbar_arrive(&rg.full[bb % S]);
+    for (int bb = 0; bb < nb0; ++bb) {
+      if (!pieces_path) mbar_arrive(&rg.full[bb % S]);  // the side arrivals
       mbar_wait(&rg.full[bb % S], (bb / S) & 1);
     }
     return;
   }
-  for (int bb = 0; bb < b; ++bb) issue_side(bb, idx[bb & 1]);
-  for (; b < nb; ++b) {
-    if (b + 1 < nb) load_idx(b + 1, idx[(b + 1) & 1]);
-    issue_x(b, idx[b & 1]);
-    issue_side(b, idx[b & 1]);
+  CL_TLP(-1, 7);
+  int64_t cur[IPL], nxt[IPL];
+#pragma unroll
+  for (int j = 0; j < IPL; ++j) cur[j] = nxt[j] = 0;
+  for (int bb = 0; bb < nb0; ++bb) issue_side(bb, cur);  // apply: no use of the indices
+  // the rest: indices one block ahead
+  if (nb0 < nb) load_idx(nb0, cur);
+  for (int b = nb0; b < nb; ++b) {
+    if (b + 1 < nb) load_idx(b + 1, nxt);
+    issue_x(b, cur);
+    CL_TLP(b, 2);
+    issue_side(b, cur);
+#pragma unroll
+    for (int j = 0; j < IPL; ++j) cur[j] = nxt[j];
   }
 }
 
@@ -931,6 +965,7 @@ template <int K, typename T>
 __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant__ Args a) {
   constexpr int R = kRR;
   constexpr int NMT = 8;  // column tiles: p <= 64
+  CL_TL(-1, 0);
   pdl_trigger();
   extern __shared__ __align__(1024) unsigned char smem[];
   Ring rg;
@@ -966,19 +1001,23 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
     tiles[(size_t)r * WS + wq + j] = T(0);
   }
   __syncthreads();
+  CL_TL(-1, 6);
   if (warp == kNW) {
     produce<R, K, T>(a, rg, row_lo, row_hi, nb, 0, wq, lane, &sh_skip);
     return;
   }
   pdl_wait();
+  CL_TL(-1, 8);
   if (a.skip != nullptr && *a.skip != 0.0) return;
   const int g = lane >> 2, t = lane & 3;
   const int nch = (wq + 15) >> 4, nmt = (wq + 7) >> 3;
   double qf[kNCH][4];
   load_qfrag<K, kNCH>(a, 0, wq, g, t, 0, 1, nch, qf);
+  CL_TL(-1, 9);
   load_q8<K>(a, Q8, 0, wq, a.WQ, tid, kNC);
   cp_async_wait_all();
   consumer_sync(kNC);
+  CL_TL(-1, 1);
   double acc[NMT][2], acc8[NMT];
 #pragma unroll
   for (int m = 0; m < NMT; ++m) acc[m][0] = acc[m][1] = acc8[m] = 0.0;
@@ -995,20 +1034,27 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
     const int gr0 = 8 * warp;          // the warp's first row in the block
     const int ng = min(8, nr - gr0);   // its valid rows (warp-uniform)
     mbar_wait(&rg.full[s], ph);
+    CL_TL(b, 0);
     __syncwarp();  // reconverge before the warp-wide MMAs
     if (ng > 0) {
       const T *tile = tiles + (size_t)s * R * WS + (size_t)gr0 * WS;
+      const int row = gr0 + g;
+      const bool rv = g < ng;
+      // apply: the lane's h values straight from global memory, in flight
+      // during the logits MMAs
+      double h0 = 0.0, h1 = 0.0, h8 = 0.0;
+      if (apply && rv) {
+        const double *hr = a.h + (r0 + row) * K;
+        if (c0v) h0 = __ldcg(hr + 2 * t);
+        if (c1v) h1 = __ldcg(hr + 2 * t + 1);
+        if (K == 9) h8 = __ldcg(hr + (K == 9 ? 8 : 0));
+      }
       double c2[2], v8;
       vgroup<K, kNCH, T>(tile + (size_t)g * WS + 4 * t, Q8 + 4 * t, qf, 0, 1, nch, c2, v8);
       // row algebra: lane (g, t) holds classes 2t, 2t+1 of row g (+ class 8)
-      const int row = gr0 + g;
-      const bool rv = g < ng;
       const double z0 = c0v ? c2[0] : 0.0, z1 = c1v ? c2[1] : 0.0, z8 = K == 9 ? v8 : 0.0;
       double u0 = 0.0, u1 = 0.0, u8 = 0.0;
       if (apply) {
-        const double *hr = rg.side + ((size_t)s * R + row) * K;
-        const double h0 = (rv && c0v) ? hr[2 * t] : 0.0, h1 = (rv && c1v) ? hr[2 * t + 1] : 0.0;
-        const double h8 = (rv && K == 9) ? hr[K == 9 ? 8 : 0] : 0.0;
         const double w0 = z0 * h0, w1 = z1 * h1, w8 = z8 * h8;
         const double sm = gsum<4>(w0 + w1) + w8;  // softmax.py:207 rowsum(VW)
         u0 = w0 - h0 * sm;
@@ -1066,6 +1112,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
                        nmt, acc, acc8);
       __syncwarp();
     }
+    CL_TL(b, 3);
     if (lane == 0) mbar_arrive(&rg.empty[s]);
     if (++s == S) {
       s = 0;
@@ -1073,6 +1120,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
     }
   }
   // the CTA's partial: warps reduced in order through shared memory (the tiles)
+  CL_TL(-1, 3);
   consumer_sync(kNC);
   if (!prep) {
     double *comb = static_cast<double *>(rg.tiles);  // [NW][64 columns][kUP] (over the tiles)
@@ -1094,6 +1142,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
       if (col < a.p) a.gp[(int64_t)cl * d + (int64_t)c * a.p + col] = sm;
     }
   }
+  CL_TL(-1, 4);
   if (grad || apply) {  // apply: lossp[cl] = the CTA's sum of V.U (curvature)
     const double l = warp_allsum(loss_acc);
     unsigned long long cc = corr_acc;
@@ -1115,6 +1164,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
       a.corrp[cl] = ct;
     }
   }
+  CL_TL(-1, 5);
 }
 
 #ifdef SNX_CL_TIMELINE
@@ -1146,8 +1196,10 @@ __global__ void __launch_bounds__(kFinThreads)
                     double *__restrict__ out, double *dots, const double *skip,
                     const double *lossp, const unsigned long long *corrp, double *loss_out,
                     long long *corr_out) {
+  CGR_TL(0);
   pdl_trigger();  // the next row pass may start staging its X tiles (it waits for this grid)
   pdl_wait();
+  CGR_TL(1);
   if (skip != nullptr && *skip != 0.0) return;
   __shared__ double sh[kFinThreads / 32];
   __shared__ double part[kFinThreads];
@@ -1209,6 +1261,7 @@ __global__ void __launch_bounds__(kFinThreads)
       if (corr_out != nullptr) *corr_out = (long long)cc;
     }
   }
+  CGR_TL(2);
 }
 
 // The CG iteration's first half (cg.py:77-86) fused with the product's

@@ -38,6 +38,8 @@ st = torch.cuda.current_stream()
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 if mode == "prep":
     run = lambda: orc.hessian_operator(x)  # noqa: E731
+elif mode == "grad":  # the full-data gradient pass
+    run = lambda: orc.gradient_device(x)  # noqa: E731
 elif mode == "cg":  # the products of a captured CG solve (the stamps: its last product)
     from paper_1802_09113_b200 import cg as cgmod
     run = lambda: cgmod.cg_graph_for(op, 10, 1e-12).run(g)  # noqa: E731
@@ -93,3 +95,13 @@ for c in used:
             d["xchg_peers"].append(r[8] - r[7])
             d["xchg_rows"].append(r[9] - r[8])
 print("median phase us: " + ", ".join(f"{k} {np.median(v) / 1e3:.3f}" for k, v in d.items() if v))
+if mode in ("b2b", "sync"):  # the last product's finalize (same clock)
+    cr = (ctypes.c_ulonglong * (256 * 6))()
+    _lib.load().snx_debug_cgr_timeline(cr)
+    cr = np.frombuffer(cr, dtype=np.uint64).reshape(256, 6).astype(np.int64)
+    ok = cr[:, 0] >= t0
+    if ok.any():
+        ext = np.array([t[c, 0, 5] for c in used])
+        print(f"product exit med {rel(np.median(ext)):7.2f} max {rel(ext.max()):7.2f}; finalize "
+              f"entry {rel(cr[ok, 0].min()):7.2f} dependency met {rel(np.median(cr[ok, 1])):7.2f}"
+              f" exit med {rel(np.median(cr[ok, 2])):7.2f} max {rel(cr[ok, 2].max()):7.2f}")
