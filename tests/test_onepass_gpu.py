@@ -124,3 +124,30 @@ def test_f32_rows_widened(n, p, C):
     assert rel_err(hv, oracle.hess_apply(A[s_h], oracle.hess_probs(A[s_h], y[s_h], C, x), C, v,
                                          n / len(s_h), lam)) <= 1e-4
     assert rel_err(snx.gradient(prob, x), oracle.grad(A32, y, C, x, lam)) <= 1e-10
+
+
+@pytest.mark.parametrize("n,p,C", SHAPES)
+def test_cg_early_stop_skips_products(n, p, C):
+    """A loose tolerance stops CG after a few iterations: the remaining products
+    of the captured solve see the done flag and leave (the producer completes the
+    ring stages it staged before griddepcontrol.wait); the result is the
+    oracle's, and a second solve on the same graph reproduces it bit for bit."""
+    A, y = oracle.synthetic_problem(n, p, C, seed=3 * p + C)
+    rng = np.random.default_rng(n)
+    x = 0.1 * rng.standard_normal((C - 1) * p)
+    lam = 1e-2
+    ds = snx.DeviceDataset.from_numpy(A, y, C)
+    orc = snx.SubsampledOracle(snx.SoftmaxProblem(ds, lam), snx.SampleConfig(1.0, 0.2), 5)
+    op = orc.hessian_operator(x)
+    s_h = orc.s_h
+    h = oracle.hess_probs(A[s_h], y[s_h], C, x)
+    g = oracle.grad(A, y, C, x, lam)
+    scale = n / len(s_h)
+    rep = snx.cg_solve(op, g, snx.CgConfig(0.5, 10))
+    p_ref, rn_ref, it_ref, conv_ref = oracle.cg(
+        lambda u: oracle.hess_apply(A[s_h], h, C, u, scale, lam), g, 0.5, 10)
+    assert conv_ref and it_ref < 10
+    assert rep.iterations == it_ref and rep.converged
+    assert rel_err(rep.solution, p_ref) <= 1e-9
+    rep2 = snx.cg_solve(op, g, snx.CgConfig(0.5, 10))
+    assert np.array_equal(rep2.solution, rep.solution)
