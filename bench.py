@@ -448,11 +448,14 @@ def time_to_tolerance(snx, torch, rank, world, skip_cpu):
         # warm-up: one outer iteration captures this variant's CUDA graphs
         snx.newton_solve(prob, replace(ncfg, max_outer_iters=1), x0=x0.clone())
         torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        tr = snx.newton_solve(prob, ncfg, x0=x0.clone())
-        torch.cuda.synchronize()
-        dt = time.perf_counter() - t0
-        out[name] = {"time_to_tol_s": dt, "outer_iters": tr.iterations,
+        runs = []
+        for _ in range(3):  # the same deterministic solve three times: best of 3
+            t0 = time.perf_counter()
+            tr = snx.newton_solve(prob, ncfg, x0=x0.clone())
+            torch.cuda.synchronize()
+            runs.append(time.perf_counter() - t0)
+        dt = min(runs)
+        out[name] = {"time_to_tol_s": dt, "runs_s": runs, "outer_iters": tr.iterations,
                      "ms_per_outer_iter": 1e3 * dt / max(tr.iterations, 1), "reason": tr.reason,
                      "final_objective": tr.final_objective,
                      "cg_iters": [r.cg_iters for r in tr.records[1:]],

@@ -2,6 +2,7 @@
 prepare at the BASELINE shapes (CUDA events, back-to-back launches).
 
     python tools/prof_shapes.py [cifar,mnist,covertype] [reps]
+SNX_FRAC=1.0 samples the whole dataset (the full-Newton products).
 SNX_TWO_PASS=1 selects the two-GEMM kernels (snx_rowpass.cu) for an A/B."""
 import os
 import sys
@@ -60,7 +61,8 @@ def main():
         ds = snx.DeviceDataset.from_numpy(A, y, C)
         prob = snx.SoftmaxProblem(ds, 1e-3)
         x = torch.from_numpy(0.01 * np.random.default_rng(7).standard_normal((C - 1) * p)).cuda()
-        orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, 0.05), 0)
+        frac = float(os.environ.get("SNX_FRAC", "0.05"))  # Hessian sample fraction
+        orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, frac), 0)
         g = orc.gradient_device(x)
         g = g[0] if isinstance(g, tuple) else g
         op = orc.hessian_operator(x)
