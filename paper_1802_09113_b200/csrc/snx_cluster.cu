@@ -293,10 +293,10 @@ __device__ __forceinline__ double2 ld2d(const float *p) {
 // index compile-time); X slices by TMA bulk copies (one per row), or by 16-B
 // cp.async pieces in the row split's Hessian passes; side data (h rows /
 // labels) by cp.async; each lane arrives on the stage's full barrier once its
-// copies have landed.  The first S stages' X copies go out before
-// griddepcontrol.wait (X and the row indices are older than the predecessor
-// grid); everything the predecessor may write (weights, h, labels, the skip
-// flag) waits.
+// copies have landed.  Launched as a programmatic dependent (`early`), the
+// first S stages' X copies go out before griddepcontrol.wait (X and the row
+// indices are older than the predecessor grid); everything the predecessor may
+// write (weights, h, labels, the skip flag) waits.
 template <int R, int K, typename T>
 __device__ __forceinline__ void produce(const Args &a, const Ring &rg, int64_t row_lo,
                                         int64_t row_hi, int nb, int c0, int wq, int lane,
