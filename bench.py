@@ -405,6 +405,11 @@ def secondary(snx, torch, args):
     res, _, _, _ = large_shard.measure(1_000_000, 10, solve_iters=5)
     out["large_c100_shard_f32"] = res
     torch.cuda.empty_cache()
+    # the same shard in fp64 (the reference's precision): library DGEMMs + row
+    # kernels (csrc/snx_wide64.cu)
+    res, _, _, _ = large_shard.measure(1_000_000, 10, solve_iters=3, dtype="f64")
+    out["large_c100_shard_f64"] = res
+    torch.cuda.empty_cache()
     return out
 
 

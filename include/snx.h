@@ -329,6 +329,45 @@ int snx_tr_update(int32_t j, int32_t max_iters, int64_t d, const double *radius,
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
                   int64_t ldd, void *stream);
 
+/* ---- fp64 data with many classes (K = C-1 = 17..128; the fast paths above
+ * stop at K = 16).  The reference computes in fp64 for any C
+ * (softmax.py:85-212); here the feature products are library DGEMMs (cuBLAS)
+ * and the per-row softmax algebra is one warp per row (csrc/snx_wide64.cu).
+ * X is row-major [n][ldx] fp64, weights class-major fp64 as everywhere.
+ * Rows are processed in chunks of zrows; `scratch` holds
+ * snx_wide_scratch_doubles(n, p, K, zrows) doubles (n = the rows of the call). */
+int64_t snx_wide_scratch_doubles(int64_t n, int32_t p, int32_t K, int64_t zrows);
+/* snx_objective on wide-class data: out = [data loss, ||w_eff||^2], w_eff =
+ * w + alpha*dir (dir nullable); correct_out (nullable) = rows whose argmax
+ * probability is their label (softmax.py:125-141, :224-247). */
+int snx_wide_objective(const double *X, int64_t ldx, int64_t n, int32_t p, int32_t K,
+                       const int32_t *labels, const double *w, const double *dir, double alpha,
+                       double *out, long long *correct_out, double *scratch, int64_t zrows,
+                       void *stream);
+/* snx_objective_grad on wide-class data: G = scale * data_gradient + lam * w,
+ * out = [data loss, ||w||^2] (softmax.py:144-169). */
+int snx_wide_objective_grad(const double *X, int64_t ldx, int64_t n, int32_t p, int32_t K,
+                            const int32_t *labels, const double *w, double scale, double lam,
+                            double *out, double *G, double *scratch, int64_t zrows,
+                            void *stream);
+/* snx_hess_prepare on wide-class data (softmax.py:181-195): with rows != NULL
+ * the sample X[rows] is gathered into Xs_out (ld_out); H_out[r*K + c] = h_rc. */
+int snx_wide_hess_prepare(const double *X, int64_t ldx, const int64_t *rows, int64_t nrows,
+                          int32_t p, int32_t K, const double *w, double *Xs_out, int64_t ld_out,
+                          double *H_out, double *scratch, int64_t zrows, void *stream);
+/* snx_hess_apply on wide-class data (softmax.py:197-212): out = scale *
+ * X_S^T U + lam * v, U = h*V - h*rowsum(h*V), V = X_S v^T; dots / skip as in
+ * snx_hess_apply (with *skip != 0 the result and dots are left untouched). */
+int snx_wide_hess_apply(const double *Xs, int64_t lds, int64_t m, int32_t p, int32_t K,
+                        const double *H, const double *v, double scale, double lam, double *out,
+                        double *dots, const double *skip, double *scratch, int64_t zrows,
+                        void *stream);
+/* snx_class_probabilities on wide-class data (same outputs, each nullable). */
+int snx_wide_class_probabilities(const double *X, int64_t ldx, int64_t n, int32_t p, int32_t K,
+                                 const int32_t *labels, const double *w, double *probs_out,
+                                 int32_t *pred_out, double *stats_out, double *scratch,
+                                 int64_t zrows, void *stream);
+
 #ifdef __cplusplus
 }
 #endif

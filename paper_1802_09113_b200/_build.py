@@ -18,6 +18,8 @@ INCLUDE = os.path.join(ROOT, "include")
 OBJDIR = os.path.join(ROOT, "build", "obj")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# cuBLAS: the library DGEMMs of the wide-class fp64 path (csrc/snx_wide64.cu)
+LINK = ["-lcublas", "-Xlinker", "-rpath", "-Xlinker", "/usr/local/cuda/lib64"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
          "--expt-relaxed-constexpr"]
 
@@ -76,7 +78,7 @@ def build(force=False, verbose=False):
             f.result()
     os.makedirs(LIBDIR, exist_ok=True)
     tmp = LIBPATH + ".tmp"
-    _run([_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, "-o", tmp], verbose)
+    _run([_nvcc(), *ARCH, "-shared", "-Xcompiler", "-fPIC", *objs, *LINK, "-o", tmp], verbose)
     os.replace(tmp, LIBPATH)
     return LIBPATH
 
@@ -84,7 +86,7 @@ def build(force=False, verbose=False):
 def build_timeline(out, extra=("-DSNX_TIMELINE",)):
     """Debug variant with per-CTA globaltimer stamps (tools/timeline.py with
     -DSNX_TIMELINE, tools/cl_timeline.py with -DSNX_CL_TIMELINE)."""
-    cmd = [_nvcc(), *ARCH, *FLAGS, *extra, "-I", INCLUDE, *sources(), "-o", out]
+    cmd = [_nvcc(), *ARCH, *FLAGS, *extra, "-I", INCLUDE, *sources(), *LINK, "-o", out]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
         raise RuntimeError(proc.stderr)

@@ -49,6 +49,17 @@ SIGNATURES = {
                                         _c_dbl, _c_dbl, _c_i32, _c_i32, _c_p, _c_p, _c_p, _c_p,
                                         _c_p, _c_p, _c_p, _c_size, _c_p]),
     "snx_tc_ld": (_c_i64, [_c_i32]),
+    "snx_wide_scratch_doubles": (_c_i64, [_c_i64, _c_i32, _c_i32, _c_i64]),
+    "snx_wide_objective": (_c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_p,
+                                    _c_dbl, _c_p, _c_p, _c_p, _c_i64, _c_p]),
+    "snx_wide_objective_grad": (_c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                         _c_dbl, _c_dbl, _c_p, _c_p, _c_p, _c_i64, _c_p]),
+    "snx_wide_hess_prepare": (_c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                       _c_i64, _c_p, _c_p, _c_i64, _c_p]),
+    "snx_wide_hess_apply": (_c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p, _c_dbl,
+                                     _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
+    "snx_wide_class_probabilities": (_c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
+                                              _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
     "snx_hess_prepare_tc": (_c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                      _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_size, _c_p]),
     "snx_hess_apply_tc": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,

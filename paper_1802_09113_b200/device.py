@@ -62,9 +62,10 @@ class DeviceDataset:
             raise ValueError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
         if n_classes < 2:
             raise DataError(f"need at least 2 classes, got {n_classes}")
-        if n_classes - 1 > (16 if dtype == "f64" else 128):
-            raise DataError(f"C = {n_classes} classes: this build supports C <= 17 for fp64 "
-                            "data and C <= 129 for f32 data (wide tensor-core path)")
+        if n_classes - 1 > 128:
+            raise DataError(f"C = {n_classes} classes: this build supports C <= 129 "
+                            "(fp64 C > 17: library DGEMMs + row kernels; f32 C > 17: the "
+                            "wide tensor-core path)")
         self.X = X
         self.labels = labels
         self.n_classes = int(n_classes)

@@ -80,6 +80,27 @@ def _wide(view):
     return view.code == _lib.F32 and view.K > 16
 
 
+def _wide64(view):
+    """fp64 data with more than 16 free classes: library DGEMMs + row kernels
+    (csrc/snx_wide64.cu)."""
+    return view.code == _lib.F64 and view.K > 16
+
+
+_ZROWS = 32768  # rows per logits chunk of the wide fp64 passes (Z: ZROWS x K doubles)
+
+
+def _wscratch(owner, n, p, K, device):
+    """(scratch tensor, zrows) of a wide fp64 call over n rows, cached on `owner`
+    (a dataset or the shared Hessian buffers: fixed addresses for graph replays)."""
+    zr = min(max(int(n), 1), _ZROWS)
+    need = int(_lib.load().snx_wide_scratch_doubles(int(n), p, K, zr))
+    buf = getattr(owner, "_wide_scratch", None)
+    if buf is None or buf.numel() < need:
+        buf = torch.empty(need, dtype=torch.float64, device=device)
+        owner._wide_scratch = buf
+    return buf, zr
+
+
 def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
     """Device [data loss, ||w_eff||^2] (+ correct count) at w_eff = w + alpha*direction."""
     if getattr(view, "is_sparse", False):
@@ -92,6 +113,12 @@ def objective_parts(view, w, direction=None, alpha=0.0, want_correct=False):
         _lib.call("snx_objective_tc", ptr(xs[0]), ptr(xs[1]), ldb, view.n_rows,
                   view.n_features, view.K, ptr(view.labels), ptr(w), ptr(direction),
                   float(alpha), ptr(out), ptr(corr), *_ws(view), stream_handle())
+        return out, corr
+    if _wide64(view):
+        sc, zr = _wscratch(view, view.n_rows, view.n_features, view.K, w.device)
+        _lib.call("snx_wide_objective", ptr(view.X), view.ld, view.n_rows, view.n_features,
+                  view.K, ptr(view.labels), ptr(w), ptr(direction), float(alpha), ptr(out),
+                  ptr(corr), ptr(sc), zr, stream_handle())
         return out, corr
     _lib.call("snx_objective", *_args(view), ptr(view.labels), ptr(w), ptr(direction),
               float(alpha), ptr(out), ptr(corr), *_ws(view), stream_handle())
@@ -111,6 +138,12 @@ def gradient_parts(view, w, scale, lam):
                   view.n_features, view.K, ptr(view.labels), ptr(w), float(scale), float(lam),
                   ptr(out), ptr(G), *_ws(view), stream_handle())
         return G, out
+    if _wide64(view):
+        sc, zr = _wscratch(view, view.n_rows, view.n_features, view.K, w.device)
+        _lib.call("snx_wide_objective_grad", ptr(view.X), view.ld, view.n_rows,
+                  view.n_features, view.K, ptr(view.labels), ptr(w), float(scale), float(lam),
+                  ptr(out), ptr(G), ptr(sc), zr, stream_handle())
+        return G, out
     _lib.call("snx_objective_grad", *_args(view), ptr(view.labels), ptr(w), float(scale),
               float(lam), ptr(out), ptr(G), *_ws(view), stream_handle())
     return G, out
@@ -123,7 +156,7 @@ def gradient_and_correct(view, w, scale, lam):
     if getattr(view, "is_sparse", False):
         return None
     view = view.materialized()
-    if _wide(view):
+    if _wide(view) or _wide64(view):
         return None
     out = torch.empty(2, dtype=torch.float64, device=w.device)
     corr = torch.empty(1, dtype=torch.int64, device=w.device)
@@ -202,6 +235,11 @@ class HessianOperator:
             _lib.call("snx_hess_prepare", base.code, ptr(base.X), base.ld, ptr(rows),
                       view.n_rows, view.n_features, view.K, ptr(self._w), None, base.ld,
                       ptr(hb.h), *_ws(view), stream_handle())
+        elif _wide64(base):  # fp64, K > 16: library DGEMMs + row kernels
+            sc, zr = _wscratch(hb, view.n_rows, self.p, view.K, base.X.device)
+            _lib.call("snx_wide_hess_prepare", ptr(base.X), base.ld, ptr(view.rows), view.n_rows,
+                      self.p, view.K, ptr(self._w), ptr(hb.xs), base.ld, ptr(hb.h), ptr(sc), zr,
+                      stream_handle())
         elif hb.xs_tc is not None:  # f32: tensor-core product (csrc/snx_tc.cu)
             _lib.call("snx_hess_prepare_tc", ptr(base.X), base.ld, ptr(view.rows), view.n_rows,
                       view.n_features, view.K, ptr(self._w), ptr(hb.xs), base.ld, ptr(hb.h),
@@ -230,6 +268,11 @@ class HessianOperator:
             _lib.call("snx_hess_apply_rows", base.code, ptr(base.X), base.ld, ptr(rows),
                       self.view.n_rows, self.p, self.view.K, ptr(hb.h), ptr(v), self.scale,
                       self.lam, ptr(out), ptr(dots), skip, *_ws(self.view), stream_handle())
+        elif _wide64(base):
+            sc, zr = _wscratch(hb, self.view.n_rows, self.p, self.view.K, v.device)
+            _lib.call("snx_wide_hess_apply", ptr(hb.xs), base.ld, self.view.n_rows, self.p,
+                      self.view.K, ptr(hb.h), ptr(v), self.scale, self.lam, ptr(out), ptr(dots),
+                      skip, ptr(sc), zr, stream_handle())
         elif hb.xs_tc is not None:
             _lib.call("snx_hess_apply_tc", ptr(hb.xs_tc[0]), ptr(hb.xs_tc[1]), hb.ldb,
                       self.view.n_rows, self.p, self.view.K, ptr(hb.h), ptr(v), self.scale,
@@ -304,6 +347,11 @@ def _probs_pass(ds, x, probs=False, pred=False, stats=False):
         elif _wide(view):
             raise DataError(f"class probabilities are built for C <= 17 on f32 data "
                             f"(C = {C}); use the fp64 dataset")
+        elif _wide64(view):
+            sc, zr = _wscratch(view, n, view.n_features, view.K, dev)
+            _lib.call("snx_wide_class_probabilities", ptr(view.X), view.ld, n, view.n_features,
+                      view.K, ptr(view.labels), ptr(w), ptr(P), ptr(Y), ptr(S), ptr(sc), zr,
+                      stream_handle())
         else:
             _lib.call("snx_class_probabilities", *_args(view), ptr(view.labels), ptr(w), ptr(P),
                       ptr(Y), ptr(S), *_ws(view), stream_handle())

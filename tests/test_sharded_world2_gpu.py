@@ -26,6 +26,8 @@ CASES = {
     # name: (n, p, C, variant, f_g, f_h, iters, seed)
     "subsampled20": (3000, 40, 7, "subsampled-20", None, None, 4, 5),
     "tiny_hessian_sample": (600, 24, 4, "subsampled-100", 1.0, 0.004, 4, 3),
+    # fp64 with many classes (library DGEMMs + row kernels on each shard)
+    "wide_classes_c40": (1600, 48, 40, "subsampled-20", None, None, 3, 9),
 }
 
 
