@@ -367,6 +367,15 @@ int snx_wide_class_probabilities(const double *X, int64_t ldx, int64_t n, int32_
                                  const int32_t *labels, const double *w, double *probs_out,
                                  int32_t *pred_out, double *stats_out, double *scratch,
                                  int64_t zrows, void *stream);
+/* snx_class_probabilities on f32 data with C = 18..129: each chunk of zrows
+ * rows is widened to fp64 (exact) and goes through the fp64 path above, so the
+ * results are the fp64 arithmetic on the f32-rounded data; scratch holds
+ * snx_wide_f32_scratch_doubles(n, p, K, zrows) doubles. */
+int64_t snx_wide_f32_scratch_doubles(int64_t n, int32_t p, int32_t K, int64_t zrows);
+int snx_wide_class_probabilities_f32(const float *X, int64_t ldx, int64_t n, int32_t p,
+                                     int32_t K, const int32_t *labels, const double *w,
+                                     double *probs_out, int32_t *pred_out, double *stats_out,
+                                     double *scratch, int64_t zrows, void *stream);
 
 #ifdef __cplusplus
 }

@@ -60,6 +60,9 @@ SIGNATURES = {
                                      _c_dbl, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
     "snx_wide_class_probabilities": (_c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                               _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
+    "snx_wide_f32_scratch_doubles": (_c_i64, [_c_i64, _c_i32, _c_i32, _c_i64]),
+    "snx_wide_class_probabilities_f32": (_c_int, [_c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p,
+                                                  _c_p, _c_p, _c_p, _c_p, _c_p, _c_i64, _c_p]),
     "snx_hess_prepare_tc": (_c_int, [_c_p, _c_i64, _c_p, _c_i64, _c_i32, _c_i32, _c_p, _c_p,
                                      _c_i64, _c_p, _c_p, _c_p, _c_i64, _c_p, _c_size, _c_p]),
     "snx_hess_apply_tc": (_c_int, [_c_p, _c_p, _c_i64, _c_i64, _c_i32, _c_i32, _c_p, _c_p,

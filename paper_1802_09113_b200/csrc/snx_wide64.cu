@@ -206,6 +206,17 @@ __global__ void __launch_bounds__(32 * kRowWarps) row_kernel(const RowArgs a) {
   }
 }
 
+// f32 rows widened to fp64 (exact), row-major [mc][ldo]
+__global__ void widen_kernel(const float *X, int64_t ldx, int64_t mc, int32_t p, double *out,
+                             int64_t ldo) {
+  const int64_t total = mc * (int64_t)p;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / p, j = e - r * p;
+    out[r * ldo + j] = (double)X[r * ldx + j];
+  }
+}
+
 // w_eff = w + alpha * dir (numpy rounding, newton.py:92)
 __global__ void weff_kernel(const double *w, const double *dir, double alpha, int64_t d,
                             double *out) {
@@ -500,6 +511,42 @@ int snx_wide_class_probabilities(const double *X, int64_t ldx, int64_t n, int32_
     a.m = mc;
     a.K = K;
     a.Z = sc.Z;
+    a.y = labels != nullptr ? labels + r0 : nullptr;
+    a.P = probs_out != nullptr ? probs_out + r0 * (K + 1) : nullptr;
+    a.Y = pred_out != nullptr ? pred_out + r0 : nullptr;
+    a.S = stats_out != nullptr ? stats_out + r0 * 3 : nullptr;
+    if (rows_launch(a, st)) return 1;
+  }
+  return 0;
+}
+
+int64_t snx_wide_f32_scratch_doubles(int64_t n, int32_t p, int32_t K, int64_t zrows) {
+  (void)n;
+  return zrows * K + zrows * (int64_t)p + 2;
+}
+
+int snx_wide_class_probabilities_f32(const float *X, int64_t ldx, int64_t n, int32_t p,
+                                     int32_t K, const int32_t *labels, const double *w,
+                                     double *probs_out, int32_t *pred_out, double *stats_out,
+                                     double *scratch, int64_t zrows, void *stream) {
+  if (check_args("snx_wide_class_probabilities_f32", X, ldx, n, p, K, scratch, zrows))
+    return 1;
+  if (w == nullptr || (n > 0 && stats_out != nullptr && labels == nullptr)) {
+    set_error("snx_wide_class_probabilities_f32: NULL w (or labels with stats_out)");
+    return 1;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  double *Z = scratch, *Xd = scratch + zrows * K;
+  for (int64_t r0 = 0; r0 < n; r0 += zrows) {
+    const int64_t mc = n - r0 < zrows ? n - r0 : zrows;
+    widen_kernel<<<296, 256, 0, st>>>(X + r0 * ldx, ldx, mc, p, Xd, p);
+    if (check_launch("wide widen")) return 1;
+    if (logits(Xd, p, mc, p, K, w, Z, st)) return 1;
+    RowArgs a{};
+    a.mode = kProbs;
+    a.m = mc;
+    a.K = K;
+    a.Z = Z;
     a.y = labels != nullptr ? labels + r0 : nullptr;
     a.P = probs_out != nullptr ? probs_out + r0 * (K + 1) : nullptr;
     a.Y = pred_out != nullptr ? pred_out + r0 : nullptr;

@@ -344,9 +344,15 @@ def _probs_pass(ds, x, probs=False, pred=False, stats=False):
             _lib.call("snx_csr_class_probabilities", ptr(view.indptr), ptr(view.indices),
                       ptr(view.data), n, view.n_features, view.K, ptr(view.labels), ptr(w),
                       ptr(P), ptr(Y), ptr(S), ptr(ws), ws.numel(), stream_handle())
-        elif _wide(view):
-            raise DataError(f"class probabilities are built for C <= 17 on f32 data "
-                            f"(C = {C}); use the fp64 dataset")
+        elif _wide(view):  # f32, K > 16: row chunks widened to fp64, the fp64 path
+            zr = min(max(n, 1), 4096)
+            need = int(_lib.load().snx_wide_f32_scratch_doubles(n, view.n_features, view.K, zr))
+            sc = getattr(view, "_wide_scratch", None)
+            if sc is None or sc.numel() < need:
+                sc = view._wide_scratch = torch.empty(need, dtype=torch.float64, device=dev)
+            _lib.call("snx_wide_class_probabilities_f32", ptr(view.X), view.ld, n,
+                      view.n_features, view.K, ptr(view.labels), ptr(w), ptr(P), ptr(Y), ptr(S),
+                      ptr(sc), zr, stream_handle())
         elif _wide64(view):
             sc, zr = _wscratch(view, n, view.n_features, view.K, dev)
             _lib.call("snx_wide_class_probabilities", ptr(view.X), view.ld, n, view.n_features,

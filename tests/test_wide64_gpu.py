@@ -98,3 +98,21 @@ def test_newton_trajectory_wide_classes():
         assert r.step_size == alpha and r.cg_iters == it, k
         assert r.train_acc == acc, k
     assert rel_err(tr.x_final, ref["x"]) <= 1e-9
+
+
+def test_f32_wide_probabilities():
+    """f32 data with C = 60: class_probabilities / predict / row_stats widen each
+    row chunk to fp64 (the fp64 path on the f32-rounded data): 1e-12 against the
+    oracle on the rounded data, predictions exact."""
+    n, p, C = 700, 45, 60
+    A, y = oracle.synthetic_problem(n, p, C, seed=4)
+    A32 = A.astype(np.float32).astype(np.float64)
+    x = 0.3 * np.random.default_rng(5).standard_normal((C - 1) * p)
+    ds = snx.DeviceDataset.from_numpy(A, y, C, dtype="f32")
+    P = snx.class_probabilities(ds, x)
+    assert rel_err(P, oracle.class_probs(A32, y, C, x)) <= 1e-12
+    assert np.array_equal(snx.predict(ds, x), oracle.predict(A32, y, C, x))
+    M, E, alpha, lin = oracle.row_terms(A32, y, oracle.weights_matrix(x, p, C), C)
+    rs = snx.row_stats(ds, x)
+    assert rel_err(rs.sum_exp_part, E.sum(axis=1)) <= 1e-12
+    assert rel_err(rs.linear_part, lin) <= 1e-12
