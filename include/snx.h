@@ -329,8 +329,9 @@ int snx_tr_update(int32_t j, int32_t max_iters, int64_t d, const double *radius,
 int snx_pack_rows(int dtype, const double *src, int64_t nrows, int32_t p, void *dst,
                   int64_t ldd, void *stream);
 
-/* ---- fp64 data with many classes (K = C-1 = 17..128; the fast paths above
- * stop at K = 16).  The reference computes in fp64 for any C
+/* ---- fp64 data with many classes (K = C-1 >= 17, any C: up to 4 classes
+ * per lane in registers to K = 128, a loop variant beyond; the fast paths
+ * above stop at K = 16).  The reference computes in fp64 for any C
  * (softmax.py:85-212); here the feature products are library DGEMMs (cuBLAS)
  * and the per-row softmax algebra is one warp per row (csrc/snx_wide64.cu).
  * X is row-major [n][ldx] fp64, weights class-major fp64 as everywhere.

@@ -1,4 +1,4 @@
-// fp64 data with many classes (K = C-1 = 17..128; the reference is fp64 for
+// fp64 data with many classes (K = C-1 >= 17; the reference is fp64 for
 // any C, softmax.py:85-212): the feature products are library DGEMMs
 // (cuBLAS, column-major views of the row-major arrays) and the per-row softmax
 // algebra is one warp per row here.  Rows are processed in chunks of `zrows`
@@ -23,6 +23,7 @@ namespace wide {
 
 constexpr int kKMax = 128;        // K <= 128 (C <= 129), 4 classes per lane
 constexpr int kCPL = kKMax / 32;  // classes per lane
+constexpr int kKAny = 1 << 16;    // K > 128: row_kernel_any (logits re-read from L1 / L2)
 constexpr int kRowWarps = 8;      // rows per 256-thread block
 constexpr int kRedThreads = 1024;
 
@@ -206,6 +207,113 @@ __global__ void __launch_bounds__(32 * kRowWarps) row_kernel(const RowArgs a) {
   }
 }
 
+// The same row algebra for K > 128 (any C): each lane walks its classes
+// c = lane, lane + 32, ... through the chunk's logits in global memory (L1 /
+// L2-resident), recomputing E where needed -- same values and the same
+// summation order as row_kernel.
+__global__ void __launch_bounds__(32 * kRowWarps) row_kernel_any(const RowArgs a) {
+  if (a.skip != nullptr && *a.skip != 0.0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * kRowWarps + (threadIdx.x >> 5);
+  if (r >= a.m) return;
+  const int K = a.K;
+  double *zr = a.Z + r * K;
+  if (a.mode == kApply) {
+    const double *hr = a.h + r * K;
+    double s = 0.0;
+    for (int c = lane; c < K; c += 32) s += zr[c] * hr[c];
+    s = warp_allsum(s);
+    __syncwarp();
+    for (int c = lane; c < K; c += 32) {
+      const double vw = zr[c] * hr[c];
+      zr[c] = vw - hr[c] * s;
+    }
+    return;
+  }
+  double M = 0.0;
+  for (int c = lane; c < K; c += 32) {
+    const double z = zr[c];
+    if (z > M || isnan(z)) M = z;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double q = __shfl_xor_sync(0xffffffffu, M, o);
+    if (isnan(q) || q > M) M = q;
+  }
+  double se = 0.0;
+  for (int c = lane; c < K; c += 32) se += exp(zr[c] - M);
+  se = warp_allsum(se);
+  const double eM = exp(-M), alpha = eM + se;
+  if (a.mode == kPrep) {
+    double *ho = a.hout + r * K;
+    for (int c = lane; c < K; c += 32) ho[c] = exp(zr[c] - M) / alpha;
+    return;
+  }
+  const int y = a.y != nullptr ? a.y[r] : -1;
+  double lin = 0.0;
+  if (y >= 0 && y < K && (y & 31) == lane) lin = zr[y];
+  lin = warp_allsum(lin);
+  double bv = (double)NAN;
+  int bi = 1 << 30;
+  bool have = false;
+  for (int c = lane; c < K; c += 32) {
+    const double pc = exp(zr[c] - M) / alpha;
+    if (!have) {
+      bv = pc;
+      bi = c;
+      have = true;
+    } else {
+      amax_merge(bv, bi, pc, c);
+    }
+  }
+  if (lane == 0) {
+    if (!have) {
+      bv = eM / alpha;
+      bi = K;
+      have = true;
+    } else {
+      amax_merge(bv, bi, eM / alpha, K);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, bv, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, bi, o);
+    const bool h2 = __shfl_xor_sync(0xffffffffu, (int)have, o) != 0;
+    if (h2) {
+      if (!have) {
+        bv = v2;
+        bi = i2;
+        have = true;
+      } else {
+        amax_merge(bv, bi, v2, i2);
+      }
+    }
+  }
+  if (a.mode == kProbs) {
+    if (a.P != nullptr) {
+      double *pr = a.P + r * (K + 1);
+      for (int c = lane; c < K; c += 32) pr[c] = exp(zr[c] - M) / alpha;
+      if (lane == 0) pr[K] = eM / alpha;
+    }
+    if (lane == 0) {
+      if (a.Y != nullptr) a.Y[r] = bi;
+      if (a.S != nullptr) {
+        a.S[r * 3 + 0] = M;
+        a.S[r * 3 + 1] = se;
+        a.S[r * 3 + 2] = lin;
+      }
+    }
+    return;
+  }
+  if (lane == 0) {
+    a.rl[a.row0 + r] = (M + log(alpha)) - lin;
+    if (a.rc != nullptr) a.rc[a.row0 + r] = bi == y ? 1 : 0;
+  }
+  if (a.mode == kGrad)
+    for (int c = lane; c < K; c += 32) zr[c] = exp(zr[c] - M) / alpha - (c == y ? 1.0 : 0.0);
+}
+
 // f32 rows widened to fp64 (exact), row-major [mc][ldo]
 __global__ void widen_kernel(const float *X, int64_t ldx, int64_t mc, int32_t p, double *out,
                              int64_t ldo) {
@@ -280,8 +388,8 @@ __global__ void __launch_bounds__(kDotThreads)
 
 static int check_args(const char *who, const void *X, int64_t ldx, int64_t n, int32_t p,
                       int32_t K, const double *scratch, int64_t zrows) {
-  if (K < 1 || K > kKMax) {
-    set_error("%s: K = C-1 = %d outside [1, %d]", who, K, kKMax);
+  if (K < 1 || K > kKAny) {
+    set_error("%s: K = C-1 = %d outside [1, %d]", who, K, kKAny);
     return 1;
   }
   if (p < 1 || ldx < p || n < 0 || (n > 0 && X == nullptr)) {
@@ -332,7 +440,11 @@ static int xtz(const double *X, int64_t ldx, int64_t mc, int32_t p, int32_t K, c
 
 static int rows_launch(const RowArgs &a, cudaStream_t st) {
   if (a.m <= 0) return 0;
-  row_kernel<<<(unsigned)((a.m + kRowWarps - 1) / kRowWarps), 32 * kRowWarps, 0, st>>>(a);
+  const unsigned blocks = (unsigned)((a.m + kRowWarps - 1) / kRowWarps);
+  if (a.K <= kKMax)
+    row_kernel<<<blocks, 32 * kRowWarps, 0, st>>>(a);
+  else
+    row_kernel_any<<<blocks, 32 * kRowWarps, 0, st>>>(a);
   return check_launch("wide row pass");
 }
 

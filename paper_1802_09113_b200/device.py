@@ -62,10 +62,9 @@ class DeviceDataset:
             raise ValueError(f"dtype must be one of {sorted(DTYPES)}, got {dtype!r}")
         if n_classes < 2:
             raise DataError(f"need at least 2 classes, got {n_classes}")
-        if n_classes - 1 > 128:
-            raise DataError(f"C = {n_classes} classes: this build supports C <= 129 "
-                            "(fp64 C > 17: library DGEMMs + row kernels; f32 C > 17: the "
-                            "wide tensor-core path)")
+        if dtype != "f64" and n_classes - 1 > 128:
+            raise DataError(f"C = {n_classes} classes: f32 data supports C <= 129 (the wide "
+                            "tensor-core path); fp64 data takes any C")
         self.X = X
         self.labels = labels
         self.n_classes = int(n_classes)

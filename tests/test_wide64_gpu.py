@@ -1,6 +1,6 @@
-"""fp64 data with many classes (C = 18..129, csrc/snx_wide64.cu: library DGEMMs
-+ one warp per row) against the CPU oracle -- the reference computes in fp64
-for any C (softmax.py:85-247), so these are fp64 bars: objective / gradient /
+"""fp64 data with many classes (C = 18..129, and C = 300 on the loop variant;
+csrc/snx_wide64.cu: library DGEMMs + one warp per row) against the CPU oracle
+-- the reference computes in fp64 for any C (softmax.py:85-247), so these are fp64 bars: objective / gradient /
 h / Hv / probabilities 1e-10 relative, predictions and accuracy exact, CG
 iteration counts exact, Newton trajectories as in test_scale_parity_gpu.
 Chunking of the logits (zrows < n) is exercised by shrinking the chunk."""
@@ -16,7 +16,7 @@ from conftest import rel_err
 
 pytestmark = pytest.mark.gpu
 
-SHAPES = [(600, 50, 20), (500, 37, 41), (300, 64, 129)]
+SHAPES = [(600, 50, 20), (500, 37, 41), (300, 64, 129), (200, 40, 300)]
 
 
 @pytest.fixture(scope="module", autouse=True)
