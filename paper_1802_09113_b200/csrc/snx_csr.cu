@@ -553,6 +553,11 @@ using namespace snx;
 extern "C" {
 
 size_t snx_csr_workspace_bytes(int64_t nrows, int32_t p, int32_t K) {
+  if (K > 32) {  // the wide-class passes (and the row gather's K = 1 layout)
+    const size_t a = csr_ws_layout(nrows, p, 1, nullptr, nullptr);
+    const size_t b = snx::wide::csr_wide_ws_bytes(nrows, p, K);
+    return a > b ? a : b;
+  }
   return csr_ws_layout(nrows, p, K, nullptr, nullptr);
 }
 
@@ -582,6 +587,9 @@ int snx_csr_objective(const int64_t *indptr, const int32_t *indices, const doubl
                       int64_t nrows, int32_t p, int32_t K, const int32_t *labels, const double *w,
                       const double *dir, double alpha, double *out, int64_t *correct_out,
                       void *ws, size_t ws_bytes, void *stream) {
+  if (K > 32)
+    return wide::csr_wide_objective(indptr, indices, data, nrows, p, K, labels, w, dir, alpha,
+                                    out, correct_out, ws, ws_bytes, (cudaStream_t)stream);
   if (check_ws("snx_csr_objective", nrows, p, K, ws_bytes)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   CsrWs W;
@@ -607,6 +615,9 @@ int snx_csr_class_probabilities(const int64_t *indptr, const int32_t *indices,
                                 const int32_t *labels, const double *w, double *probs_out,
                                 int32_t *pred_out, double *stats_out, void *ws, size_t ws_bytes,
                                 void *stream) {
+  if (K > 32)
+    return wide::csr_wide_probs(indptr, indices, data, nrows, p, K, labels, w, probs_out,
+                                pred_out, stats_out, ws, ws_bytes, (cudaStream_t)stream);
   if (check_ws("snx_csr_class_probabilities", nrows, p, K, ws_bytes)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   CsrWs W;
@@ -628,6 +639,10 @@ int snx_csr_objective_grad(const int64_t *indptr, const int32_t *indices, const 
                            int64_t nrows, int32_t p, int32_t K, const int32_t *labels,
                            const double *w, double scale, double lam, double *out, double *G_out,
                            void *ws, size_t ws_bytes, void *stream) {
+  if (K > 32)
+    return wide::csr_wide_objective_grad(indptr, indices, data, colptr, rowidx, cdata, nrows, p,
+                                         K, labels, w, scale, lam, out, G_out, ws, ws_bytes,
+                                         (cudaStream_t)stream);
   if (check_ws("snx_csr_objective_grad", nrows, p, K, ws_bytes)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   CsrWs W;
@@ -676,6 +691,9 @@ int snx_csr_gather(const int64_t *indptr, const int32_t *indices, const double *
 int snx_csr_hess_prepare(const int64_t *indptr, const int32_t *indices, const double *data,
                          int64_t nrows, int32_t p, int32_t K, const double *w, double *H_out,
                          void *ws, size_t ws_bytes, void *stream) {
+  if (K > 32)
+    return wide::csr_wide_hess_prepare(indptr, indices, data, nrows, p, K, w, H_out, ws, ws_bytes,
+                                       (cudaStream_t)stream);
   if (check_ws("snx_csr_hess_prepare", nrows, p, K, ws_bytes)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   CsrWs W;
@@ -697,6 +715,10 @@ int snx_csr_hess_apply(const int64_t *indptr, const int32_t *indices, const doub
                        int64_t nrows, int32_t p, int32_t K, const double *H, const double *v,
                        double scale, double lam, double *Hv_out, double *dots, const double *skip,
                        void *ws, size_t ws_bytes, void *stream) {
+  if (K > 32)
+    return wide::csr_wide_hess_apply(indptr, indices, data, colptr, rowidx, cdata, nrows, p, K, H,
+                                     v, scale, lam, Hv_out, dots, skip, ws, ws_bytes,
+                                     (cudaStream_t)stream);
   if (check_ws("snx_csr_hess_apply", nrows, p, K, ws_bytes)) return 1;
   cudaStream_t st = (cudaStream_t)stream;
   CsrWs W;

@@ -150,3 +150,31 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 bool gemm2_pdl();
 
 }  // namespace snx
+// fp64 wide-class passes on CSR data (K > 32), csrc/snx_wide64.cu
+namespace snx {
+namespace wide {
+size_t csr_wide_ws_bytes(int64_t n, int32_t p, int32_t K);
+int csr_wide_objective(const int64_t *indptr, const int32_t *indices, const double *data,
+                       int64_t n, int32_t p, int32_t K, const int32_t *labels, const double *w,
+                       const double *dir, double alpha, double *out, int64_t *correct_out,
+                       void *ws, size_t ws_bytes, cudaStream_t st);
+int csr_wide_objective_grad(const int64_t *indptr, const int32_t *indices, const double *data,
+                            const int64_t *colptr, const int32_t *rowidx, const double *cdata,
+                            int64_t n, int32_t p, int32_t K, const int32_t *labels,
+                            const double *w, double scale, double lam, double *out, double *G,
+                            void *ws, size_t ws_bytes, cudaStream_t st);
+int csr_wide_probs(const int64_t *indptr, const int32_t *indices, const double *data, int64_t n,
+                   int32_t p, int32_t K, const int32_t *labels, const double *w, double *P,
+                   int32_t *Y, double *S, void *ws, size_t ws_bytes, cudaStream_t st);
+int csr_wide_hess_prepare(const int64_t *indptr, const int32_t *indices, const double *data,
+                          int64_t n, int32_t p, int32_t K, const double *w, double *H,
+                          void *ws, size_t ws_bytes, cudaStream_t st);
+int csr_wide_hess_apply(const int64_t *indptr, const int32_t *indices, const double *data,
+                        const int64_t *colptr, const int32_t *rowidx, const double *cdata,
+                        int64_t n, int32_t p, int32_t K, const double *H, const double *v,
+                        double scale, double lam, double *out, double *dots, const double *skip,
+                        void *ws, size_t ws_bytes, cudaStream_t st);
+}  // namespace wide
+}  // namespace snx
+
+

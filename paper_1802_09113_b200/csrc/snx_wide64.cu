@@ -463,6 +463,205 @@ static Scratch carve(double *s, int64_t zrows, int32_t K, int64_t n) {
   return c;
 }
 
+// ---------------------------------------------------------------- CSR data
+// Sparse rows with many classes (K > 32; the CSR kernels of snx_csr.cu keep a
+// row's logits in registers): logits by a warp per row over the row's entries
+// in stored order (lanes over classes, weights transposed to [p][K] so the
+// loads coalesce), X^T R by a warp per CSC column -- both fixed-order -- and
+// the row algebra of row_kernel.  One chunk (Z: nrows x K doubles).
+
+// wt[j*K + c] = (w + alpha*dir)[c*p + j]; block partials not needed here
+__global__ void transpose_w_kernel(const double *w, const double *dir, double alpha, int32_t p,
+                                   int32_t K, double *wt) {
+  const int64_t d = (int64_t)K * p;
+  for (int64_t f = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; f < d;
+       f += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = f / p, j = f - c * p;
+    wt[j * K + c] = dir != nullptr ? __dadd_rn(w[f], __dmul_rn(alpha, dir[f])) : w[f];
+  }
+}
+
+__global__ void __launch_bounds__(256)
+    csr_logits_kernel(const int64_t *indptr, const int32_t *indices, const double *data,
+                      int64_t nrows, const double *wt, int32_t K, double *Z,
+                      const double *skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= nrows) return;
+  const int64_t e0 = indptr[r], e1 = indptr[r + 1];
+  for (int c0 = 0; c0 < K; c0 += 32) {
+    const int c = c0 + lane;
+    double acc = 0.0;
+    if (c < K)
+      for (int64_t t = e0; t < e1; ++t) acc = fma(data[t], __ldg(wt + (int64_t)indices[t] * K + c), acc);
+    if (c < K) Z[r * K + c] = acc;
+  }
+}
+
+// acc[c*p + j] = sum over column j's entries (stored order) of cdata * R[row][c]
+__global__ void __launch_bounds__(256)
+    csc_xtr_kernel(const int64_t *colptr, const int32_t *rowidx, const double *cdata, int32_t p,
+                   const double *R, int32_t K, double *acc, const double *skip) {
+  if (skip != nullptr && *skip != 0.0) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t j = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (j >= p) return;
+  const int64_t e0 = colptr[j], e1 = colptr[j + 1];
+  for (int c0 = 0; c0 < K; c0 += 32) {
+    const int c = c0 + lane;
+    double s = 0.0;
+    if (c < K)
+      for (int64_t t = e0; t < e1; ++t) s = fma(cdata[t], R[(int64_t)rowidx[t] * K + c], s);
+    if (c < K) acc[(int64_t)c * p + j] = s;
+  }
+}
+
+// workspace (bytes) of the sparse wide passes: wt [d] | Z [n*K] | rl [n] |
+// rc [n ints] | acc [d] | 2
+size_t csr_wide_ws_bytes(int64_t n, int32_t p, int32_t K) {
+  const int64_t d = (int64_t)K * p;
+  return (size_t)(d + (int64_t)n * K + n + (n + 1) / 2 + d + 2) * sizeof(double);
+}
+
+struct CsrWs {
+  double *wt, *Z, *rl, *acc;
+  int32_t *rc;
+};
+static int csr_carve(const char *who, void *ws, size_t ws_bytes, int64_t n, int32_t p, int32_t K,
+                     CsrWs &c) {
+  if (ws == nullptr || ws_bytes < csr_wide_ws_bytes(n, p, K)) {
+    set_error("%s: workspace of %zu bytes < %zu", who, ws_bytes, csr_wide_ws_bytes(n, p, K));
+    return 1;
+  }
+  const int64_t d = (int64_t)K * p;
+  double *s = static_cast<double *>(ws);
+  c.wt = s;
+  c.Z = s + d;
+  c.rl = c.Z + n * K;
+  c.rc = reinterpret_cast<int32_t *>(c.rl + n);
+  c.acc = c.rl + n + (n + 1) / 2;
+  return 0;
+}
+
+static int csr_logits(const int64_t *indptr, const int32_t *indices, const double *data,
+                      int64_t n, int32_t p, int32_t K, const double *w, const double *dir,
+                      double alpha, const CsrWs &c, const double *skip, cudaStream_t st) {
+  transpose_w_kernel<<<296, 256, 0, st>>>(w, dir, alpha, p, K, c.wt);
+  if (check_launch("csr wide transpose")) return 1;
+  if (n > 0) {
+    csr_logits_kernel<<<(unsigned)((n + 7) / 8), 256, 0, st>>>(indptr, indices, data, n, c.wt, K,
+                                                            c.Z, skip);
+    if (check_launch("csr wide logits")) return 1;
+  }
+  return 0;
+}
+
+int csr_wide_objective(const int64_t *indptr, const int32_t *indices, const double *data,
+                       int64_t n, int32_t p, int32_t K, const int32_t *labels, const double *w,
+                       const double *dir, double alpha, double *out, int64_t *correct_out,
+                       void *ws, size_t ws_bytes, cudaStream_t st) {
+  CsrWs c;
+  if (csr_carve("snx_csr_objective", ws, ws_bytes, n, p, K, c)) return 1;
+  if (csr_logits(indptr, indices, data, n, p, K, w, dir, alpha, c, nullptr, st)) return 1;
+  RowArgs a{};
+  a.mode = kObj;
+  a.m = n;
+  a.K = K;
+  a.Z = c.Z;
+  a.y = labels;
+  a.rl = c.rl;
+  a.rc = correct_out != nullptr ? c.rc : nullptr;
+  if (rows_launch(a, st)) return 1;
+  // ||w_eff||^2 from the transposed copy (same values, a different order)
+  reduce_kernel<<<1, kRedThreads, 0, st>>>(c.rl, a.rc, n, c.wt, (int64_t)K * p, out,
+                                           reinterpret_cast<long long *>(correct_out));
+  return check_launch("csr wide reduce");
+}
+
+int csr_wide_objective_grad(const int64_t *indptr, const int32_t *indices, const double *data,
+                            const int64_t *colptr, const int32_t *rowidx, const double *cdata,
+                            int64_t n, int32_t p, int32_t K, const int32_t *labels,
+                            const double *w, double scale, double lam, double *out, double *G,
+                            void *ws, size_t ws_bytes, cudaStream_t st) {
+  CsrWs c;
+  if (csr_carve("snx_csr_objective_grad", ws, ws_bytes, n, p, K, c)) return 1;
+  if (csr_logits(indptr, indices, data, n, p, K, w, nullptr, 0.0, c, nullptr, st)) return 1;
+  RowArgs a{};
+  a.mode = kGrad;
+  a.m = n;
+  a.K = K;
+  a.Z = c.Z;
+  a.y = labels;
+  a.rl = c.rl;
+  if (rows_launch(a, st)) return 1;
+  csc_xtr_kernel<<<(unsigned)((p + 7) / 8), 256, 0, st>>>(colptr, rowidx, cdata, p, c.Z, K, c.acc,
+                                                        nullptr);
+  if (check_launch("csr wide X^T R")) return 1;
+  reduce_kernel<<<1, kRedThreads, 0, st>>>(c.rl, nullptr, n, w, (int64_t)K * p, out, nullptr);
+  if (check_launch("csr wide reduce")) return 1;
+  finish_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(c.acc, scale, lam, w, (int64_t)K * p, G,
+                                                   nullptr, nullptr);
+  return check_launch("csr wide gradient finish");
+}
+
+int csr_wide_probs(const int64_t *indptr, const int32_t *indices, const double *data, int64_t n,
+                   int32_t p, int32_t K, const int32_t *labels, const double *w, double *P,
+                   int32_t *Y, double *S, void *ws, size_t ws_bytes, cudaStream_t st) {
+  CsrWs c;
+  if (csr_carve("snx_csr_class_probabilities", ws, ws_bytes, n, p, K, c)) return 1;
+  if (csr_logits(indptr, indices, data, n, p, K, w, nullptr, 0.0, c, nullptr, st)) return 1;
+  RowArgs a{};
+  a.mode = kProbs;
+  a.m = n;
+  a.K = K;
+  a.Z = c.Z;
+  a.y = labels;
+  a.P = P;
+  a.Y = Y;
+  a.S = S;
+  return rows_launch(a, st);
+}
+
+int csr_wide_hess_prepare(const int64_t *indptr, const int32_t *indices, const double *data,
+                          int64_t n, int32_t p, int32_t K, const double *w, double *H,
+                          void *ws, size_t ws_bytes, cudaStream_t st) {
+  CsrWs c;
+  if (csr_carve("snx_csr_hess_prepare", ws, ws_bytes, n, p, K, c)) return 1;
+  if (csr_logits(indptr, indices, data, n, p, K, w, nullptr, 0.0, c, nullptr, st)) return 1;
+  RowArgs a{};
+  a.mode = kPrep;
+  a.m = n;
+  a.K = K;
+  a.Z = c.Z;
+  a.hout = H;
+  return rows_launch(a, st);
+}
+
+int csr_wide_hess_apply(const int64_t *indptr, const int32_t *indices, const double *data,
+                        const int64_t *colptr, const int32_t *rowidx, const double *cdata,
+                        int64_t n, int32_t p, int32_t K, const double *H, const double *v,
+                        double scale, double lam, double *out, double *dots, const double *skip,
+                        void *ws, size_t ws_bytes, cudaStream_t st) {
+  CsrWs c;
+  if (csr_carve("snx_csr_hess_apply", ws, ws_bytes, n, p, K, c)) return 1;
+  if (csr_logits(indptr, indices, data, n, p, K, v, nullptr, 0.0, c, skip, st)) return 1;
+  RowArgs a{};
+  a.mode = kApply;
+  a.m = n;
+  a.K = K;
+  a.Z = c.Z;
+  a.h = H;
+  a.skip = skip;
+  if (rows_launch(a, st)) return 1;
+  csc_xtr_kernel<<<(unsigned)((p + 7) / 8), 256, 0, st>>>(colptr, rowidx, cdata, p, c.Z, K, c.acc,
+                                                        skip);
+  if (check_launch("csr wide X^T U")) return 1;
+  finish_kernel<<<kDotBlocks, kDotThreads, 0, st>>>(c.acc, scale, lam, v, (int64_t)K * p, out,
+                                                   dots, skip);
+  return check_launch("csr wide product finish");
+}
+
 }  // namespace wide
 }  // namespace snx
 

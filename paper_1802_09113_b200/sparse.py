@@ -31,8 +31,8 @@ class CsrDataset:
                  host_indptr):
         if n_classes < 2:
             raise DataError(f"need at least 2 classes, got {n_classes}")
-        if n_classes - 1 > 32:
-            raise DataError(f"C = {n_classes} classes: the sparse path supports C <= 33")
+        if n_classes - 1 > 1 << 16:
+            raise DataError(f"C = {n_classes} classes: too many for the sparse path")
         self.indptr, self.indices, self.data = indptr, indices, data
         self.colptr, self.rowidx, self.cdata = colptr, rowidx, cdata
         self.labels = labels

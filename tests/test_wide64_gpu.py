@@ -116,3 +116,49 @@ def test_f32_wide_probabilities():
     rs = snx.row_stats(ds, x)
     assert rel_err(rs.sum_exp_part, E.sum(axis=1)) <= 1e-12
     assert rel_err(rs.linear_part, lin) <= 1e-12
+
+
+@pytest.mark.parametrize("C", [40, 150])
+def test_csr_wide_classes(C):
+    """CSR storage with C > 33 (the wide row kernels behind a warp-per-row CSR
+    logits pass and a warp-per-column CSC X^T R pass): objective, gradient,
+    accuracy, probabilities, the sampled product (with duplicate rows), CG and
+    a short Newton trajectory against the oracle on the dense matrix."""
+    import scipy.sparse as sp
+
+    from paper_1802_09113_b200.sparse import CsrDataset
+
+    n, p, lam = 900, 120, 1e-3
+    rng = np.random.default_rng(C)
+    As = sp.random(n, p, density=0.08, format="csr", random_state=C)
+    A = As.toarray()
+    y = rng.integers(0, C, size=n)
+    x = 0.3 * rng.standard_normal((C - 1) * p)
+    v = rng.standard_normal((C - 1) * p)
+    ds = CsrDataset.from_scipy(As, y, C)
+    prob = snx.SoftmaxProblem(ds, lam)
+    f_ref = oracle.loss(A, y, C, x, lam)
+    assert abs(snx.objective(prob, x) - f_ref) <= 1e-10 * abs(f_ref)
+    assert rel_err(snx.gradient(prob, x), oracle.grad(A, y, C, x, lam)) <= 1e-10
+    assert snx.accuracy(ds, x) == oracle.accuracy(A, y, C, x)
+    assert rel_err(snx.class_probabilities(ds, x), oracle.class_probs(A, y, C, x)) <= 1e-12
+    orc = snx.SubsampledOracle(prob, snx.SampleConfig(1.0, 0.3, True, 7), 1)
+    s_h = orc.s_h
+    assert len(np.unique(s_h)) < len(s_h)  # duplicates
+    h = oracle.hess_probs(A[s_h], y[s_h], C, x)
+    scale = n / len(s_h)
+    op = orc.hessian_operator(x)
+    assert rel_err(op.apply(v), oracle.hess_apply(A[s_h], h, C, v, scale, lam)) <= 1e-10
+    g = oracle.grad(A, y, C, x, lam)
+    rep = snx.cg_solve(op, g, snx.CgConfig(1e-6, 6))
+    p_ref, _, it_ref, conv_ref = oracle.cg(
+        lambda u: oracle.hess_apply(A[s_h], h, C, u, scale, lam), g, 1e-6, 6)
+    assert rep.iterations == it_ref and rep.converged == conv_ref
+    assert rel_err(rep.solution, p_ref) <= 1e-9
+    ref = oracle.newton_solve(A, y, C, lam, "subsampled-100", max_outer_iters=3)
+    tr = snx.newton_solve(prob, snx.make_variant("subsampled-100",
+                                                 snx.NewtonConfig(max_outer_iters=3)))
+    for r, (k, f, acc, _, alpha, it) in zip(tr.records, ref["records"]):
+        assert abs(r.objective - f) <= 1e-10 * abs(f), k
+        assert r.step_size == alpha and r.cg_iters == it, k
+    assert rel_err(tr.x_final, ref["x"]) <= 1e-9
