@@ -651,10 +651,11 @@ __device__ __forceinline__ void rows_block(const Args &a, const Ring &rg, const 
     for (int j = 0; j < 3; ++j) E[j] = (sub + 4 * j < K) ? exp(z[j] - M) : 0.0;
     const double eM = exp(-M);
     const double alpha = eM + gsum<4>((E[0] + E[1]) + E[2]);
+    const double ia = 1.0 / alpha;  // one division per lane (alpha >= 1 for finite rows)
     if (prep) {
 #pragma unroll
       for (int j = 0; j < 3; ++j)
-        if (rv && sub + 4 * j < K && q == 0) a.hout[(r0 + row) * K + sub + 4 * j] = E[j] / alpha;
+        if (rv && sub + 4 * j < K && q == 0) a.hout[(r0 + row) * K + sub + 4 * j] = E[j] * ia;
     } else {
       // grad: residual (softmax.py:157-161), loss (:134), accuracy (:224-247)
       const int y = rv ? reinterpret_cast<const int *>(rg.side)[s * R + row] : -1;
@@ -662,7 +663,7 @@ __device__ __forceinline__ void rows_block(const Args &a, const Ring &rg, const 
 #pragma unroll
       for (int j = 0; j < 3; ++j) {
         const int c = sub + 4 * j;
-        pr[j] = E[j] / alpha;
+        pr[j] = E[j] * ia;
         uo[j] = pr[j] - (c == y ? 1.0 : 0.0);
         if (c < K && c == y) lin = z[j];
       }
@@ -674,7 +675,7 @@ __device__ __forceinline__ void rows_block(const Args &a, const Ring &rg, const 
       for (int j = 0; j < 3; ++j)
         if (sub + 4 * j < K) amax_take(bv, bi, pr[j], sub + 4 * j);
       gargmax<4>(bv, bi);
-      amax_take(bv, bi, eM / alpha, K);  // the reference class
+      amax_take(bv, bi, eM * ia, K);  // the reference class
       if (rv && sub == 0 && q == 0 && bi == y) corr_acc += 1ull;
     }
   }
@@ -1071,17 +1072,18 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
         const double E8 = K == 9 ? exp(z8 - M) : 0.0;
         const double eM = exp(-M);
         const double alpha = eM + (gsum<4>(E0 + E1) + E8);
+        const double ia = 1.0 / alpha;  // one division per lane
         if (prep) {
           if (rv) {
             double *ho = a.hout + (r0 + row) * K;
-            if (c0v) ho[2 * t] = E0 / alpha;
-            if (c1v) ho[2 * t + 1] = E1 / alpha;
-            if (K == 9 && t == 0) ho[K == 9 ? 8 : 0] = E8 / alpha;
+            if (c0v) ho[2 * t] = E0 * ia;
+            if (c1v) ho[2 * t + 1] = E1 * ia;
+            if (K == 9 && t == 0) ho[K == 9 ? 8 : 0] = E8 * ia;
           }
         } else {
           // grad: residual (softmax.py:157-161), loss (:134), accuracy (:224-247)
           const int y = rv ? reinterpret_cast<const int *>(rg.side)[s * R + row] : -1;
-          const double p0 = E0 / alpha, p1 = E1 / alpha, p8 = E8 / alpha;
+          const double p0 = E0 * ia, p1 = E1 * ia, p8 = E8 * ia;
           u0 = p0 - (2 * t == y ? 1.0 : 0.0);
           u1 = p1 - (2 * t + 1 == y ? 1.0 : 0.0);
           u8 = p8 - (y == 8 ? 1.0 : 0.0);
@@ -1095,7 +1097,7 @@ __global__ void __launch_bounds__(kNTR, 1) rowsplit_kernel(const __grid_constant
           if (c1v) amax_take(bv, bi, p1, 2 * t + 1);
           gargmax<4>(bv, bi);
           if (K == 9) amax_take(bv, bi, p8, 8);
-          amax_take(bv, bi, eM / alpha, K);
+          amax_take(bv, bi, eM * ia, K);
           if (rv && t == 0 && bi == y) corr_acc += 1ull;
         }
       }
